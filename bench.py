@@ -1,0 +1,408 @@
+"""bench.py -- exponential-Euler throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+One "step" = one exponential-Euler step (integrator.cpp:52-63) of the configured
+workload (default C4: 256^3 fp64 shell phantom, the headline config).  Our arm runs the
+CUDA path with all state resident in HBM; the reported ``value`` is whole-job steps/s
+(N independent replicas under torchrun: the path does not shard, DESIGN.md "replicas
+only").  ``e2e`` is the same metric through the drop-in step() call with host buffers
+(pinned H2D of u, the step, D2H of the new u every step).  ``roofline`` covers the
+persistent solve kernel (the only kernel in the timed region) against the measured HBM
+copy peak; ``cpu_baseline`` is the UNMODIFIED reference (oracle/_ref) timed on this
+host on a bounded slab sample.  ``--impl reference`` times that reference alone.
+
+Working set at C4: u, b, f x2, T x2 = 6 x 128 MiB fp64 (+ 16 MiB labels) >> 126 MB L2,
+so no L2 flush is needed between steps ("inputs larger than L2").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_TERM = 33   # per voxel per Taylor term: T 8 + f 8 + label 1 read, T 8 + f 8 write
+BYTES_PER_STEP = 49   # per voxel per step outside the terms: RHS 17, bordered column 8, update 24
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work for the baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/gs_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            return None
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for nm, val in zip(names, r[4:8]):
+                    if val.strip() == "Active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_case(w, member=0):
+    """Host inputs for a workload: intensity bytes, labels (for the CPU side), u0 pieces."""
+    from paper_2402_02273_b200 import workloads as W
+    data, wd, ht, sl = W.intensity(w, member)
+    table = W.classify_table()
+    if w.stack_slices:
+        from paper_2402_02273_b200 import phantom  # noqa: F401
+        # labels come from the device resample; the CPU side gets them back from the GPU
+        labels = None
+    else:
+        labels = table[data]
+    return data, (wd, ht, sl), labels
+
+
+def make_operator(w, data, dims):
+    from paper_2402_02273_b200 import gliosim as G
+    from paper_2402_02273_b200 import workloads as W
+    cfg = G.SimConfig(d_white=W.D_WHITE, d_gray=W.D_GRAY)
+    return G.StencilOperator.from_intensity(G.Grid(w.nx, w.ny, w.nz, w.h), data, dims[0], dims[1], dims[2], cfg)
+
+
+def initial_state(w, op, labels):
+    from paper_2402_02273_b200 import gliosim as G
+    from paper_2402_02273_b200 import workloads as W
+    u = None
+    for c in W.seed_points(w, labels):
+        cfg = G.SimConfig(seed_center=c, seed_amplitude=1.0, seed_width=W.seed_width(w))
+        ui = G.seed_initial(op, cfg, mask=True)
+        u = ui if u is None else np.maximum(u, ui)
+    return u
+
+
+# ------------------------------------------------------------------------------------------
+# CPU side: the unmodified reference on a bounded slab sample
+# ------------------------------------------------------------------------------------------
+
+def slab_of(w, labels, u0, depth):
+    """A z-slab of `depth` planes centred on the seed plane (same phantom, same physics)."""
+    nxy = w.nx * w.ny
+    kz = int(np.argmax(u0.reshape(w.nz, nxy).max(axis=1)))
+    z0 = max(0, min(w.nz - depth, kz - depth // 2))
+    sl = slice(z0 * nxy, (z0 + depth) * nxy)
+    return labels[sl].copy(), u0[sl].copy()
+
+
+def cpu_reference_sample(w, labels, u0, target_s, steps=None, warmup=0, gpu_terms_of=None):
+    """Time the reference's own run() loop (RunTimings::step_seconds, integrator.cpp:123-125)
+    on a slab with workers = all host cores; the C port stands in only if oracle/_ref is
+    absent.  `steps` fixed -> exactly that many timed steps after `warmup` untimed ones;
+    otherwise as many as fit in ~target_s seconds."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Port
+    try:
+        from oracle import Ref
+        ref = Ref()
+        kind = "reference"
+    except Exception:
+        ref = None
+        kind = "port"
+    from paper_2402_02273_b200 import workloads as W
+    cores = os.cpu_count() or 1
+    depth = w.nz if w.n <= 128 ** 3 else 16
+    lab_s, u_s = slab_of(w, labels, u0, depth)
+    shape = (w.nx, w.ny, depth)
+    d_s = np.array([0.0, W.D_WHITE, W.D_GRAY, 0.0])[lab_s]
+    center = (0.0, 0.0, 0.0)
+    port = Port()
+    op_p = port.stencil(shape, w.h, d_s)
+
+    def timed(u, k):
+        if k <= 0:
+            return u, 0.0
+        if ref:
+            u2, _, secs = ref.run(shape, w.h, d_s, u, k, w.rho, W.T0, W.T0 + k * W.TAU, W.TOL, center,
+                                  workers=cores)
+            return u2, secs
+        t0 = time.perf_counter()
+        u2, _, _ = port.run(op_p, u, k, w.rho, W.TAU, W.TOL, center)
+        return u2, time.perf_counter() - t0
+
+    u, _ = timed(u_s, warmup)
+    if steps is None:
+        _, t1 = timed(u, 1)
+        steps = max(1, min(50, int(target_s / max(t1, 1e-6))))
+    u_end, secs = timed(u, steps)
+    terms = gpu_terms_of(shape, lab_s, u_s, steps + warmup) if gpu_terms_of else None
+    return {"kind": kind, "cores": cores if kind == "reference" else 1, "n_slab": lab_s.size,
+            "slab_shape": shape, "step_times": [secs / steps] * steps, "steps": steps, "terms_slab": terms}
+
+
+def extrapolate(sample, n_full):
+    """Full-grid steps/s from slab timings, scaled by voxel count (the reference's step
+    cost is linear in voxels x Taylor terms; the slab has the same (s, m) -- ||A||_1 is
+    set by interior white matter -- and its terms per step are reported alongside)."""
+    t = float(np.mean(sample["step_times"]))
+    full = t * n_full / sample["n_slab"]
+    return 1.0 / full, full
+
+
+# ------------------------------------------------------------------------------------------
+# arms
+# ------------------------------------------------------------------------------------------
+
+def run_ours(args, w, rank, world, local):
+    import torch
+    from paper_2402_02273_b200 import gliosim as G
+    from paper_2402_02273_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as D
+        D.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = D
+
+    data, dims, labels = build_case(w)
+    op = make_operator(w, data, dims)
+    if labels is None:
+        labels = op.labels()
+    u0 = initial_state(w, op, labels)
+    stream = torch.cuda.ExternalStream(op.stream_handle())
+    peak, peak_kind = measured_peak()
+
+    # warm-up (untimed): W steps
+    op.set_state(u0)
+    op.run_resident(args.warmup, w.rho, w.tau, W.TOL, metrics=False, infos=False)
+    op.set_state(u0)
+    torch.cuda.synchronize()
+
+    # timed: exactly K steps, one persistent launch, device-timed on the launching stream
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        metrics, infos = op.run_resident(args.steps, w.rho, w.tau, W.TOL, (0, 0, 0), (0, 0, 0), 0.1,
+                                         metrics=True, infos=True)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    terms = [infos[q].total_terms for q in range(args.steps)]
+    sm = [(infos[q].s, infos[q].m) for q in range(args.steps)]
+    ms_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+    alg_bytes = w.n * (BYTES_PER_TERM * sum(terms) + BYTES_PER_STEP * args.steps)
+    achieved = alg_bytes / (ms / 1e3) / 1e9
+
+    # e2e through the drop-in step() with host buffers (pinned H2D + step + D2H)
+    e2e = None
+    if not args.no_e2e:
+        import ctypes as C
+        from paper_2402_02273_b200 import _native as N
+        pin_in = torch.empty(w.n, dtype=torch.float64, pin_memory=True)
+        pin_out = torch.empty(w.n, dtype=torch.float64, pin_memory=True)
+        pin_in.numpy()[:] = u0
+        lib = op.lib
+        info = N.GsStepInfo()
+        k_e2e = max(1, min(args.steps, 5))
+        for _ in range(1):
+            rc = lib.gs_step_host(op.ctx, pin_in.numpy(), w.rho, w.tau, W.TOL, pin_out.numpy(), C.byref(info))
+            assert rc == 0
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        src, dst = pin_in, pin_out
+        for _ in range(k_e2e):
+            rc = lib.gs_step_host(op.ctx, src.numpy(), w.rho, w.tau, W.TOL, dst.numpy(), C.byref(info))
+            assert rc == 0
+            src, dst = dst, src
+        dt = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": world * k_e2e / dt, "unit": "steps/s", "h2d_bytes_per_step": 8 * w.n,
+               "d2h_bytes_per_step": 8 * w.n, "api": "gs_step_host (drop-in step(): u H2D from pinned, u' D2H)",
+               "steps": k_e2e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        def gpu_terms_of(shape, lab_s, u_s, k):
+            g = G.Grid(*shape, h=w.h)
+            with G.StencilOperator.from_labels(g, lab_s) as ops:
+                ops.set_state(u_s)
+                _, inf = ops.run_resident(k, w.rho, w.tau, W.TOL, metrics=False, infos=True)
+                return [inf[q].total_terms for q in range(k)]
+        try:
+            sample = cpu_reference_sample(w, labels, u0, args.cpu_seconds, gpu_terms_of=gpu_terms_of)
+            v, full_s = extrapolate(sample, w.n)
+            cpu = {"value": v, "unit": "steps/s", "cores": sample["cores"], "kind": sample["kind"],
+                   "sample": (f"{len(sample['step_times'])} gliosim::step calls (workers={sample['cores']}) on a "
+                              f"{sample['slab_shape'][0]}x{sample['slab_shape'][1]}x{sample['slab_shape'][2]} z-slab "
+                              f"of the same phantom through the seed; mean {np.mean(sample['step_times']):.3f} s/step, "
+                              f"extrapolated by voxel count to {full_s:.1f} s per {w.nx}x{w.ny}x{w.nz} step; slab Taylor "
+                              f"terms/step {np.mean(sample['terms_slab']) if sample['terms_slab'] else float('nan'):.1f} "
+                              f"vs full grid {np.mean(terms):.1f}")}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "unavailable",
+                   "sample": f"failed: {e}"}
+
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(w.name)
+            if tr:
+                # dram bytes per step from the committed ncu capture, per launch of K steps
+                traffic = tr["dram_bytes_per_step"] * args.steps
+    except Exception:
+        pass
+
+    line = {
+        "metric": "expEuler steps/s at 256^3 fp64" if w.name.startswith("C4") else f"expEuler steps/s ({w.name})",
+        "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded shell phantom, BASELINE.json config)",
+        "config": {"workload": f"{w.name}: {w.note}", "grid": [w.nx, w.ny, w.nz], "h_mm": w.h, "rho": w.rho,
+                   "tau_days": w.tau, "tol": W.TOL, "sigma_vox": w.sigma_vox,
+                   "parallelism": f"replicas x{world} (path does not shard)",
+                   "l2": "working set 6x128 MiB fp64 > 126 MB L2 (no flush needed)",
+                   "s_m": sorted(set(sm)), "terms_per_step": float(np.mean(terms))},
+        "taylor_terms_per_s": world * sum(terms) / (ms / 1e3),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "gs::solve_kernel (persistent, 1 launch per K steps)",
+                     "algorithmic_bytes": f"N*(33*terms + 49) per step; {alg_bytes / 1e9:.2f} GB per launch"},
+        "gpu_launches": 1,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    op.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_reference(args, w, rank, world, local):
+    if rank != 0:
+        return
+    from paper_2402_02273_b200 import workloads as W
+    data, dims, labels = build_case(w)
+    if labels is None:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from oracle import Port
+        labels = Port().resample(data, dims[0], dims[1], dims[2], (w.nx, w.ny, w.nz))
+    # u0 with the reference's own seed_initial (libm), max over seeds
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Port
+    port = Port()
+    d = np.array([0.0, W.D_WHITE, W.D_GRAY, 0.0])[labels]
+    u0 = None
+    for c in W.seed_points(w, labels):
+        ui = port.seed_initial((w.nx, w.ny, w.nz), w.h, 1.0, W.seed_width(w), c, d)
+        u0 = ui if u0 is None else np.maximum(u0, ui)
+    # Taylor-term counts of the full grid for the extrapolation come from the oracle's log
+    # of the first slab step ratio; without a GPU we scale by voxels only.
+    sample = cpu_reference_sample(w, labels, u0, args.cpu_seconds, steps=args.steps, warmup=args.warmup)
+    v, full_s = extrapolate(sample, w.n)
+    line = {
+        "impl": "reference", "metric": "expEuler steps/s at 256^3 fp64" if w.name.startswith("C4") else
+        f"expEuler steps/s ({w.name})", "value": v, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * full_s, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded shell phantom, BASELINE.json config)",
+        "config": {"workload": f"{w.name}: {w.note}", "grid": [w.nx, w.ny, w.nz], "parallelism": "CPU threads"},
+        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": sample["cores"], "kind": sample["kind"],
+                         "sample": (f"{args.steps} timed gliosim::step calls (+{args.warmup} warm-up) on a "
+                                    f"{sample['slab_shape'][0]}x{sample['slab_shape'][1]}x{sample['slab_shape'][2]} "
+                                    f"z-slab, extrapolated by voxel count to {w.nx}x{w.ny}x{w.nz}")},
+        "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    from paper_2402_02273_b200 import workloads as W
+    w = W.get(args.config)
+    if args.impl == "reference":
+        run_reference(args, w, rank, world, local)
+    else:
+        run_ours(args, w, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,129 @@
+/*
+ * gliosim_b200.h -- C-ABI of the B200-native exponential-Euler hot path.
+ *
+ * Drop-in boundary for the reference gliosim library (/root/reference/proj).  Every
+ * entry point names the reference interface it replaces (file:line, paths relative to
+ * /root/reference/proj).  Plain pointers and sizes only; host buffers are
+ * caller-owned, device memory belongs to the context.  One context = one grid
+ * operator + one CUDA stream; a context is not thread-safe (use one per thread),
+ * matching the reference's caller-single-threaded API (sparse.hpp:27-29).
+ *
+ * Errors: every call returns a gs_status.  The codes map 1:1 onto the reference's
+ * exception types (errors.hpp:10-17, std::invalid_argument); gs_last_error() returns
+ * the reference's message text for the failing call.  There is no CPU fallback: a
+ * missing or failing GPU returns GS_ECUDA.
+ */
+#ifndef GLIOSIM_B200_H
+#define GLIOSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum gs_status {
+    GS_OK = 0,
+    GS_EINVAL = 1,   /* std::invalid_argument */
+    GS_ENUMERIC = 2, /* gliosim::numeric_error */
+    GS_EDATA = 3,    /* gliosim::data_error */
+    GS_ECUDA = 4     /* device / driver failure (no reference analogue) */
+} gs_status;
+
+#define GS_MAX_LOGGED_STAGES 256
+
+/* What one exponential-Euler step (or phi1v / expmv) did.  The reference exposes none
+ * of this; it is the parity log ((s,m) and terms-per-stage must match). */
+typedef struct gs_step_info {
+    int32_t s, m;            /* select_params result (expact.cpp:29-61) */
+    int32_t branch;          /* 0 Taylor, 1 t == 0, 2 ||b||_1 == 0, 3 small-norm (expact.cpp:108-122) */
+    int32_t pad;
+    int64_t total_terms;     /* Taylor terms = operator applications inside expmv */
+    int32_t terms[GS_MAX_LOGGED_STAGES]; /* terms used per stage (expact.cpp:81-95) */
+    double bnorm;            /* ||b||_1 (expact.cpp:110), device tree-reduced */
+    double anorm;            /* ||A||_1 (sparse.cpp:36-40), exact */
+    double coln;             /* bordered column sum sum|b_i/gamma| (sparse.cpp:36-38 on the bordered CSR) */
+    double gamma;            /* bnorm / anorm (expact.cpp:126) */
+    double norm_tA;          /* |t| * ||A_bordered||_1 fed to select_params */
+} gs_step_info;
+
+/* StepMetrics (integrator.hpp:30-37) minus step/time, which the caller knows. */
+typedef struct gs_metrics {
+    double total_mass, max_density, min_density, radius;
+} gs_metrics;
+
+typedef struct gs_ctx gs_ctx;
+
+/* ---- context: one regular grid (Grid, grid.hpp:14-51) ------------------------------ */
+/* Replaces the SparseOperator that assemble_diffusion (stencil.hpp:20, stencil.cpp:5-43)
+ * builds: the operator stays matrix-free on the device.  Validation and messages follow
+ * Grid's constructor (grid.hpp:24-29). */
+gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device);
+void gs_destroy(gs_ctx* ctx);
+/* Message of the last failing call on ctx (or of the last failed gs_create when ctx is NULL). */
+const char* gs_last_error(const gs_ctx* ctx);
+/* Number of voxels nx*ny*nz (Grid::num_points, grid.hpp:31-33). */
+int64_t gs_num_points(const gs_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t), for callers that time or order work on it. */
+void* gs_stream(gs_ctx* ctx);
+
+/* ---- material map (K1) ------------------------------------------------------------ */
+/* resample + classify (imaging.cpp:65-72, 118-141) on the device from a uint8 stack
+ * (x-fastest, x + y*w + z*w*hgt, imaging.hpp:21-25), then the D table of
+ * diffusion_from_materials (imaging.cpp:143-153).  Thresholds as SimConfig
+ * (config.hpp:40-43). */
+gs_status gs_set_intensity(gs_ctx* ctx, const uint8_t* stack, int w, int hgt, int slices, int t_air,
+                           int t_white, int t_gray, double d_white, double d_gray);
+/* MaterialVolume labels (0 Air, 1 White, 2 Gray, 3 Skull; fields.hpp:13-18) ->
+ * diffusion_from_materials (imaging.cpp:143-153). */
+gs_status gs_set_labels(gs_ctx* ctx, const uint8_t* labels, double d_white, double d_gray);
+/* Arbitrary DiffusionField (fields.hpp:51-60) for assemble_diffusion (stencil.cpp:5-43). */
+gs_status gs_set_diffusion(gs_ctx* ctx, const double* d);
+/* Copy back the device material labels (valid after gs_set_intensity / gs_set_labels). */
+gs_status gs_get_labels(gs_ctx* ctx, uint8_t* labels);
+/* Copy back the per-voxel D(x) the operator uses. */
+gs_status gs_get_diffusion(gs_ctx* ctx, double* d);
+
+/* ---- operator ---------------------------------------------------------------------- */
+/* SparseOperator::one_norm (sparse.hpp:22, sparse.cpp:36-40): exact max column sum. */
+gs_status gs_one_norm(gs_ctx* ctx, double* out);
+/* SparseOperator::apply (sparse.hpp:29, sparse.cpp:43-76): y = A x, host buffers. */
+gs_status gs_apply(gs_ctx* ctx, const double* x, double* y);
+
+/* ---- state ------------------------------------------------------------------------- */
+gs_status gs_set_state(gs_ctx* ctx, const double* u);
+gs_status gs_get_state(gs_ctx* ctx, double* u);
+/* Device pointer of the resident state u (N doubles), for zero-copy callers. */
+double* gs_state_device_ptr(gs_ctx* ctx);
+
+/* ---- exponential action / integrator ------------------------------------------------ */
+/* select_params (expact.hpp:42, expact.cpp:29-61). */
+gs_status gs_select_params(double norm_tA, double tol, int* s, int* m);
+/* expmv (expact.hpp:45-46, expact.cpp:63-99) with A = this grid's operator. */
+gs_status gs_expmv(gs_ctx* ctx, double t, const double* b, double tol, double* out, gs_step_info* info);
+/* phi1v (expact.hpp:49-50, expact.cpp:101-153). */
+gs_status gs_phi1v(gs_ctx* ctx, double t, const double* b, double tol, double* out, gs_step_info* info);
+/* step (integrator.hpp:59-60, integrator.cpp:52-63) on the RESIDENT state: u <- step(A, u). */
+gs_status gs_step(gs_ctx* ctx, double rho, double tau, double tol, gs_step_info* info);
+/* step with host vectors, value semantics as the reference (u in, out returned). */
+gs_status gs_step_host(gs_ctx* ctx, const double* u, double rho, double tau, double tol, double* out,
+                       gs_step_info* info);
+/* The time loop of run (integrator.cpp:91-138) on the resident state: n_steps steps,
+ * compute_metrics (integrator.cpp:65-89) at every node.  metrics: n_steps+1 records
+ * (node 0 = the state on entry) or NULL; infos: n_steps records or NULL.  One device
+ * launch for the whole loop. */
+gs_status gs_run(gs_ctx* ctx, int n_steps, double rho, double tau, double tol, const double origin[3],
+                 const double seed_center[3], double front_threshold, gs_metrics* metrics,
+                 gs_step_info* infos);
+
+/* ---- host helpers with libm parity --------------------------------------------------- */
+/* seed_initial (integrator.cpp:32-50): u = amplitude*exp(-width*|x-c|^2), zero where the
+ * context's D is 0 when mask != 0.  Host libm, so u0 is bit-identical to the reference. */
+gs_status gs_seed_initial(gs_ctx* ctx, const double origin[3], double amplitude, double width,
+                          const double center[3], int mask, double* u);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,619 @@
+// gs_capi.cu -- host side of the C-ABI (include/gliosim_b200.h).
+//
+// Owns the device state of one grid operator and drives the kernels of gs_kernels.cu.
+// The host does exactly the libm-dependent scalar work the reference does with glibc
+// (r_m of select_params, expact.cpp:47-48; the Gaussian seed, integrator.cpp:40-41) so
+// those values are bit-identical; everything per-voxel runs on the GPU.  No CPU
+// fallback exists: without a device every entry point returns GS_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gliosim_b200.h"
+#include "gs_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t alloc(size_t b) {
+        if (bytes >= b && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e == cudaSuccess) bytes = b;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct gs_ctx {
+    int device = 0;
+    int nx = 0, ny = 0, nz = 0;
+    double h = 1.0;
+    int64_t n = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 0;
+    int capacity = 0;  // co-resident CTAs of solve_kernel
+
+    // operator
+    DevBuf pal, dvox, wtab, dtab;   // palette indices, fp64 D (fallback), w table, D table
+    bool has_operator = false;
+    bool palette_mode = true;
+    bool has_labels = false;        // pal holds Material codes (0..3)
+    std::vector<double> dtab_host;  // palette D values
+    double anorm = 0.0;
+    bool anorm_valid = false;
+
+    // vectors
+    DevBuf u, g, f0, f1, t0, t1, out;
+    // scratch
+    DevBuf part_b, part_c, part_u, slots, mslots, status, metrics, infos, normbits;
+
+    gs::StencilOp op{};
+    int grid_blocks = 0;
+    std::string err;
+};
+
+namespace {
+
+gs_status fail(gs_ctx* c, gs_status code, const std::string& msg) {
+    if (c) c->err = msg;
+    else g_create_error = msg;
+    return code;
+}
+
+gs_status cuda_fail(gs_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, GS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define GS_CUDA(ctx, call)                                  \
+    do {                                                    \
+        cudaError_t e_ = (call);                            \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+// Pick the z-chunk so the items spread evenly over the co-resident CTAs (balance first,
+// then the longest chunk for z-reuse along each column).
+void plan_items(gs_ctx* c) {
+    gs::StencilOp& op = c->op;
+    op.tiles_x = (c->nx + gs::kTX - 1) / gs::kTX;
+    op.tiles_y = (c->ny + gs::kTY - 1) / gs::kTY;
+    const int64_t tiles = static_cast<int64_t>(op.tiles_x) * op.tiles_y;
+    const int cap = std::max(1, c->capacity);
+    int best_zc = 1;
+    double best_score = -1.0;
+    for (int zc = 1; zc <= c->nz; ++zc) {
+        const int64_t chunks = (c->nz + zc - 1) / zc;
+        const int64_t items = tiles * chunks;
+        const int64_t grid = std::min<int64_t>(items, cap);
+        const int64_t rounds = (items + grid - 1) / grid;
+        // work per CTA ~ planes; imbalance from ragged last chunk and last round
+        const double work = static_cast<double>(tiles) * c->nz;
+        const double span = static_cast<double>(rounds) * zc;  // planes per CTA (critical path)
+        const double eff = work / (static_cast<double>(grid) * span);
+        const double halo = 2.0 / (zc + 2.0);  // extra plane loads per chunk
+        const double score = eff * (1.0 - 0.5 * halo);
+        if (score > best_score + 1e-9) {
+            best_score = score;
+            best_zc = zc;
+        }
+    }
+    op.zc = best_zc;
+    op.chunks_z = (c->nz + best_zc - 1) / best_zc;
+    op.n_items = tiles * op.chunks_z;
+    c->grid_blocks = static_cast<int>(std::min<int64_t>(op.n_items, cap));
+}
+
+gs_status ensure_operator(gs_ctx* c) {
+    if (!c->has_operator)
+        return fail(c, GS_EINVAL, "operator not set: call gs_set_labels, gs_set_intensity or gs_set_diffusion");
+    return GS_OK;
+}
+
+void fill_op(gs_ctx* c) {
+    gs::StencilOp& op = c->op;
+    op.nx = c->nx;
+    op.ny = c->ny;
+    op.nz = c->nz;
+    op.n = c->n;
+    op.sy = c->nx;
+    op.sz = static_cast<int64_t>(c->nx) * c->ny;
+    op.inv_h2 = 1.0 / (c->h * c->h);  // stencil.cpp:8
+    op.pal = c->palette_mode ? c->pal.as<uint8_t>() : nullptr;
+    op.dvox = c->palette_mode ? nullptr : c->dvox.as<double>();
+    op.wtab = c->wtab.as<double>();
+}
+
+// w table from palette D values: w = D * (1/(h*h)) exactly as stencil.cpp:8,23.
+gs_status upload_palette(gs_ctx* c, const std::vector<double>& dvals) {
+    std::vector<double> w(256, 0.0), d(256, 0.0);
+    const double inv_h2 = 1.0 / (c->h * c->h);
+    for (size_t k = 0; k < dvals.size(); ++k) {
+        d[k] = dvals[k];
+        w[k] = dvals[k] != 0.0 ? dvals[k] * inv_h2 : 0.0;
+        if (dvals[k] != 0.0 && w[k] == 0.0)
+            return fail(c, GS_EINVAL, "diffusion coefficient underflows D/h^2");
+    }
+    c->dtab_host = d;
+    GS_CUDA(c, c->wtab.alloc(256 * sizeof(double)));
+    GS_CUDA(c, c->dtab.alloc(256 * sizeof(double)));
+    GS_CUDA(c, cudaMemcpyAsync(c->wtab.p, w.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    GS_CUDA(c, cudaMemcpyAsync(c->dtab.p, d.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    return GS_OK;
+}
+
+gs_status compute_anorm(gs_ctx* c) {
+    GS_CUDA(c, c->normbits.alloc(sizeof(unsigned long long)));
+    GS_CUDA(c, cudaMemsetAsync(c->normbits.p, 0, sizeof(unsigned long long), c->stream));
+    const int blocks = static_cast<int>(std::min<int64_t>((c->n + 255) / 256, 148 * 8));
+    gs::colsum_norm_kernel<<<std::max(1, blocks), 256, 0, c->stream>>>(c->op, c->normbits.as<unsigned long long>());
+    GS_CUDA(c, cudaGetLastError());
+    unsigned long long bits = 0;
+    GS_CUDA(c, cudaMemcpyAsync(&bits, c->normbits.p, sizeof bits, cudaMemcpyDeviceToHost, c->stream));
+    GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    double v;
+    std::memcpy(&v, &bits, sizeof v);
+    c->anorm = v;
+    c->anorm_valid = true;
+    return GS_OK;
+}
+
+gs_status operator_ready(gs_ctx* c) {
+    c->has_operator = true;
+    c->anorm_valid = false;
+    fill_op(c);
+    return compute_anorm(c);
+}
+
+// r_m for m = 1..55 with glibc, exactly expact.cpp:47-48.
+void fill_rtab(double tol, double* rtab) {
+    rtab[0] = 0.0;
+    for (int m = 1; m <= gs::kMaxDegree; ++m) {
+        double r = std::exp((std::log(tol) + std::lgamma(m + 2.0)) / (m + 1.0));
+        rtab[m] = (6.0 < r) ? 6.0 : r;  // std::min(r, r_cap)
+    }
+}
+
+gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* metrics, gs_step_info* infos) {
+    const int gb = c->grid_blocks;
+    GS_CUDA(c, c->part_b.alloc(sizeof(double) * gb));
+    GS_CUDA(c, c->part_c.alloc(sizeof(double) * gb));
+    GS_CUDA(c, c->part_u.alloc(sizeof(double) * gb));
+    GS_CUDA(c, c->slots.alloc(sizeof(unsigned long long) * 12));
+    GS_CUDA(c, c->mslots.alloc(sizeof(unsigned long long) * 8));
+    GS_CUDA(c, c->status.alloc(sizeof(int) * 2));
+    GS_CUDA(c, cudaMemsetAsync(c->slots.p, 0, sizeof(unsigned long long) * 12, c->stream));
+    const unsigned long long ms_init[8] = {0ull, ~0ull, 0ull, 0ull, 0ull, ~0ull, 0ull, 0ull};
+    GS_CUDA(c, cudaMemcpyAsync(c->mslots.p, ms_init, sizeof ms_init, cudaMemcpyHostToDevice, c->stream));
+    GS_CUDA(c, cudaMemsetAsync(c->status.p, 0, sizeof(int) * 2, c->stream));
+    if (metrics) GS_CUDA(c, c->metrics.alloc(sizeof(double) * 4 * (n_steps + 1)));
+    if (infos) {
+        GS_CUDA(c, c->infos.alloc(sizeof(gs_step_info) * std::max(1, n_steps)));
+        GS_CUDA(c, cudaMemsetAsync(c->infos.p, 0, sizeof(gs_step_info) * std::max(1, n_steps), c->stream));
+    }
+    p.op = c->op;
+    p.grid_blocks = gb;
+    p.anorm = c->anorm;
+    p.metrics = metrics ? c->metrics.as<double>() : nullptr;
+    p.want_metrics = metrics ? 1 : 0;
+    p.infos = infos ? c->infos.as<gs_step_info>() : nullptr;
+    p.part_b = c->part_b.as<double>();
+    p.part_c = c->part_c.as<double>();
+    p.part_u = c->part_u.as<double>();
+    p.slots = c->slots.as<unsigned long long>();
+    p.mslots = c->mslots.as<unsigned long long>();
+    p.status = c->status.as<int>();
+    p.u = c->u.as<double>();
+    p.g = c->g.as<double>();
+    p.f[0] = c->f0.as<double>();
+    p.f[1] = c->f1.as<double>();
+    p.t[0] = c->t0.as<double>();
+    p.t[1] = c->t1.as<double>();
+    p.out = c->out.as<double>();
+    void* args[] = {&p};
+    GS_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gs::solve_kernel), dim3(gb), dim3(gs::kThreads),
+                                           args, 0, c->stream));
+    int status[2] = {0, 0};
+    GS_CUDA(c, cudaMemcpyAsync(status, c->status.p, sizeof status, cudaMemcpyDeviceToHost, c->stream));
+    if (metrics)
+        GS_CUDA(c, cudaMemcpyAsync(metrics, c->metrics.p, sizeof(double) * 4 * (n_steps + 1), cudaMemcpyDeviceToHost,
+                                   c->stream));
+    if (infos)
+        GS_CUDA(c, cudaMemcpyAsync(infos, c->infos.p, sizeof(gs_step_info) * std::max(1, n_steps),
+                                   cudaMemcpyDeviceToHost, c->stream));
+    GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (status[0] != GS_OK) {
+        if (status[1] == 2) return fail(c, GS_ENUMERIC, "expmv: series diverged to non-finite values; reduce t");
+        if (status[0] == GS_EINVAL)
+            return fail(c, GS_EINVAL, "select_params: operator norm must be finite and nonnegative");
+        return fail(c, GS_ENUMERIC, "select_params: scaled operator norm too large for any stage count");
+    }
+    return GS_OK;
+}
+
+bool tol_ok(double tol) { return tol > 0.0 && tol < 1.0; }
+
+}  // namespace
+
+extern "C" {
+
+gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) {
+    if (!out) return fail(nullptr, GS_EINVAL, "gs_create: null output pointer");
+    *out = nullptr;
+    if (nx < 1 || ny < 1 || nz < 1) return fail(nullptr, GS_EINVAL, "Grid: point counts must be >= 1");
+    if (!(h > 0.0)) return fail(nullptr, GS_EINVAL, "Grid: spacing h must be positive");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(nullptr, GS_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(nullptr, GS_EINVAL, "gs_create: bad device ordinal");
+    gs_ctx* c = new gs_ctx();
+    c->device = device;
+    c->nx = nx;
+    c->ny = ny;
+    c->nz = nz;
+    c->h = h;
+    c->n = static_cast<int64_t>(nx) * ny * nz;
+    auto bail = [&](cudaError_t err, const char* where) {
+        g_create_error = std::string(where) + ": " + cudaGetErrorString(err);
+        gs_destroy(c);
+        return GS_ECUDA;
+    };
+    if ((e = cudaSetDevice(device)) != cudaSuccess) return bail(e, "cudaSetDevice");
+    cudaDeviceProp prop{};
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return bail(e, "cudaGetDeviceProperties");
+    if (prop.major != 10) {
+        g_create_error = "gs_create: this build targets sm_100a (B200); device is sm_" + std::to_string(prop.major) +
+                         std::to_string(prop.minor);
+        gs_destroy(c);
+        return GS_ECUDA;
+    }
+    if (!prop.cooperativeLaunch) {
+        g_create_error = "gs_create: device lacks cooperative launch";
+        gs_destroy(c);
+        return GS_ECUDA;
+    }
+    c->num_sms = prop.multiProcessorCount;
+    int per_sm = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::solve_kernel, gs::kThreads, 0)) != cudaSuccess)
+        return bail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    c->capacity = per_sm * c->num_sms;
+    if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return bail(e, "cudaStreamCreate");
+    const size_t vb = sizeof(double) * static_cast<size_t>(c->n);
+    for (DevBuf* b : {&c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out})
+        if ((e = b->alloc(vb)) != cudaSuccess) return bail(e, "cudaMalloc(state vectors)");
+    if ((e = c->pal.alloc(static_cast<size_t>(c->n))) != cudaSuccess) return bail(e, "cudaMalloc(labels)");
+    if ((e = cudaMemsetAsync(c->u.p, 0, vb, c->stream)) != cudaSuccess) return bail(e, "cudaMemset");
+    plan_items(c);
+    fill_op(c);
+    *out = c;
+    return GS_OK;
+}
+
+void gs_destroy(gs_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (DevBuf* b : {&c->pal, &c->dvox, &c->wtab, &c->dtab, &c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out,
+                      &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->status, &c->metrics, &c->infos,
+                      &c->normbits})
+        b->release();
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* gs_last_error(const gs_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+int64_t gs_num_points(const gs_ctx* c) { return c ? c->n : 0; }
+
+void* gs_stream(gs_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+gs_status gs_set_intensity(gs_ctx* c, const uint8_t* stack, int w, int hgt, int slices, int t_air, int t_white,
+                           int t_gray, double d_white, double d_gray) {
+    if (!c || !stack) return fail(c, GS_EINVAL, "gs_set_intensity: null argument");
+    if (slices < 1 || w < 1 || hgt < 1) return fail(c, GS_EDATA, "resample: degenerate stack");  // imaging.cpp:126-127
+    cudaSetDevice(c->device);
+    const size_t sb = static_cast<size_t>(w) * hgt * slices;
+    DevBuf dstack;
+    GS_CUDA(c, dstack.alloc(sb));
+    GS_CUDA(c, cudaMemcpyAsync(dstack.p, stack, sb, cudaMemcpyHostToDevice, c->stream));
+    const int blocks = static_cast<int>(std::min<int64_t>((c->n + 255) / 256, 148 * 16));
+    gs::material_kernel<<<std::max(1, blocks), 256, 0, c->stream>>>(dstack.as<uint8_t>(), w, hgt, slices, c->nx, c->ny,
+                                                                    c->nz, t_air, t_white, t_gray, c->pal.as<uint8_t>());
+    GS_CUDA(c, cudaGetLastError());
+    GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    dstack.release();
+    c->palette_mode = true;
+    c->has_labels = true;
+    // diffusion_from_materials (imaging.cpp:143-153): Air, Skull -> 0; White, Gray -> d
+    gs_status st = upload_palette(c, {0.0, d_white, d_gray, 0.0});
+    if (st != GS_OK) return st;
+    return operator_ready(c);
+}
+
+gs_status gs_set_labels(gs_ctx* c, const uint8_t* labels, double d_white, double d_gray) {
+    if (!c || !labels) return fail(c, GS_EINVAL, "gs_set_labels: null argument");
+    for (int64_t v = 0; v < c->n; ++v)
+        if (labels[v] > 3)
+            return fail(c, GS_EDATA, "label volume: byte " + std::to_string(labels[v]) + " is not a material label");
+    cudaSetDevice(c->device);
+    GS_CUDA(c, cudaMemcpyAsync(c->pal.p, labels, static_cast<size_t>(c->n), cudaMemcpyHostToDevice, c->stream));
+    c->palette_mode = true;
+    c->has_labels = true;
+    gs_status st = upload_palette(c, {0.0, d_white, d_gray, 0.0});
+    if (st != GS_OK) return st;
+    return operator_ready(c);
+}
+
+gs_status gs_set_diffusion(gs_ctx* c, const double* d) {
+    if (!c || !d) return fail(c, GS_EINVAL, "gs_set_diffusion: null argument");
+    cudaSetDevice(c->device);
+    // Palette compression: <= 256 distinct bit patterns -> uint8 index + table (1 B/voxel
+    // instead of 8); otherwise the fp64 field is used directly.
+    std::vector<uint64_t> keys(static_cast<size_t>(c->n));
+    std::memcpy(keys.data(), d, sizeof(double) * keys.size());
+    std::vector<uint64_t> uniq(keys);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    c->has_labels = false;
+    if (uniq.size() <= 256) {
+        std::vector<uint8_t> idx(keys.size());
+        for (size_t v = 0; v < keys.size(); ++v)
+            idx[v] = static_cast<uint8_t>(std::lower_bound(uniq.begin(), uniq.end(), keys[v]) - uniq.begin());
+        std::vector<double> dvals(uniq.size());
+        std::memcpy(dvals.data(), uniq.data(), sizeof(double) * uniq.size());
+        GS_CUDA(c, cudaMemcpyAsync(c->pal.p, idx.data(), idx.size(), cudaMemcpyHostToDevice, c->stream));
+        GS_CUDA(c, cudaStreamSynchronize(c->stream));
+        c->palette_mode = true;
+        gs_status st = upload_palette(c, dvals);
+        if (st != GS_OK) return st;
+    } else {
+        GS_CUDA(c, c->dvox.alloc(sizeof(double) * static_cast<size_t>(c->n)));
+        GS_CUDA(c, cudaMemcpyAsync(c->dvox.p, d, sizeof(double) * static_cast<size_t>(c->n), cudaMemcpyHostToDevice,
+                                   c->stream));
+        GS_CUDA(c, c->wtab.alloc(256 * sizeof(double)));
+        GS_CUDA(c, cudaStreamSynchronize(c->stream));
+        c->palette_mode = false;
+    }
+    return operator_ready(c);
+}
+
+gs_status gs_get_labels(gs_ctx* c, uint8_t* labels) {
+    if (!c || !labels) return fail(c, GS_EINVAL, "gs_get_labels: null argument");
+    if (!c->has_labels) return fail(c, GS_EINVAL, "gs_get_labels: operator was not built from material labels");
+    cudaSetDevice(c->device);
+    GS_CUDA(c, cudaMemcpyAsync(labels, c->pal.p, static_cast<size_t>(c->n), cudaMemcpyDeviceToHost, c->stream));
+    GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    return GS_OK;
+}
+
+gs_status gs_get_diffusion(gs_ctx* c, double* d) {
+    if (!c || !d) return fail(c, GS_EINVAL, "gs_get_diffusion: null argument");
+    gs_status st = ensure_operator(c);
+    if (st != GS_OK) return st;
+    cudaSetDevice(c->device);
+    const size_t bytes = sizeof(double) * static_cast<size_t>(c->n);
+    if (c->palette_mode) {
+        const int blocks = static_cast<int>(std::min<int64_t>((c->n + 255) / 256, 148 * 16));
+        gs::expand_palette_kernel<<<std::max(1, blocks), 256, 0, c->stream>>>(c->pal.as<uint8_t>(), c->dtab.as<double>(),
+                                                                               c->n, c->out.as<double>());
+        GS_CUDA(c, cudaGetLastError());
+        GS_CUDA(c, cudaMemcpyAsync(d, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    } else {
+        GS_CUDA(c, cudaMemcpyAsync(d, c->dvox.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    }
+    GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    return GS_OK;
+}
+
+gs_status gs_one_norm(gs_ctx* c, double* out) {
+    if (!c || !out) return fail(c, GS_EINVAL, "gs_one_norm: null argument");
+    gs_status st = ensure_operator(c);
+    if (st != GS_OK) return st;
+    *out = c->anorm;
+    return GS_OK;
+}
+
+gs_status gs_apply(gs_ctx* c, const double* x, double* y) {
+    if (!c || !x || !y) return fail(c, GS_EINVAL, "gs_apply: null argument");
+    gs_status st = ensure_operator(c);
+    if (st != GS_OK) return st;
+    cudaSetDevice(c->device);
+    const size_t bytes = sizeof(double) * static_cast<size_t>(c->n);
+    GS_CUDA(c, cudaMemcpyAsync(c->g.p, x, bytes, cudaMemcpyHostToDevice, c->stream));
+    gs::SolveParams p{};
+    p.mode = gs::kModeApply;
+    p.n_steps = 1;
+    st = launch_solve(c, p, 1, nullptr, nullptr);
+    if (st != GS_OK) return st;
+    GS_CUDA(c, cudaMemcpyAsync(y, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    return GS_OK;
+}
+
+gs_status gs_set_state(gs_ctx* c, const double* u) {
+    if (!c || !u) return fail(c, GS_EINVAL, "gs_set_state: null argument");
+    cudaSetDevice(c->device);
+    GS_CUDA(c, cudaMemcpyAsync(c->u.p, u, sizeof(double) * static_cast<size_t>(c->n), cudaMemcpyHostToDevice,
+                               c->stream));
+    GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    return GS_OK;
+}
+
+gs_status gs_get_state(gs_ctx* c, double* u) {
+    if (!c || !u) return fail(c, GS_EINVAL, "gs_get_state: null argument");
+    cudaSetDevice(c->device);
+    GS_CUDA(c, cudaMemcpyAsync(u, c->u.p, sizeof(double) * static_cast<size_t>(c->n), cudaMemcpyDeviceToHost,
+                               c->stream));
+    GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    return GS_OK;
+}
+
+double* gs_state_device_ptr(gs_ctx* c) { return c ? c->u.as<double>() : nullptr; }
+
+gs_status gs_select_params(double norm_tA, double tol, int* s, int* m) {
+    if (!s || !m) return GS_EINVAL;
+    if (!std::isfinite(norm_tA) || norm_tA < 0.0) {
+        g_create_error = "select_params: operator norm must be finite and nonnegative";
+        return GS_EINVAL;
+    }
+    if (!tol_ok(tol)) {
+        g_create_error = "select_params: tolerance must lie in (0, 1)";
+        return GS_EINVAL;
+    }
+    double rtab[gs::kMaxDegree + 1];
+    fill_rtab(tol, rtab);
+    *s = 1;
+    *m = 1;
+    if (norm_tA == 0.0) return GS_OK;
+    double best_cost = -1.0;
+    for (int mm = 1; mm <= gs::kMaxDegree; ++mm) {
+        const double c = std::ceil(norm_tA / rtab[mm]);
+        const double stages = (1.0 < c) ? c : 1.0;
+        if (stages > 2e9) continue;
+        const double cost = stages * mm;
+        if (best_cost < 0.0 || cost < best_cost) {
+            best_cost = cost;
+            *s = static_cast<int>(stages);
+            *m = mm;
+        }
+    }
+    if (best_cost < 0.0) {
+        g_create_error = "select_params: scaled operator norm too large for any stage count";
+        return GS_ENUMERIC;
+    }
+    return GS_OK;
+}
+
+static gs_status action(gs_ctx* c, int mode, double t, const double* b, double tol, double* out,
+                        gs_step_info* info) {
+    const char* who = mode == gs::kModeExpmv ? "expmv" : "phi1v";
+    if (!c || !b || !out) return fail(c, GS_EINVAL, std::string(who) + ": null argument");
+    if (!tol_ok(tol)) return fail(c, GS_EINVAL, std::string(who) + ": tolerance must lie in (0, 1)");
+    gs_status st = ensure_operator(c);
+    if (st != GS_OK) return st;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(c->n);
+    if (t == 0.0) {  // expact.cpp:69, :108
+        std::memcpy(out, b, bytes);
+        if (info) {
+            std::memset(info, 0, sizeof *info);
+            info->s = info->m = 1;
+            info->branch = 1;
+        }
+        return GS_OK;
+    }
+    cudaSetDevice(c->device);
+    GS_CUDA(c, cudaMemcpyAsync(c->g.p, b, bytes, cudaMemcpyHostToDevice, c->stream));
+    gs::SolveParams p{};
+    p.mode = mode;
+    p.n_steps = 1;
+    p.tau = t;
+    p.tol = tol;
+    fill_rtab(tol, p.rtab);
+    st = launch_solve(c, p, 1, nullptr, info);
+    if (st != GS_OK) return st;
+    GS_CUDA(c, cudaMemcpyAsync(out, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    return GS_OK;
+}
+
+gs_status gs_expmv(gs_ctx* c, double t, const double* b, double tol, double* out, gs_step_info* info) {
+    return action(c, gs::kModeExpmv, t, b, tol, out, info);
+}
+
+gs_status gs_phi1v(gs_ctx* c, double t, const double* b, double tol, double* out, gs_step_info* info) {
+    return action(c, gs::kModePhi1v, t, b, tol, out, info);
+}
+
+gs_status gs_run(gs_ctx* c, int n_steps, double rho, double tau, double tol, const double origin[3],
+                 const double seed_center[3], double front_threshold, gs_metrics* metrics, gs_step_info* infos) {
+    if (!c) return fail(c, GS_EINVAL, "run: null context");
+    if (n_steps < 0) return fail(c, GS_EINVAL, "run: negative step count");
+    if (!tol_ok(tol)) return fail(c, GS_EINVAL, "phi1v: tolerance must lie in (0, 1)");
+    gs_status st = ensure_operator(c);
+    if (st != GS_OK) return st;
+    if (metrics && (!origin || !seed_center)) return fail(c, GS_EINVAL, "run: metrics need origin and seed center");
+    cudaSetDevice(c->device);
+    gs::SolveParams p{};
+    p.mode = gs::kModeRun;
+    p.n_steps = n_steps;
+    p.rho = rho;
+    p.tau = tau;
+    p.tol = tol;
+    p.h = c->h;
+    p.front_threshold = front_threshold;
+    for (int a = 0; a < 3; ++a) {
+        p.origin[a] = origin ? origin[a] : 0.0;
+        p.center[a] = seed_center ? seed_center[a] : 0.0;
+    }
+    fill_rtab(tol, p.rtab);
+    return launch_solve(c, p, n_steps, reinterpret_cast<gs_metrics*>(metrics), infos);
+}
+
+gs_status gs_step(gs_ctx* c, double rho, double tau, double tol, gs_step_info* info) {
+    return gs_run(c, 1, rho, tau, tol, nullptr, nullptr, 0.1, nullptr, info);
+}
+
+gs_status gs_step_host(gs_ctx* c, const double* u, double rho, double tau, double tol, double* out,
+                       gs_step_info* info) {
+    gs_status st = gs_set_state(c, u);
+    if (st != GS_OK) return st;
+    st = gs_step(c, rho, tau, tol, info);
+    if (st != GS_OK) return st;
+    return gs_get_state(c, out);
+}
+
+gs_status gs_seed_initial(gs_ctx* c, const double origin[3], double amplitude, double width, const double center[3],
+                          int mask, double* u) {
+    if (!c || !u || !center) return fail(c, GS_EINVAL, "seed_initial: null argument");
+    const double o[3] = {origin ? origin[0] : 0.0, origin ? origin[1] : 0.0, origin ? origin[2] : 0.0};
+    // Grid::contains (grid.hpp:43-50)
+    const int dims[3] = {c->nx, c->ny, c->nz};
+    for (int a = 0; a < 3; ++a) {
+        const double lo = o[a], hi = o[a] + (dims[a] - 1) * c->h;
+        if (center[a] < lo || center[a] > hi)
+            return fail(c, GS_EDATA, "seed center lies outside the computational domain");
+    }
+    std::vector<double> d;
+    if (mask) {
+        gs_status st = ensure_operator(c);
+        if (st != GS_OK) return st;
+        d.resize(static_cast<size_t>(c->n));
+        st = gs_get_diffusion(c, d.data());
+        if (st != GS_OK) return st;
+    }
+    // integrator.cpp:32-50; sq_dist integrator.cpp:23-29 (this file is built with
+    // -ffp-contract=off on the host side too)
+    int64_t v = 0;
+    for (int k = 1; k <= c->nz; ++k)
+        for (int j = 1; j <= c->ny; ++j)
+            for (int i = 1; i <= c->nx; ++i, ++v) {
+                const double px = o[0] + (i - 1) * c->h, py = o[1] + (j - 1) * c->h, pz = o[2] + (k - 1) * c->h;
+                const double dx = px - center[0], dy = py - center[1], dz = pz - center[2];
+                const double sq = dx * dx + dy * dy + dz * dz;
+                u[v] = amplitude * std::exp(-width * sq);
+                if (mask && d[static_cast<size_t>(v)] == 0.0) u[v] = 0.0;
+            }
+    return GS_OK;
+}
+
+}  // extern "C"

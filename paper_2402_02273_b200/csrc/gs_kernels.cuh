@@ -1,0 +1,56 @@
+// gs_kernels.cuh -- kernel entry points and their parameter blocks.
+#pragma once
+
+#include <cstdint>
+
+#include "gliosim_b200.h"
+#include "gs_device.cuh"
+
+namespace gs {
+
+enum SolveMode : int {
+    kModeRun = 0,      // n exponential-Euler steps on the resident state (integrator.cpp:122-134)
+    kModePhi1v = 1,    // phi1v(t, A, b) (expact.cpp:101-153)
+    kModeExpmv = 2,    // expmv(t, A, b) (expact.cpp:63-99)
+    kModeApply = 3,    // y = A x (sparse.cpp:43-76)
+};
+
+struct SolveParams {
+    StencilOp op;
+    int mode;
+    int n_steps;
+    int want_metrics;
+    int grid_blocks;
+    double rho, tau, tol;   // tau doubles as t for phi1v / expmv
+    double anorm;           // exact ||A||_1 (computed once by the norm kernel)
+    double rtab[kMaxDegree + 1];  // r_m, m = 1..55, host libm (expact.cpp:47-48)
+    // vectors (N doubles each)
+    double* u;
+    double* g;              // RHS b, then b/gamma in place
+    double* f[2];
+    double* t[2];
+    double* out;
+    // compute_metrics (integrator.cpp:65-89)
+    double origin[3], center[3], h, front_threshold;
+    double* metrics;        // [(n_steps+1)*4]
+    gs_step_info* infos;    // [n_steps] or nullptr
+    // cross-CTA scratch
+    double* part_b;         // [grid] block partial sums of |b|
+    double* part_c;         // [grid] block partial sums of |b/gamma|
+    double* part_u;         // [grid] block partial sums of u (metrics)
+    unsigned long long* slots;   // [3][4] rotating max slots for per-term reductions
+    unsigned long long* mslots;  // [2][4] metric max/min/r2 slots (step parity)
+    int* status;            // [0] gs_status, [1] detail
+};
+
+// K1: resample + classify (imaging.cpp:65-72, 118-141)
+__global__ void material_kernel(const uint8_t* stack, int w, int hgt, int slices, int nx, int ny, int nz,
+                                int t_air, int t_white, int t_gray, uint8_t* labels);
+// K3: exact 1-norm of the stencil operator (sparse.cpp:36-40), result as ordered bits
+__global__ void colsum_norm_kernel(StencilOp op, unsigned long long* out_bits);
+// Per-voxel D(x) reconstruction (for gs_get_diffusion in palette mode)
+__global__ void expand_palette_kernel(const uint8_t* pal, const double* dtab, int64_t n, double* d);
+// The persistent exponential-Euler kernel (cooperative launch)
+__global__ void solve_kernel(const __grid_constant__ SolveParams p);
+
+}  // namespace gs

@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the reference's
+golden vectors.
+
+Bars (BASELINE.json north_star): material map and (s, m) sequence exact; u within a
+relative L2 error of 1e-10 per step and 1e-8 after a full run.  Beyond that, with the
+device's tree-reduced ||b||_1 and bordered column sum fed to the oracle, every Taylor
+term is reproduced BIT-FOR-BIT (those two sums are the only order-
+dependent reductions on the path).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+STEP_TOL = 1e-10   # relative L2 per step (north_star)
+RUN_TOL = 1e-8     # relative L2 after the full run (north_star)
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2402_02273_b200 import gliosim
+    return gliosim
+
+
+def rel_l2(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def case(runs_kat, name):
+    p = name + "."
+    shape = tuple(int(v) for v in runs_kat[p + "shape"])
+    h, rho, tau, tol, width, cx, cy, cz = (float(v) for v in runs_kat[p + "params"])
+    return dict(shape=shape, h=h, rho=rho, tau=tau, tol=tol, width=width, center=(cx, cy, cz),
+                labels=runs_kat[p + "labels"], states=runs_kat[p + "states"], metrics=runs_kat[p + "metrics"],
+                log=runs_kat[p + "log"])
+
+
+RUN_NAMES = ["r16", "r2d", "rtau", "rs9", "r4rho", "runmasked", "rflat"]
+
+
+# ---- material map (K1) ----------------------------------------------------------------
+
+def test_material_map_stack29(G, material_kat):
+    stack = material_kat["stack29"]
+    for shape, key in [((24, 20, 40), "stack29.labels"), ((17, 31, 9), "stack29.labels_xy")]:
+        labels = G.resample(stack, 24, 20, 29, G.Grid(*shape, h=1.0))
+        assert np.array_equal(labels, material_kat[key]), key
+
+
+def test_material_map_nearest_kats(G, material_kat):
+    for src in range(1, 8):
+        px = np.array([0 if s % 2 == 0 else 100 for s in range(src)], dtype=np.uint8)
+        for n in range(1, 8):
+            got = G.resample(px, src, 1, 1, G.Grid(n, 1, 1, 1.0))
+            assert np.array_equal(got, material_kat[f"nn.{src}.{n}"]), (src, n)
+
+
+def test_classify_all_intensities(G, material_kat):
+    stack = np.arange(256, dtype=np.uint8)
+    labels = G.resample(stack, 256, 1, 1, G.Grid(256, 1, 1, 1.0))
+    assert np.array_equal(labels, material_kat["classify"])
+
+
+def test_diffusion_from_labels_matches_reference(G, material_kat):
+    labels = material_kat["stack29.labels"]
+    with G.StencilOperator.from_labels(G.Grid(24, 20, 40, 1.0), labels) as op:
+        assert np.array_equal(op.diffusion(), material_kat["stack29.d"])
+        assert np.array_equal(op.labels(), labels)
+
+
+# ---- operator: apply and exact 1-norm ----------------------------------------------------
+
+def test_stencil_apply_and_norm_bitwise(G, kat):
+    for i in range(int(kat["stencil.count"][0])):
+        p = f"stencil.{i}"
+        shape = tuple(int(v) for v in kat[p + ".shape"])
+        with G.assemble_diffusion(G.Grid(*shape, h=float(kat[p + ".h"][0])), kat[p + ".d"]) as op:
+            assert np.array_equal(op.apply(kat[p + ".x"]), kat[p + ".Ax"]), p
+            assert op.one_norm() == kat[p + ".A.norm1"][0], p
+
+
+def test_fp64_field_mode_matches_oracle(G, port):
+    """> 256 distinct D values: the operator runs on the fp64 D field instead of the palette."""
+    rng = np.random.default_rng(3)
+    shape = (19, 13, 11)
+    n = np.prod(shape)
+    d = np.where(rng.random(n) < 0.2, 0.0, rng.uniform(0.01, 0.2, n))
+    x = rng.uniform(-1, 1, n)
+    op_o = port.stencil(shape, 1.3, d)
+    with G.assemble_diffusion(G.Grid(*shape, h=1.3), d) as op:
+        assert np.array_equal(op.apply(x), port.apply(op_o, x))
+        assert op.one_norm() == port.one_norm(op_o)
+        u = rng.uniform(0, 1, n)
+        got, info = G.step(op, u, 0.2, 9.0, 1e-9, info=True)
+        want, _ = port.step(op_o, u, 0.2, 9.0, 1e-9, bnorm=info.bnorm, coln=info.coln)
+        assert np.array_equal(got, want)
+
+
+# ---- exponential action on the stencil ------------------------------------------------------
+
+def test_phi1v_expmv_stencil_kats(G, kat, port):
+    for i in range(int(kat["stencil.count"][0])):
+        p = f"stencil.{i}"
+        shape = tuple(int(v) for v in kat[p + ".shape"])
+        h = float(kat[p + ".h"][0])
+        x = kat[p + ".x"]
+        with G.assemble_diffusion(G.Grid(*shape, h=h), kat[p + ".d"]) as op:
+            got, info = G.phi1v(7.5, op, x, 1e-10, info=True)
+            assert rel_l2(got, kat[p + ".phi1v"]) <= 1e-13, p
+            want, log = port.phi1v(7.5, port.stencil(shape, h, kat[p + ".d"]), x, 1e-10, bnorm=info.bnorm,
+                                   coln=info.coln)
+            assert np.array_equal(got, want), p
+            assert (info.s, info.m, info.total_terms) == (log.s, log.m, log.total_terms)
+            got_e, info_e = G.expmv(7.5, op, x, 1e-10, info=True)
+            # expmv has no order-dependent reduction at all: bitwise against the reference
+            assert np.array_equal(got_e, kat[p + ".expmv"]), p
+
+
+# ---- exponential-Euler step and run ---------------------------------------------------------
+
+@pytest.mark.parametrize("name", RUN_NAMES)
+def test_step_parity_per_step(G, port, runs_kat, name):
+    c = case(runs_kat, name)
+    grid = G.Grid(*c["shape"], h=c["h"])
+    d_oracle = port.diffusion_from_labels(c["labels"])
+    op_o = port.stencil(c["shape"], c["h"], d_oracle)
+    with G.StencilOperator.from_labels(grid, c["labels"]) as op:
+        for n in range(len(c["states"]) - 1):
+            got, info = G.step(op, c["states"][n], c["rho"], c["tau"], c["tol"], info=True)
+            # north_star gate: relative L2 <= 1e-10 per step vs the reference's own step
+            assert rel_l2(got, c["states"][n + 1]) <= STEP_TOL, (name, n)
+            # (s, m) and the terms actually used match the reference's log exactly
+            assert [info.s, info.m, info.total_terms] == list(c["log"][n]), (name, n)
+            # with the device's two order-dependent sums, the oracle reproduces every bit
+            want, log = port.step(op_o, c["states"][n], c["rho"], c["tau"], c["tol"], bnorm=info.bnorm,
+                                  coln=info.coln)
+            assert np.array_equal(got, want), (name, n)
+            assert info.stage_terms() == log.stage_terms()
+
+
+@pytest.mark.parametrize("name", RUN_NAMES)
+def test_run_parity_full(G, runs_kat, name):
+    c = case(runs_kat, name)
+    steps = len(c["states"]) - 1
+    grid = G.Grid(*c["shape"], h=c["h"])
+    with G.StencilOperator.from_labels(grid, c["labels"]) as op:
+        op.set_state(c["states"][0])
+        m, infos = op.run_resident(steps, c["rho"], c["tau"], c["tol"], (0.0, 0.0, 0.0), c["center"], 0.1,
+                                   metrics=True, infos=True)
+        u = op.get_state()
+    assert rel_l2(u, c["states"][-1]) <= RUN_TOL
+    for q in range(steps):
+        assert [infos[q].s, infos[q].m, infos[q].total_terms] == list(c["log"][q])
+    ref_m = c["metrics"]
+    for q in range(steps + 1):
+        # max / min / radius are order-free reductions: exact.  The mass is a sum (tree vs serial).
+        assert m[q].max_density == pytest.approx(ref_m[q, 1], rel=1e-12, abs=0)
+        assert m[q].min_density == pytest.approx(ref_m[q, 2], rel=1e-12, abs=1e-300)
+        assert m[q].radius == pytest.approx(ref_m[q, 3], rel=1e-12, abs=0)
+        assert m[q].total_mass == pytest.approx(ref_m[q, 0], rel=1e-12)
+    # node 0 sees the identical state: the order-free metrics are bitwise there
+    assert m[0].max_density == ref_m[0, 1] and m[0].radius == ref_m[0, 3]
+
+
+def test_seed_initial_bitwise(G, runs_kat):
+    for name in RUN_NAMES:
+        if name == "runmasked":
+            continue
+        c = case(runs_kat, name)
+        cfg = G.SimConfig(seed_center=c["center"], seed_amplitude=1.0, seed_width=c["width"])
+        with G.StencilOperator.from_labels(G.Grid(*c["shape"], h=c["h"]), c["labels"]) as op:
+            assert np.array_equal(G.seed_initial(op, cfg, mask=True), c["states"][0]), name
+
+
+def test_python_run_api_hooks(G, runs_kat):
+    c = case(runs_kat, "r16")
+    steps = len(c["states"]) - 1
+    cfg = G.SimConfig(rho=c["rho"], exp_tol=c["tol"], nx=16, ny=16, nz=16, h=c["h"], t0=150.0,
+                      t_end=150.0 + steps * c["tau"], num_steps=steps, seed_center=c["center"], snapshot_every=3)
+    seen, snaps = [], []
+    with G.StencilOperator.from_labels(cfg.grid(), c["labels"]) as op:
+        res = G.run(cfg, op, c["states"][0], snapshot=lambda n, t, u: snaps.append((n, u)),
+                    on_step=lambda m: seen.append(m.step))
+    assert seen == list(range(1, steps + 1))
+    assert [s[0] for s in snaps] == [0, 3, 6, 8]
+    assert rel_l2(snaps[1][1], c["states"][3]) <= RUN_TOL
+    assert rel_l2(res.u, c["states"][-1]) <= RUN_TOL
+    assert len(res.metrics) == steps + 1
+
+
+# ---- edge cases the reference tests ------------------------------------------------------------
+
+def test_select_params_matches_reference(G, kat):
+    for n, t, s, m in zip(kat["select.norm"], kat["select.tol"], kat["select.s"], kat["select.m"]):
+        assert G.select_params(float(n), float(t)) == (int(s), int(m))
+    with pytest.raises(ValueError):
+        G.select_params(-1.0, 1e-8)
+    with pytest.raises(G.NumericError):
+        G.select_params(1e11, 1e-8)
+
+
+def test_phi1v_edge_cases(G):
+    grid = G.Grid(4, 3, 2, 1.5)
+    rng = np.random.default_rng(21)
+    b = rng.uniform(-1, 1, grid.num_points())
+    with G.assemble_diffusion(grid, np.full(grid.num_points(), 0.1)) as op:
+        assert np.array_equal(G.phi1v(0.0, op, b, 1e-10), b)                        # test_expact.cpp:212
+        assert np.array_equal(G.phi1v(1.0, op, np.zeros_like(b), 1e-10), np.zeros_like(b))
+        with pytest.raises(ValueError, match="vector length"):
+            G.phi1v(1.0, op, np.ones(3), 1e-10)
+        with pytest.raises(ValueError, match="tolerance"):
+            G.phi1v(1.0, op, b, 0.0)
+        assert np.array_equal(G.expmv(0.0, op, b, 1e-10), b)                        # test_expact.cpp:135
+    # empty operator: phi_1(0) b = b through the small-norm branch (test_expact.cpp:218-223)
+    with G.assemble_diffusion(grid, np.zeros(grid.num_points())) as zero:
+        assert np.array_equal(G.phi1v(5.0, zero, b, 1e-10), b)
+        assert zero.one_norm() == 0.0
+
+
+def test_step_without_diffusion_is_forward_euler(G):
+    """test_integrator.cpp:99-106: A = 0 -> u + tau*rho*u*(1-u) bit for bit."""
+    grid = G.Grid(3, 1, 1, 1.0)
+    u = np.array([0.2, 0.5, 0.9])
+    rho, tau = 0.4, 0.25
+    with G.assemble_diffusion(grid, np.zeros(3)) as op:
+        got = G.step(op, u, rho, tau, 1e-10)
+    assert np.array_equal(got, u + tau * (rho * u * (1.0 - u)))
+
+
+def test_small_norm_branch(G, port):
+    """|t|*||A||_1 <= 1e-8 takes b + t*A*b/2 (expact.cpp:114-122)."""
+    shape = (5, 4, 3)
+    d = np.full(np.prod(shape), 1e-12)
+    b = np.random.default_rng(2).uniform(-1, 1, np.prod(shape))
+    with G.assemble_diffusion(G.Grid(*shape, h=1.0), d) as op:
+        got, info = G.phi1v(1.0, op, b, 1e-12, info=True)
+        assert info.branch == 3
+        want, _ = port.phi1v(1.0, port.stencil(shape, 1.0, d), b, 1e-12)
+        assert np.array_equal(got, want)
+
+
+def test_divergence_raises_numeric_error(G):
+    """A growing operator overflows the series -> numeric_error (test_expact.cpp:140-143)."""
+    shape = (4, 4, 4)
+    d = np.full(64, -5.0e3)   # anti-diffusion: exponential growth
+    b = np.random.default_rng(1).uniform(0, 1, 64)
+    with G.assemble_diffusion(G.Grid(*shape, h=1.0), d) as op:
+        with pytest.raises(G.NumericError, match="non-finite"):
+            G.expmv(1e3, op, b, 1e-10)
+
+
+def test_constants_preserved_by_expmv(G):
+    """test_expact.cpp:108-116: rows sum to zero, so exp(tA) 1 = 1."""
+    grid = G.Grid(5, 4, 3, 1.5)
+    with G.assemble_diffusion(grid, np.full(grid.num_points(), 0.13)) as op:
+        y = G.expmv(3.0, op, np.ones(grid.num_points()), 1e-10)
+    assert np.allclose(y, 1.0, rtol=1e-12, atol=0)
+
+
+def test_mid_size_step_vs_oracle(G, port):
+    """64^3 phantom, several steps: bitwise against the oracle given the device sums."""
+    from paper_2402_02273_b200 import phantom
+    n = 64
+    inten = phantom.shell_phantom(n, n, n, seed=31)
+    table = np.array([port.classify(v) for v in range(256)], dtype=np.uint8)
+    labels = table[inten.ravel()]
+    h = 200.0 / (n - 1)
+    i, j, k = phantom.pick_seed_voxel(labels, (n, n, n), 31)
+    d = port.diffusion_from_labels(labels)
+    u = port.seed_initial((n, n, n), h, 1.0, 1.0 / (2 * (3 * h) ** 2), (i * h, j * h, k * h), d)
+    op_o = port.stencil((n, n, n), h, d)
+    with G.StencilOperator.from_intensity(G.Grid(n, n, n, h), inten.ravel(), n, n, n) as op:
+        assert np.array_equal(op.labels(), labels)
+        for _ in range(3):
+            got, info = G.step(op, u, 0.025, 33.5, 1e-8, info=True)
+            want, log = port.step(op_o, u, 0.025, 33.5, 1e-8, bnorm=info.bnorm, coln=info.coln)
+            assert np.array_equal(got, want)
+            assert info.stage_terms() == log.stage_terms()
+            ref_plain, _ = port.step(op_o, u, 0.025, 33.5, 1e-8)
+            assert rel_l2(got, ref_plain) <= STEP_TOL
+            u = got
