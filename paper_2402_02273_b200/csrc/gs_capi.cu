@@ -5,11 +5,14 @@
 // (r_m of select_params, expact.cpp:47-48; the Gaussian seed, integrator.cpp:40-41) so
 // those values are bit-identical; everything per-voxel runs on the GPU.  No CPU
 // fallback exists: without a device every entry point returns GS_ECUDA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -69,6 +72,10 @@ struct gs_ctx {
 
     gs::StencilOp op{};
     int grid_blocks = 0;
+    bool tma_ok = false;          // TMA descriptors built (nx % 16 == 0)
+    CUtensorMap xmap[gs::kNumBufs];
+    CUtensorMap omap[gs::kNumBufs];
+    CUtensorMap lmap;
     std::string err;
 };
 
@@ -90,27 +97,26 @@ gs_status cuda_fail(gs_ctx* c, cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
     } while (0)
 
-// Pick the z-chunk so the items spread evenly over the co-resident CTAs (balance first,
-// then the longest chunk for z-reuse along each column).
+// Fallback-sweep decomposition (sweep_l1): tiles of 32 x (threads/32) columns; pick the
+// z-chunk so the items spread evenly over the co-resident CTAs (balance first, then the
+// longest chunk for z-reuse along each column).  The TMA sweep partitions tile-planes
+// itself (contiguous, balanced ranges per CTA).
 void plan_items(gs_ctx* c) {
     gs::StencilOp& op = c->op;
-    op.tiles_x = (c->nx + gs::kTX - 1) / gs::kTX;
-    op.tiles_y = (c->ny + gs::kTY - 1) / gs::kTY;
+    const int ty = gs::kSolveThreads / 32;
+    op.tiles_x = (c->nx + 31) / 32;
+    op.tiles_y = (c->ny + ty - 1) / ty;
     const int64_t tiles = static_cast<int64_t>(op.tiles_x) * op.tiles_y;
-    const int cap = std::max(1, c->capacity);
+    const int grid = std::max(1, c->capacity);
     int best_zc = 1;
     double best_score = -1.0;
     for (int zc = 1; zc <= c->nz; ++zc) {
         const int64_t chunks = (c->nz + zc - 1) / zc;
         const int64_t items = tiles * chunks;
-        const int64_t grid = std::min<int64_t>(items, cap);
         const int64_t rounds = (items + grid - 1) / grid;
-        // work per CTA ~ planes; imbalance from ragged last chunk and last round
-        const double work = static_cast<double>(tiles) * c->nz;
-        const double span = static_cast<double>(rounds) * zc;  // planes per CTA (critical path)
-        const double eff = work / (static_cast<double>(grid) * span);
-        const double halo = 2.0 / (zc + 2.0);  // extra plane loads per chunk
-        const double score = eff * (1.0 - 0.5 * halo);
+        const double span = static_cast<double>(rounds) * zc;  // planes per CTA on the critical path
+        const double eff = static_cast<double>(tiles) * c->nz / (static_cast<double>(grid) * span);
+        const double score = eff * (1.0 - 1.0 / (zc + 2.0));
         if (score > best_score + 1e-9) {
             best_score = score;
             best_zc = zc;
@@ -119,7 +125,47 @@ void plan_items(gs_ctx* c) {
     op.zc = best_zc;
     op.chunks_z = (c->nz + best_zc - 1) / best_zc;
     op.n_items = tiles * op.chunks_z;
-    c->grid_blocks = static_cast<int>(std::min<int64_t>(op.n_items, cap));
+    c->grid_blocks = grid;
+}
+
+// TMA descriptors over the x-fastest arrays: halo boxes (TX+2)x(TY+2)x1 starting one voxel
+// outside the tile (out-of-bounds elements read as 0.0), own boxes TXxTYx1, labels as u8.
+gs_status build_tensor_maps(gs_ctx* c) {
+    c->tma_ok = false;
+    if (c->nx % 16 != 0) return GS_OK;  // u8 label rows need 16-byte pitch
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return GS_OK;  // no TMA: fallback sweep
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(c->nx), static_cast<cuuint64_t>(c->ny),
+                                static_cast<cuuint64_t>(c->nz)};
+    const cuuint64_t st8[2] = {static_cast<cuuint64_t>(c->nx) * 8, static_cast<cuuint64_t>(c->nx) * c->ny * 8};
+    const cuuint64_t st1[2] = {static_cast<cuuint64_t>(c->nx), static_cast<cuuint64_t>(c->nx) * c->ny};
+    const cuuint32_t halo[3] = {gs::kTmaTX + 2, gs::kTmaTY + 2, 1};
+    const cuuint32_t own[3] = {gs::kTmaTX, gs::kTmaTY, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    DevBuf* bufs[gs::kNumBufs] = {&c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out};
+    for (int b = 0; b < gs::kNumBufs; ++b) {
+        CUresult r = encode(&c->xmap[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, bufs[b]->p, dims, st8, halo, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(halo) failed: " + std::to_string(r));
+        r = encode(&c->omap[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, bufs[b]->p, dims, st8, own, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(own) failed: " + std::to_string(r));
+    }
+    CUresult r = encode(&c->lmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, c->pal.p, dims, st1, own, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(labels) failed: " + std::to_string(r));
+    c->tma_ok = true;
+    return GS_OK;
 }
 
 gs_status ensure_operator(gs_ctx* c) {
@@ -212,6 +258,14 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     p.op = c->op;
     p.grid_blocks = gb;
     p.anorm = c->anorm;
+    p.use_tma = (c->tma_ok && c->palette_mode && std::getenv("GS_DISABLE_TMA") == nullptr) ? 1 : 0;
+    if (p.use_tma) {
+        for (int b = 0; b < gs::kNumBufs; ++b) {
+            p.xmap[b] = c->xmap[b];
+            p.omap[b] = c->omap[b];
+        }
+        p.lmap = c->lmap;
+    }
     p.metrics = metrics ? c->metrics.as<double>() : nullptr;
     p.want_metrics = metrics ? 1 : 0;
     p.infos = infos ? c->infos.as<gs_step_info>() : nullptr;
@@ -221,16 +275,12 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     p.slots = c->slots.as<unsigned long long>();
     p.mslots = c->mslots.as<unsigned long long>();
     p.status = c->status.as<int>();
-    p.u = c->u.as<double>();
-    p.g = c->g.as<double>();
-    p.f[0] = c->f0.as<double>();
-    p.f[1] = c->f1.as<double>();
-    p.t[0] = c->t0.as<double>();
-    p.t[1] = c->t1.as<double>();
-    p.out = c->out.as<double>();
+    DevBuf* bufs[gs::kNumBufs] = {&c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out};
+    for (int b = 0; b < gs::kNumBufs; ++b) p.buf[b] = bufs[b]->as<double>();
     void* args[] = {&p};
-    GS_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gs::solve_kernel), dim3(gb), dim3(gs::kThreads),
-                                           args, 0, c->stream));
+    GS_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gs::solve_kernel), dim3(gb),
+                                           dim3(gs::kSolveThreads), args, p.use_tma ? gs::kRingBytes : 0,
+                                           c->stream));
     int status[2] = {0, 0};
     GS_CUDA(c, cudaMemcpyAsync(status, c->status.p, sizeof status, cudaMemcpyDeviceToHost, c->stream));
     if (metrics)
@@ -292,9 +342,18 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
         return GS_ECUDA;
     }
     c->num_sms = prop.multiProcessorCount;
+    if ((e = cudaFuncSetAttribute(gs::solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kRingBytes)) !=
+        cudaSuccess)
+        return bail(e, "cudaFuncSetAttribute(smem)");
     int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::solve_kernel, gs::kThreads, 0)) != cudaSuccess)
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::solve_kernel, gs::kSolveThreads,
+                                                           gs::kRingBytes)) != cudaSuccess)
         return bail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (per_sm < 1) {
+        g_create_error = "gs_create: solve kernel does not fit on an SM";
+        gs_destroy(c);
+        return GS_ECUDA;
+    }
     c->capacity = per_sm * c->num_sms;
     if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess)
         return bail(e, "cudaStreamCreate");
@@ -305,6 +364,11 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
     if ((e = cudaMemsetAsync(c->u.p, 0, vb, c->stream)) != cudaSuccess) return bail(e, "cudaMemset");
     plan_items(c);
     fill_op(c);
+    if (build_tensor_maps(c) != GS_OK) {
+        g_create_error = c->err;
+        gs_destroy(c);
+        return GS_ECUDA;
+    }
     *out = c;
     return GS_OK;
 }

@@ -1,6 +1,7 @@
 // gs_kernels.cuh -- kernel entry points and their parameter blocks.
 #pragma once
 
+#include <cuda.h>
 #include <cstdint>
 
 #include "gliosim_b200.h"
@@ -15,8 +16,30 @@ enum SolveMode : int {
     kModeApply = 3,    // y = A x (sparse.cpp:43-76)
 };
 
+// Device vectors, by index (the TMA descriptors are indexed the same way).
+enum Buf : int { kBufU = 0, kBufG = 1, kBufF0 = 2, kBufF1 = 3, kBufT0 = 4, kBufT1 = 5, kBufOut = 6, kNumBufs = 7 };
+
+// TMA z-slab pipeline geometry: a CTA owns tiles of kTmaTX x kTmaTY columns and
+// streams their z-planes through a kTmaStages-deep shared-memory ring.
+constexpr int kTmaTX = 64;
+constexpr int kTmaTY = 16;
+constexpr int kTmaStages = 6;
+constexpr int kSolveThreads = 512;   // 16 warps: warp w owns tile row w, two columns per lane
+
+constexpr int kXPitch = kTmaTX + 2;                                    // doubles per halo row
+constexpr int kXBytes = ((kTmaTY + 2) * kXPitch * 8 + 127) / 128 * 128;  // halo plane tile
+constexpr int kOBytes = kTmaTX * kTmaTY * 8;                            // own plane tile (fp64)
+constexpr int kLBytes = kTmaTX * kTmaTY;                                // own plane tile (labels)
+constexpr int kSlotBytes = kXBytes + 2 * kOBytes + kLBytes;
+constexpr int kRingBytes = kTmaStages * kSlotBytes + 128;              // + barriers
+
 struct SolveParams {
+    // TMA descriptors (64-byte aligned by type): halo-box and own-box maps per vector, labels
+    CUtensorMap xmap[kNumBufs];
+    CUtensorMap omap[kNumBufs];
+    CUtensorMap lmap;
     StencilOp op;
+    int use_tma;
     int mode;
     int n_steps;
     int want_metrics;
@@ -24,12 +47,7 @@ struct SolveParams {
     double rho, tau, tol;   // tau doubles as t for phi1v / expmv
     double anorm;           // exact ||A||_1 (computed once by the norm kernel)
     double rtab[kMaxDegree + 1];  // r_m, m = 1..55, host libm (expact.cpp:47-48)
-    // vectors (N doubles each)
-    double* u;
-    double* g;              // RHS b, then b/gamma in place
-    double* f[2];
-    double* t[2];
-    double* out;
+    double* buf[kNumBufs];
     // compute_metrics (integrator.cpp:65-89)
     double origin[3], center[3], h, front_threshold;
     double* metrics;        // [(n_steps+1)*4]

@@ -1,0 +1,624 @@
+// gs_solve.cu -- the persistent exponential-Euler kernel (sm_100a).
+//
+// One cooperative launch runs whole exponential-Euler steps (integrator.cpp:52-63) for
+// every step of a run (integrator.cpp:122-134):
+//
+//   K2  RHS sweep        g = A u + rho u (1-u), ||g||_1                (integrator.cpp:54-57)
+//   --  bordered column  g <- g/gamma, sum|g/gamma|; (s, m) on device   (expact.cpp:110-142, 29-61)
+//   K4  Taylor terms     T_j = (t/s)/j * (A~ T_{j-1}); f += T_j; ||T||, ||f||; stop test
+//                        (expact.cpp:79-97) -- one HBM pass per term
+//   K5  update + metrics u <- u + tau*(gamma/tau)*f; compute_metrics   (integrator.cpp:58-61, 65-89)
+//
+// Phases are separated by grid-wide barriers (cooperative groups); every CTA evaluates the
+// same scalar control flow from the same reduced values, so the (s, m) choice and the
+// early-termination decisions are taken identically everywhere with no host round trip.
+//
+// Stencil sweeps stream z-planes of a kTmaTX x kTmaTY column tile through a
+// kTmaStages-deep shared-memory ring filled by TMA (cp.async.bulk.tensor, halo tiles with
+// out-of-bounds zero fill = the missing Neumann neighbours); each thread keeps the z-1/z/z+1
+// values of its columns in registers and takes its in-plane neighbours from shared memory.
+// Each CTA owns a fixed, balanced, contiguous range of tile-planes (one CTA per SM).
+// Shapes the TMA path cannot describe (nx % 16 != 0, fp64-D mode) use an L1-cached
+// fallback sweep with identical arithmetic.
+#include <cooperative_groups.h>
+
+#include "gs_kernels.cuh"
+#include "gs_tma.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gs {
+
+namespace {
+
+struct Smem {
+    double wtab[256];
+    double red[kSolveThreads / 32][4];
+    double bcast[4];
+};
+
+struct Ring {
+    unsigned char* base;
+    uint64_t* bar;
+    __device__ double* x(int s) const { return reinterpret_cast<double*>(base + s * kSlotBytes); }
+    __device__ double* f(int s) const { return reinterpret_cast<double*>(base + s * kSlotBytes + kXBytes); }
+    __device__ double* b(int s) const { return reinterpret_cast<double*>(base + s * kSlotBytes + kXBytes + kOBytes); }
+    __device__ uint8_t* l(int s) const { return base + s * kSlotBytes + kXBytes + 2 * kOBytes; }
+};
+
+// Block reduction of up to 4 values with a fixed shape; result valid in thread 0.
+template <int K, bool kMax>
+__device__ __forceinline__ void block_reduce(double (&v)[K], Smem& sm) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < K; ++q) v[q] = kMax ? warp_max(v[q]) : warp_sum(v[q]);
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < K; ++q) sm.red[wid][q] = v[q];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            double a = sm.red[0][q];
+            for (int w = 1; w < kSolveThreads / 32; ++w)
+                a = kMax ? nan_dropping_max(a, sm.red[w][q]) : __dadd_rn(a, sm.red[w][q]);
+            v[q] = a;
+        }
+    }
+    __syncthreads();
+}
+
+// Deterministic sum of the per-CTA partials; every CTA computes the same value.
+__device__ double grid_sum(const double* part, int nb, Smem& sm) {
+    if (threadIdx.x < 32) {
+        double acc = 0.0;
+        for (int b = threadIdx.x; b < nb; b += 32) acc = __dadd_rn(acc, __ldcg(part + b));
+        acc = warp_sum(acc);
+        if (threadIdx.x == 0) sm.bcast[0] = acc;
+    }
+    __syncthreads();
+    const double r = sm.bcast[0];
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ double slot_read(const unsigned long long* s) {
+    return __longlong_as_double(static_cast<long long>(__ldcg(s)));
+}
+
+// select_params (expact.cpp:29-61) with the libm part (r_m) precomputed on the host;
+// what remains is IEEE division, ceil, max, multiply and compare: bit-identical.
+__device__ int select_params_dev(double norm_tA, const double* rtab, int* s_out, int* m_out) {
+    if (!isfinite(norm_tA) || norm_tA < 0.0) return GS_EINVAL;
+    *s_out = 1;
+    *m_out = 1;
+    if (norm_tA == 0.0) return GS_OK;
+    double best_cost = -1.0;
+    for (int m = 1; m <= kMaxDegree; ++m) {
+        const double c = ceil(__ddiv_rn(norm_tA, rtab[m]));
+        const double stages = (1.0 < c) ? c : 1.0;
+        if (stages > 2e9) continue;
+        const double cost = __dmul_rn(stages, static_cast<double>(m));
+        if (best_cost < 0.0 || cost < best_cost) {
+            best_cost = cost;
+            *s_out = static_cast<int>(stages);
+            *m_out = m;
+        }
+    }
+    return best_cost < 0.0 ? GS_ENUMERIC : GS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// Sweeps
+// ------------------------------------------------------------------------------------------
+
+// Pointwise sweep: grid-stride over voxels, no neighbours.
+template <class Body>
+__device__ __forceinline__ void sweep_points(const StencilOp& op, Body&& body) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < op.n; v += stride) body(v);
+}
+
+// Fallback stencil sweep (L1-cached loads, z-march in registers); used where TMA cannot
+// describe the arrays.  Tiles of 32 x (blockDim/32) columns times z-chunks of op.zc planes.
+template <class Body>
+__device__ __forceinline__ void sweep_l1(const StencilOp& op, const double* X, const double* F, const double* B,
+                                         const double* s_wtab, Body&& body) {
+    const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+    const int ty_n = blockDim.x >> 5;
+    const int64_t tiles = static_cast<int64_t>(op.tiles_x) * op.tiles_y;
+    for (int64_t item = blockIdx.x; item < op.n_items; item += gridDim.x) {
+        const int64_t tile = item % tiles;
+        const int chunk = static_cast<int>(item / tiles);
+        const int i = static_cast<int>(tile % op.tiles_x) * 32 + lx;
+        const int j = static_cast<int>(tile / op.tiles_x) * ty_n + ly;
+        const bool act = i < op.nx && j < op.ny;
+        const int z0 = chunk * op.zc;
+        const int z1 = min(op.nz, z0 + op.zc);
+        const int64_t colv = i + static_cast<int64_t>(j) * op.sy;
+        double xm = 0.0, xc = 0.0;
+        if (act) {
+            xm = z0 > 0 ? X[colv + (z0 - 1) * op.sz] : 0.0;
+            xc = X[colv + z0 * op.sz];
+        }
+        const bool hx0 = i > 0, hx1 = i < op.nx - 1, hy0 = j > 0, hy1 = j < op.ny - 1;
+        for (int k = z0; k < z1; ++k) {
+            const int64_t v = colv + k * op.sz;
+            const bool hz0 = k > 0, hz1 = k < op.nz - 1;
+            double xp = 0.0;
+            if (act) {
+                xp = hz1 ? X[v + op.sz] : 0.0;
+                const double xxm = hx0 ? X[v - 1] : 0.0;
+                const double xxp = hx1 ? X[v + 1] : 0.0;
+                const double xym = hy0 ? X[v - op.sy] : 0.0;
+                const double xyp = hy1 ? X[v + op.sy] : 0.0;
+                const RowCoef rc = row_coef(op, s_wtab, v);
+                const int cnt = hx0 + hx1 + hy0 + hy1 + hz0 + hz1;
+                const double acc = row_apply(rc, cnt, xm, xym, xxm, xc, xxp, xyp, xp);
+                body(v, acc, xc, F ? F[v] : 0.0, B ? B[v] : 0.0);
+            }
+            xm = xc;
+            xc = xp;
+        }
+    }
+}
+
+// TMA z-slab sweep.  `seq` counts plane loads issued so far in this launch (identical in
+// every thread); it fixes each ring slot's mbarrier phase parity.
+template <bool kNeedF, bool kNeedB, class Body>
+__device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring, int xbuf, int fbuf, int bbuf,
+                                          uint32_t& seq, const double* s_wtab, Body&& body) {
+    const StencilOp& op = p.op;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, row = tid >> 5;
+    const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
+    const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
+    const int64_t Q = static_cast<int64_t>(tiles_x) * tiles_y * op.nz;
+    const int64_t q_begin = static_cast<int64_t>(blockIdx.x) * Q / gridDim.x;
+    const int64_t q_end = static_cast<int64_t>(blockIdx.x + 1) * Q / gridDim.x;
+    constexpr uint32_t kOwnBytes = kLBytes + (kNeedF ? kOBytes : 0) + (kNeedB ? kOBytes : 0);
+    constexpr uint32_t kHaloBytes = (kTmaTY + 2) * kXPitch * 8;
+    if (tid == 0) fence_proxy_async_global();  // generic writes before this sweep -> TMA reads
+
+    for (int64_t q = q_begin; q < q_end;) {
+        const int64_t tile = q / op.nz;
+        const int z0 = static_cast<int>(q % op.nz);
+        const int z1 = static_cast<int>(min(static_cast<int64_t>(op.nz), static_cast<int64_t>(z0) + (q_end - q)));
+        q += z1 - z0;
+        const int x0 = static_cast<int>(tile % tiles_x) * kTmaTX;
+        const int y0 = static_cast<int>(tile / tiles_x) * kTmaTY;
+        const uint32_t base = seq;
+        const int np = z1 - z0 + 2;  // planes z0-1 .. z1
+
+        auto issue = [&](int pl) {
+            const uint32_t sq = base + static_cast<uint32_t>(pl - (z0 - 1));
+            const int slot = static_cast<int>(sq % kTmaStages);
+            uint64_t* bar = ring.bar + slot;
+            const bool own = pl >= z0 && pl < z1;
+            mbar_arrive_expect_tx(bar, kHaloBytes + (own ? kOwnBytes : 0));
+            tma_load_3d(ring.x(slot), &p.xmap[xbuf], x0 - 1, y0 - 1, pl, bar);
+            if (own) {
+                if (kNeedF) tma_load_3d(ring.f(slot), &p.omap[fbuf], x0, y0, pl, bar);
+                if (kNeedB) tma_load_3d(ring.b(slot), &p.omap[bbuf], x0, y0, pl, bar);
+                tma_load_3d(ring.l(slot), &p.lmap, x0, y0, pl, bar);
+            }
+        };
+        auto slot_of = [&](int pl) { return static_cast<int>((base + static_cast<uint32_t>(pl - (z0 - 1))) % kTmaStages); };
+        auto wait_plane = [&](int pl) {
+            const uint32_t sq = base + static_cast<uint32_t>(pl - (z0 - 1));
+            mbar_wait(ring.bar + sq % kTmaStages, (sq / kTmaStages) & 1u);
+        };
+
+        if (tid == 0) {
+            const int pre = min(kTmaStages, np);
+            for (int k = 0; k < pre; ++k) issue(z0 - 1 + k);
+        }
+
+        // this thread's two columns of the tile
+        const int j = y0 + row;
+        int ii[2] = {x0 + lane, x0 + lane + 32};
+        const bool hy0 = j > 0, hy1 = j < op.ny - 1;
+        double xm[2], xc[2];
+        wait_plane(z0 - 1);
+        wait_plane(z0);
+        {
+            const double* Xm = ring.x(slot_of(z0 - 1));
+            const double* Xc = ring.x(slot_of(z0));
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int lx = lane + 32 * c;
+                xm[c] = Xm[(row + 1) * kXPitch + lx + 1];
+                xc[c] = Xc[(row + 1) * kXPitch + lx + 1];
+            }
+        }
+        for (int z = z0; z < z1; ++z) {
+            wait_plane(z + 1);
+            const int sc = slot_of(z), sp = slot_of(z + 1);
+            const double* Xc = ring.x(sc);
+            const double* Xp = ring.x(sp);
+            const double* Fo = ring.f(sc);
+            const double* Bo = ring.b(sc);
+            const uint8_t* Lo = ring.l(sc);
+            const bool hz0 = z > 0, hz1 = z < op.nz - 1;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int lx = lane + 32 * c;
+                const int i = ii[c];
+                const double xp = Xp[(row + 1) * kXPitch + lx + 1];
+                if (i < op.nx && j < op.ny) {
+                    const double xym = Xc[row * kXPitch + lx + 1];
+                    const double xyp = Xc[(row + 2) * kXPitch + lx + 1];
+                    const double xxm = Xc[(row + 1) * kXPitch + lx];
+                    const double xxp = Xc[(row + 1) * kXPitch + lx + 2];
+                    const int o = row * kTmaTX + lx;
+                    RowCoef rc;
+                    rc.w = s_wtab[Lo[o]];
+                    rc.live = rc.w != 0.0;
+                    const int cnt = (i > 0) + (i < op.nx - 1) + hy0 + hy1 + hz0 + hz1;
+                    const double acc = row_apply(rc, cnt, xm[c], xym, xxm, xc[c], xxp, xyp, xp);
+                    const int64_t v = i + static_cast<int64_t>(j) * op.sy + static_cast<int64_t>(z) * op.sz;
+                    body(v, acc, xc[c], kNeedF ? Fo[o] : 0.0, kNeedB ? Bo[o] : 0.0);
+                }
+                xm[c] = xc[c];
+                xc[c] = xp;
+            }
+            __syncthreads();  // every thread is done with plane z-1's slot
+            if (tid == 0) {
+                const int nxt = z - 1 + kTmaStages;
+                if (nxt <= z1) issue(nxt);
+            }
+        }
+        seq = base + static_cast<uint32_t>(np);
+    }
+    fence_proxy_async_global();  // this thread's generic writes -> later TMA reads
+}
+
+enum TermKind { kFirstZero, kFirstBorder, kFirstPlain, kNext };
+
+}  // namespace
+
+__global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_constant__ SolveParams p) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ Smem sm;
+    extern __shared__ __align__(128) unsigned char dyn[];
+    const StencilOp& op = p.op;
+    if (op.pal)
+        for (int q = threadIdx.x; q < 256; q += blockDim.x) sm.wtab[q] = __ldg(op.wtab + q);
+    Ring ring{dyn, reinterpret_cast<uint64_t*>(dyn + kTmaStages * kSlotBytes)};
+    if (p.use_tma && threadIdx.x == 0) {
+        for (int s = 0; s < kTmaStages; ++s) mbar_init(ring.bar + s, 1);
+        mbar_fence_init();
+        for (int b = 0; b < kNumBufs; ++b) tma_prefetch_desc(&p.xmap[b]);
+    }
+    __syncthreads();
+    uint32_t seq = 0;
+    // Grid barrier; with TMA, first order this thread's generic global writes before any
+    // later async-proxy (TMA) read of them.
+    auto gsync = [&]() {
+        if (p.use_tma) fence_proxy_async_global();
+        grid.sync();
+    };
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    int round = 0;  // per-term max-reduction rounds (slot rotation, identical in every CTA)
+
+    // Stencil sweep dispatch: X = stencil input, F / B = own-voxel side inputs.
+    auto stencil = [&](int xb, int fb, int bb, auto&& body) {
+        const bool nf = fb >= 0, nb = bb >= 0;
+        if (p.use_tma) {
+            if (nf && nb) sweep_tma<true, true>(p, ring, xb, fb, bb, seq, sm.wtab, body);
+            else if (nf) sweep_tma<true, false>(p, ring, xb, fb, 0, seq, sm.wtab, body);
+            else if (nb) sweep_tma<false, true>(p, ring, xb, 0, bb, seq, sm.wtab, body);
+            else sweep_tma<false, false>(p, ring, xb, 0, 0, seq, sm.wtab, body);
+        } else {
+            sweep_l1(op, p.buf[xb], nf ? p.buf[fb] : nullptr, nb ? p.buf[bb] : nullptr, sm.wtab, body);
+        }
+    };
+
+    auto sync_round = [&]() {
+        gsync();
+        if (leader) {
+            unsigned long long* z = p.slots + ((round + 2) % 3) * 4;
+            z[0] = z[1] = z[2] = z[3] = 0ull;
+        }
+        ++round;
+    };
+    auto push_max2 = [&](double a, double b) {
+        double v[2] = {a, b};
+        block_reduce<2, true>(v, sm);
+        if (threadIdx.x == 0) {
+            unsigned long long* s = p.slots + (round % 3) * 4;
+            if (v[0] > 0.0) atomicMax(s + 0, static_cast<unsigned long long>(__double_as_longlong(v[0])));
+            if (v[1] > 0.0) atomicMax(s + 1, static_cast<unsigned long long>(__double_as_longlong(v[1])));
+        }
+    };
+
+    // compute_metrics (integrator.cpp:65-89): the sum in a fixed tree (the reference's serial
+    // sum differs in the last bits), max/min/front radius exactly.
+    auto metrics_local = [&](double& sum, double& mx, double& mn, double& r2, int64_t v, double u) {
+        sum = __dadd_rn(sum, u);
+        mx = nan_dropping_max(mx, u);
+        mn = (u < mn) ? u : mn;
+        if (u >= p.front_threshold) {
+            const int i = static_cast<int>(v % op.nx);
+            const int j = static_cast<int>((v / op.nx) % op.ny);
+            const int k = static_cast<int>(v / op.sz);
+            const double dx = __dsub_rn(__dadd_rn(p.origin[0], __dmul_rn(static_cast<double>(i), p.h)), p.center[0]);
+            const double dy = __dsub_rn(__dadd_rn(p.origin[1], __dmul_rn(static_cast<double>(j), p.h)), p.center[1]);
+            const double dz = __dsub_rn(__dadd_rn(p.origin[2], __dmul_rn(static_cast<double>(k), p.h)), p.center[2]);
+            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            r2 = nan_dropping_max(r2, d2);
+        }
+    };
+    auto metrics_push = [&](double sum, double mx, double mn, double r2, int parity) {
+        double s[1] = {sum};
+        block_reduce<1, false>(s, sm);
+        if (threadIdx.x == 0) p.part_u[blockIdx.x] = s[0];
+        const double mxw = warp_max(mx);
+        double mnw = mn;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double q = __shfl_xor_sync(0xffffffffu, mnw, o);
+            mnw = (q < mnw) ? q : mnw;
+        }
+        const double r2w = warp_max(r2);
+        if ((threadIdx.x & 31) == 0) {
+            unsigned long long* ms = p.mslots + parity * 4;
+            atomicMax(ms + 0, ordered_key(mxw));
+            atomicMin(ms + 1, ordered_key(mnw));
+            if (r2w > 0.0) atomicMax(ms + 2, static_cast<unsigned long long>(__double_as_longlong(r2w)));
+        }
+    };
+    auto metrics_finish = [&](int node, int parity) {
+        const double sum = grid_sum(p.part_u, p.grid_blocks, sm);
+        if (leader) {
+            unsigned long long* ms = p.mslots + parity * 4;
+            const double cell = __dmul_rn(__dmul_rn(p.h, p.h), p.h);
+            double* out = p.metrics + 4 * node;
+            out[0] = __dmul_rn(cell, sum);
+            out[1] = from_ordered_key(__ldcg(ms + 0));
+            out[2] = from_ordered_key(__ldcg(ms + 1));
+            out[3] = sqrt(__longlong_as_double(static_cast<long long>(__ldcg(ms + 2))));
+            ms[0] = 0ull;
+            ms[1] = ~0ull;
+            ms[2] = 0ull;
+        }
+    };
+
+    double* const U = p.buf[kBufU];
+    double* const G = p.buf[kBufG];
+    double* const OUT = p.buf[kBufOut];
+
+    // -------------------------------------------------------------- y = A x
+    if (p.mode == kModeApply) {
+        stencil(kBufG, -1, -1, [&](int64_t v, double acc, double, double, double) { OUT[v] = acc; });
+        return;
+    }
+
+    const bool run = p.mode == kModeRun;
+    const bool bordered = p.mode != kModeExpmv;
+    const double t = p.tau;
+
+    if (run && p.want_metrics) {
+        double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
+        sweep_points(op, [&](int64_t v) { metrics_local(sum, mx, mn, r2, v, U[v]); });
+        metrics_push(sum, mx, mn, r2, 0);
+        gsync();
+        metrics_finish(0, 0);
+    }
+
+    const int n_steps = run ? p.n_steps : 1;
+    for (int step = 0; step < n_steps; ++step) {
+        gs_step_info* info = (p.infos && leader) ? p.infos + step : nullptr;
+        if (info) {
+            info->s = info->m = 1;
+            info->branch = 0;
+            info->total_terms = 0;
+            info->anorm = p.anorm;
+            info->bnorm = info->coln = info->gamma = info->norm_tA = 0.0;
+        }
+        double bnorm = 0.0;
+        // ---------------------------------------------------------- K2: RHS + ||b||_1
+        if (run) {
+            // g = A u; g += rho*u*(1-u)   (integrator.cpp:54-57)
+            double bsum = 0.0;
+            stencil(kBufU, -1, -1, [&](int64_t v, double acc, double u, double, double) {
+                const double g = __dadd_rn(acc, __dmul_rn(__dmul_rn(p.rho, u), __dsub_rn(1.0, u)));
+                G[v] = g;
+                bsum = __dadd_rn(bsum, fabs(g));
+            });
+            double s[1] = {bsum};
+            block_reduce<1, false>(s, sm);
+            if (threadIdx.x == 0) p.part_b[blockIdx.x] = s[0];
+        } else if (bordered) {
+            double bsum = 0.0;
+            sweep_points(op, [&](int64_t v) { bsum = __dadd_rn(bsum, fabs(G[v])); });
+            double s[1] = {bsum};
+            block_reduce<1, false>(s, sm);
+            if (threadIdx.x == 0) p.part_b[blockIdx.x] = s[0];
+        } else {
+            // expmv: prev = ||b||_inf at stage 0 (expact.cpp:80)
+            double mb = 0.0;
+            sweep_points(op, [&](int64_t v) { mb = nan_dropping_max(mb, fabs(G[v])); });
+            push_max2(mb, 0.0);
+        }
+        gsync();
+
+        int branch = 0;
+        double prev0 = 1.0;  // ||e_{n+1}||_inf for the bordered action
+        if (bordered) {
+            bnorm = grid_sum(p.part_b, p.grid_blocks, sm);
+            if (info) info->bnorm = bnorm;
+            if (t == 0.0) branch = 1;                                  // expact.cpp:108
+            else if (bnorm == 0.0) branch = 2;                         // expact.cpp:111
+            else if (__dmul_rn(fabs(t), p.anorm) <= 1e-8) branch = 3;  // expact.cpp:114
+        } else {
+            prev0 = slot_read(p.slots + (round % 3) * 4);
+            if (leader) {
+                unsigned long long* z = p.slots + ((round + 2) % 3) * 4;
+                z[0] = z[1] = z[2] = z[3] = 0ull;
+            }
+            ++round;
+        }
+        if (info) info->branch = branch;
+
+        if (branch != 0) {
+            double* INC = p.buf[kBufT0];
+            if (branch == 3) {
+                // incr = b + 0.5*t*(A b)   (expact.cpp:117-121)
+                const double ht = __dmul_rn(0.5, t);
+                stencil(kBufG, -1, -1, [&](int64_t v, double acc, double b, double, double) {
+                    const double incr = __dadd_rn(b, __dmul_rn(ht, acc));
+                    if (run) INC[v] = incr;
+                    else OUT[v] = incr;
+                });
+                if (run) gsync();
+            }
+            if (run) {
+                double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
+                sweep_points(op, [&](int64_t v) {
+                    const double incr = branch == 1 ? G[v] : branch == 2 ? 0.0 : INC[v];
+                    const double un = __dadd_rn(U[v], __dmul_rn(t, incr));
+                    U[v] = un;
+                    if (p.want_metrics) metrics_local(sum, mx, mn, r2, v, un);
+                });
+                if (p.want_metrics) metrics_push(sum, mx, mn, r2, (step + 1) & 1);
+                gsync();
+                if (p.want_metrics) metrics_finish(step + 1, (step + 1) & 1);
+            } else if (branch != 3) {
+                sweep_points(op, [&](int64_t v) { OUT[v] = branch == 1 ? G[v] : 0.0; });
+            }
+            continue;
+        }
+
+        // ------------------------------------------- bordered column b/gamma and (s, m)
+        double gamma = 0.0, norm_tA;
+        if (bordered) {
+            gamma = __ddiv_rn(bnorm, p.anorm);  // expact.cpp:126
+            double csum = 0.0;
+            sweep_points(op, [&](int64_t v) {
+                const double b = G[v];
+                const double bg = (b != 0.0) ? __ddiv_rn(b, gamma) : 0.0;  // expact.cpp:137-138
+                G[v] = bg;
+                csum = __dadd_rn(csum, fabs(bg));
+            });
+            double s[1] = {csum};
+            block_reduce<1, false>(s, sm);
+            if (threadIdx.x == 0) p.part_c[blockIdx.x] = s[0];
+            gsync();
+            const double coln = grid_sum(p.part_c, p.grid_blocks, sm);
+            // bordered ||.||_1 = max over columns: A's columns, then column n (sparse.cpp:39-40)
+            norm_tA = __dmul_rn(fabs(t), nan_dropping_max(p.anorm, coln));
+            if (info) {
+                info->coln = coln;
+                info->gamma = gamma;
+            }
+        } else {
+            norm_tA = __dmul_rn(fabs(t), p.anorm);
+        }
+        int s_st = 1, m_deg = 1;
+        const int sel = select_params_dev(norm_tA, p.rtab, &s_st, &m_deg);
+        if (info) {
+            info->norm_tA = norm_tA;
+            info->s = s_st;
+            info->m = m_deg;
+        }
+        if (sel != GS_OK) {
+            if (leader) {
+                p.status[0] = sel;
+                p.status[1] = 1;  // select_params
+            }
+            return;  // uniform across CTAs
+        }
+
+        // ------------------------------------------------------------- K4: Taylor terms
+        const double tau_s = __ddiv_rn(t, static_cast<double>(s_st));  // expact.cpp:73
+        int fcur = bordered ? -1 : kBufG;  // -1: f = e_{n+1} (all zero) for the bordered action
+        int tprev = -1;
+        int fsel = 0, tsel = 0;
+        double prev = prev0;
+        int64_t total_terms = 0;
+        for (int stage = 0; stage < s_st; ++stage) {
+            int used = 0;
+            for (int j = 1; j <= m_deg; ++j) {
+                const double c = __ddiv_rn(tau_s, static_cast<double>(j));  // expact.cpp:83
+                const TermKind kind =
+                    j > 1 ? kNext : (fcur < 0 ? kFirstZero : (bordered ? kFirstBorder : kFirstPlain));
+                const int fout = kBufF0 + fsel;
+                const int tout = kBufT0 + tsel;
+                double* Fo = p.buf[fout];
+                double* To = p.buf[tout];
+                double mt = 0.0, mf = 0.0;
+                // term = c * (A~ term); f += term   (expact.cpp:82-87)
+                auto emit = [&](int64_t v, double sc, double fin) {
+                    const double tn = __dmul_rn(c, sc);
+                    const double fn = __dadd_rn(fin, tn);
+                    To[v] = tn;
+                    Fo[v] = fn;
+                    mt = nan_dropping_max(mt, fabs(tn));
+                    mf = nan_dropping_max(mf, fabs(fn));
+                };
+                if (kind == kFirstZero) {
+                    // A~ e_{n+1} = the border column b/gamma; f was e_{n+1}
+                    sweep_points(op, [&](int64_t v) { emit(v, __dadd_rn(0.0, G[v]), 0.0); });
+                } else if (kind == kFirstBorder) {
+                    // the border entry (column n, b_i/gamma) is last in its row; term_n = 1 only
+                    // on a stage's first term (expact.cpp:137-138, :96)
+                    stencil(fcur, -1, kBufG, [&](int64_t v, double acc, double f, double, double bg) {
+                        emit(v, __dadd_rn(acc, bg), f);
+                    });
+                } else if (kind == kFirstPlain) {
+                    stencil(fcur, -1, -1, [&](int64_t v, double acc, double f, double, double) { emit(v, acc, f); });
+                } else {
+                    stencil(tprev, fcur, -1, [&](int64_t v, double acc, double, double f, double) { emit(v, acc, f); });
+                }
+                push_max2(mt, mf);
+                sync_round();
+                ++used;
+                fcur = fout;
+                tprev = tout;
+                fsel ^= 1;
+                tsel ^= 1;
+                const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
+                const double cur = slot_read(sl + 0);
+                double fnorm = slot_read(sl + 1);
+                if (bordered) fnorm = nan_dropping_max(fnorm, 1.0);  // f_n == 1 (expact.cpp:89)
+                if (!isfinite(cur) || !isfinite(fnorm)) {             // expact.cpp:90-91
+                    if (leader) {
+                        p.status[0] = GS_ENUMERIC;
+                        p.status[1] = 2;
+                    }
+                    return;
+                }
+                if (__dadd_rn(prev, cur) <= __dmul_rn(p.tol, fnorm)) {  // expact.cpp:93
+                    prev = fnorm;  // next stage: term = f, ||term|| = ||f|| (expact.cpp:80, :96)
+                    break;
+                }
+                prev = (j == m_deg) ? fnorm : cur;
+            }
+            total_terms += used;
+            if (info && stage < kMaxLoggedStages) info->terms[stage] = used;
+        }
+        if (info) info->total_terms = total_terms;
+
+        // ------------------------------------------------ K5: output / update + metrics
+        const double* F = p.buf[fcur];
+        if (run) {
+            const double scl = __ddiv_rn(gamma, t);  // expact.cpp:150
+            double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
+            sweep_points(op, [&](int64_t v) {
+                // out = u + tau * (scale * y)   (integrator.cpp:59-61, expact.cpp:151)
+                const double un = __dadd_rn(U[v], __dmul_rn(t, __dmul_rn(scl, F[v])));
+                U[v] = un;
+                if (p.want_metrics) metrics_local(sum, mx, mn, r2, v, un);
+            });
+            if (p.want_metrics) metrics_push(sum, mx, mn, r2, (step + 1) & 1);
+            gsync();
+            if (p.want_metrics) metrics_finish(step + 1, (step + 1) & 1);
+        } else {
+            const double scale = bordered ? __ddiv_rn(gamma, t) : 1.0;
+            sweep_points(op, [&](int64_t v) { OUT[v] = bordered ? __dmul_rn(scale, F[v]) : F[v]; });
+        }
+    }
+}
+
+}  // namespace gs

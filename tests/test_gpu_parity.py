@@ -280,3 +280,32 @@ def test_mid_size_step_vs_oracle(G, port):
             ref_plain, _ = port.step(op_o, u, 0.025, 33.5, 1e-8)
             assert rel_l2(got, ref_plain) <= STEP_TOL
             u = got
+
+
+# ---- both stencil sweep paths (TMA z-slab ring and the L1 fallback) on awkward shapes ------
+
+TMA_SHAPES = [(48, 32, 20), (80, 40, 12), (64, 48, 1), (32, 32, 32), (16, 16, 16), (96, 17, 9), (128, 16, 3)]
+
+
+@pytest.mark.parametrize("shape", TMA_SHAPES)
+@pytest.mark.parametrize("tma", [True, False])
+def test_sweep_paths_vs_oracle(G, port, shape, tma, monkeypatch):
+    if not tma:
+        monkeypatch.setenv("GS_DISABLE_TMA", "1")
+    rng = np.random.default_rng(sum(shape))
+    n = int(np.prod(shape))
+    table = np.array([0.0, 0.13, 0.013, 0.05])
+    d = table[rng.integers(0, 4, n)]
+    h = 2.0
+    op_o = port.stencil(shape, h, d)
+    x = rng.uniform(-1, 1, n)
+    u = rng.uniform(0, 1, n)
+    with G.assemble_diffusion(G.Grid(*shape, h=h), d) as op:
+        assert np.array_equal(op.apply(x), port.apply(op_o, x))
+        got, info = G.step(op, u, 0.1, 33.5, 1e-9, info=True)
+        want, log = port.step(op_o, u, 0.1, 33.5, 1e-9, bnorm=info.bnorm, coln=info.coln)
+        assert np.array_equal(got, want)
+        assert info.stage_terms() == log.stage_terms()
+        got_e = G.expmv(20.0, op, x, 1e-10)
+        want_e, _ = port.expmv(20.0, op_o, x, 1e-10)
+        assert np.array_equal(got_e, want_e)
