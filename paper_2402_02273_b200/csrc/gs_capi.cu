@@ -128,8 +128,8 @@ void plan_items(gs_ctx* c) {
     c->grid_blocks = grid;
 }
 
-// TMA descriptors over the x-fastest arrays: halo boxes (TX+2)x(TY+2)x1 starting one voxel
-// outside the tile (out-of-bounds elements read as 0.0), own boxes TXxTYx1, labels as u8.
+// TMA descriptors over the x-fastest arrays: halo boxes (TX+4)x(TY+2)x1 starting two voxels
+// left of / one row below the tile (out-of-bounds elements read as 0.0), own boxes TXxTYx1, labels as u8.
 gs_status build_tensor_maps(gs_ctx* c) {
     c->tma_ok = false;
     if (c->nx % 16 != 0) return GS_OK;  // u8 label rows need 16-byte pitch
@@ -146,7 +146,7 @@ gs_status build_tensor_maps(gs_ctx* c) {
                                 static_cast<cuuint64_t>(c->nz)};
     const cuuint64_t st8[2] = {static_cast<cuuint64_t>(c->nx) * 8, static_cast<cuuint64_t>(c->nx) * c->ny * 8};
     const cuuint64_t st1[2] = {static_cast<cuuint64_t>(c->nx), static_cast<cuuint64_t>(c->nx) * c->ny};
-    const cuuint32_t halo[3] = {gs::kTmaTX + 2, gs::kTmaTY + 2, 1};
+    const cuuint32_t halo[3] = {gs::kXPitch, gs::kTmaTY + 2, 1};
     const cuuint32_t own[3] = {gs::kTmaTX, gs::kTmaTY, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     DevBuf* bufs[gs::kNumBufs] = {&c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out};

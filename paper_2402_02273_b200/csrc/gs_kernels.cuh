@@ -26,7 +26,10 @@ constexpr int kTmaTY = 16;
 constexpr int kTmaStages = 6;
 constexpr int kSolveThreads = 512;   // 16 warps: warp w owns tile row w, two columns per lane
 
-constexpr int kXPitch = kTmaTX + 2;                                    // doubles per halo row
+// The halo box starts two voxels left of the tile: TMA needs the innermost start coordinate
+// times the element size to be a multiple of 16 bytes (measured: x0-1 faults on sm_100a).
+constexpr int kXHalo = 2;                                              // x halo (left/right)
+constexpr int kXPitch = kTmaTX + 2 * kXHalo;                           // doubles per halo row
 constexpr int kXBytes = ((kTmaTY + 2) * kXPitch * 8 + 127) / 128 * 128;  // halo plane tile
 constexpr int kOBytes = kTmaTX * kTmaTY * 8;                            // own plane tile (fp64)
 constexpr int kLBytes = kTmaTX * kTmaTY;                                // own plane tile (labels)

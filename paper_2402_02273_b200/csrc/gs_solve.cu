@@ -196,7 +196,7 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
             uint64_t* bar = ring.bar + slot;
             const bool own = pl >= z0 && pl < z1;
             mbar_arrive_expect_tx(bar, kHaloBytes + (own ? kOwnBytes : 0));
-            tma_load_3d(ring.x(slot), &p.xmap[xbuf], x0 - 1, y0 - 1, pl, bar);
+            tma_load_3d(ring.x(slot), &p.xmap[xbuf], x0 - kXHalo, y0 - 1, pl, bar);
             if (own) {
                 if (kNeedF) tma_load_3d(ring.f(slot), &p.omap[fbuf], x0, y0, pl, bar);
                 if (kNeedB) tma_load_3d(ring.b(slot), &p.omap[bbuf], x0, y0, pl, bar);
@@ -227,8 +227,8 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const int lx = lane + 32 * c;
-                xm[c] = Xm[(row + 1) * kXPitch + lx + 1];
-                xc[c] = Xc[(row + 1) * kXPitch + lx + 1];
+                xm[c] = Xm[(row + 1) * kXPitch + lx + kXHalo];
+                xc[c] = Xc[(row + 1) * kXPitch + lx + kXHalo];
             }
         }
         for (int z = z0; z < z1; ++z) {
@@ -244,12 +244,12 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
             for (int c = 0; c < 2; ++c) {
                 const int lx = lane + 32 * c;
                 const int i = ii[c];
-                const double xp = Xp[(row + 1) * kXPitch + lx + 1];
+                const double xp = Xp[(row + 1) * kXPitch + lx + kXHalo];
                 if (i < op.nx && j < op.ny) {
-                    const double xym = Xc[row * kXPitch + lx + 1];
-                    const double xyp = Xc[(row + 2) * kXPitch + lx + 1];
-                    const double xxm = Xc[(row + 1) * kXPitch + lx];
-                    const double xxp = Xc[(row + 1) * kXPitch + lx + 2];
+                    const double xym = Xc[row * kXPitch + lx + kXHalo];
+                    const double xyp = Xc[(row + 2) * kXPitch + lx + kXHalo];
+                    const double xxm = Xc[(row + 1) * kXPitch + lx + kXHalo - 1];
+                    const double xxp = Xc[(row + 1) * kXPitch + lx + kXHalo + 1];
                     const int o = row * kTmaTX + lx;
                     RowCoef rc;
                     rc.w = s_wtab[Lo[o]];
