@@ -75,7 +75,8 @@ struct gs_ctx {
     bool tma_ok = false;          // TMA descriptors built (nx % 16 == 0)
     CUtensorMap xmap[gs::kNumBufs];
     CUtensorMap omap[gs::kNumBufs];
-    CUtensorMap lmap;
+    CUtensorMap x2map[gs::kNumBufs];
+    CUtensorMap lmap, l2map;
     std::string err;
 };
 
@@ -148,22 +149,31 @@ gs_status build_tensor_maps(gs_ctx* c) {
     const cuuint64_t st1[2] = {static_cast<cuuint64_t>(c->nx), static_cast<cuuint64_t>(c->nx) * c->ny};
     const cuuint32_t halo[3] = {gs::kXPitch, gs::kTmaTY + 2, 1};
     const cuuint32_t own[3] = {gs::kTmaTX, gs::kTmaTY, 1};
+    const cuuint32_t halo2[3] = {gs::kXPitch, gs::k2XRows, 1};
+    const cuuint32_t lhalo[3] = {gs::kLPitch, gs::kTmaTY + 2, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     DevBuf* bufs[gs::kNumBufs] = {&c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out};
     for (int b = 0; b < gs::kNumBufs; ++b) {
         CUresult r = encode(&c->xmap[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, bufs[b]->p, dims, st8, halo, es,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(halo) failed: " + std::to_string(r));
         r = encode(&c->omap[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, bufs[b]->p, dims, st8, own, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(own) failed: " + std::to_string(r));
+        r = encode(&c->x2map[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, bufs[b]->p, dims, st8, halo2, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(halo2) failed: " + std::to_string(r));
     }
     CUresult r = encode(&c->lmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, c->pal.p, dims, st1, own, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(labels) failed: " + std::to_string(r));
+    r = encode(&c->l2map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, c->pal.p, dims, st1, lhalo, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(labels halo) failed: " + std::to_string(r));
     c->tma_ok = true;
     return GS_OK;
 }
@@ -263,8 +273,10 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
         for (int b = 0; b < gs::kNumBufs; ++b) {
             p.xmap[b] = c->xmap[b];
             p.omap[b] = c->omap[b];
+            p.x2map[b] = c->x2map[b];
         }
         p.lmap = c->lmap;
+        p.l2map = c->l2map;
     }
     p.metrics = metrics ? c->metrics.as<double>() : nullptr;
     p.want_metrics = metrics ? 1 : 0;
@@ -279,7 +291,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     for (int b = 0; b < gs::kNumBufs; ++b) p.buf[b] = bufs[b]->as<double>();
     void* args[] = {&p};
     GS_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gs::solve_kernel), dim3(gb),
-                                           dim3(gs::kSolveThreads), args, p.use_tma ? gs::kRingBytes : 0,
+                                           dim3(gs::kSolveThreads), args, p.use_tma ? gs::kDynSmemBytes : 0,
                                            c->stream));
     int status[2] = {0, 0};
     GS_CUDA(c, cudaMemcpyAsync(status, c->status.p, sizeof status, cudaMemcpyDeviceToHost, c->stream));
@@ -342,12 +354,12 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
         return GS_ECUDA;
     }
     c->num_sms = prop.multiProcessorCount;
-    if ((e = cudaFuncSetAttribute(gs::solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kRingBytes)) !=
+    if ((e = cudaFuncSetAttribute(gs::solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kDynSmemBytes)) !=
         cudaSuccess)
         return bail(e, "cudaFuncSetAttribute(smem)");
     int per_sm = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::solve_kernel, gs::kSolveThreads,
-                                                           gs::kRingBytes)) != cudaSuccess)
+                                                           gs::kDynSmemBytes)) != cudaSuccess)
         return bail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) {
         g_create_error = "gs_create: solve kernel does not fit on an SM";

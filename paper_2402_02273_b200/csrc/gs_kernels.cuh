@@ -36,11 +36,31 @@ constexpr int kLBytes = kTmaTX * kTmaTY;                                // own p
 constexpr int kSlotBytes = kXBytes + 2 * kOBytes + kLBytes;
 constexpr int kRingBytes = kTmaStages * kSlotBytes + 128;              // + barriers
 
+// Two-term fused sweep (temporal blocking): T_{j+1} is computed on the tile plus a one-voxel
+// halo and kept in a 3-plane shared ring, T_{j+2} on the tile; the input therefore needs a
+// two-voxel halo in x, y and z.
+constexpr int k2Stages = 5;
+constexpr int k2XRows = kTmaTY + 4;                                     // y halo 2
+constexpr int k2XBytes = (k2XRows * kXPitch * 8 + 127) / 128 * 128;    // 20 x 68 doubles
+constexpr int k2BRows = kTmaTY + 2;                                     // y halo 1
+constexpr int k2BBytes = (k2BRows * kXPitch * 8 + 127) / 128 * 128;    // 18 x 68 doubles
+constexpr int kLHaloX = 16;                                             // u8 box: 16-byte aligned start
+constexpr int kLPitch = kTmaTX + 2 * kLHaloX;                           // 96 labels per halo row
+constexpr int k2LBytes = ((kTmaTY + 2) * kLPitch + 127) / 128 * 128;   // 18 x 96 labels
+constexpr int k2SlotBytes = k2XBytes + kOBytes + k2BBytes + k2LBytes;
+constexpr int kT1Pitch = kTmaTX + 2;
+constexpr int kT1Rows = kTmaTY + 2;
+constexpr int kT1Bytes = kT1Rows * kT1Pitch * 8;
+constexpr int k2RingBytes = k2Stages * k2SlotBytes + 3 * kT1Bytes + 128;
+constexpr int kDynSmemBytes = kRingBytes > k2RingBytes ? kRingBytes : k2RingBytes;
+
 struct SolveParams {
     // TMA descriptors (64-byte aligned by type): halo-box and own-box maps per vector, labels
     CUtensorMap xmap[kNumBufs];
     CUtensorMap omap[kNumBufs];
+    CUtensorMap x2map[kNumBufs];   // halo-2 boxes (fused two-term sweep)
     CUtensorMap lmap;
+    CUtensorMap l2map;             // labels with a one-voxel halo
     StencilOp op;
     int use_tma;
     int mode;

@@ -35,6 +35,8 @@ struct Smem {
     double wtab[256];
     double red[kSolveThreads / 32][4];
     double bcast[4];
+    uint64_t bar1[kTmaStages];  // single-term ring
+    uint64_t bar2[k2Stages];    // fused two-term ring
 };
 
 struct Ring {
@@ -273,6 +275,199 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
     fence_proxy_async_global();  // this thread's generic writes -> later TMA reads
 }
 
+// ------------------------------------------------------------------------------------------
+// Two-term fused TMA sweep (temporal blocking)
+// ------------------------------------------------------------------------------------------
+// One pass over HBM computes two consecutive Taylor terms (expact.cpp:81-95 twice):
+//   T1 = c1 * (A~ X)          on the tile plus a one-voxel halo, per plane, into a 3-plane
+//                             shared ring (OOB points hold 0.0, i.e. missing neighbours)
+//   T2 = c2 * (A T1)          on the tile
+//   F1 = Fprev + T1, F2 = F1 + T2  (the reference's f += term, same operations, same order)
+// and writes T2 and F1; F2 = F1 + T2 stays implicit (recomputed bit-exactly by its consumer).
+// The four maxima |T1|, |F1|, |T2|, |F2| feed the two termination tests.
+//
+// Kinds:   first-zero    stage 0 of the bordered action: T1 = c1*(0 + b/gamma), Fprev = 0
+//          first-border  stage >= 1: X = f, T1 = c1*(A f + b/gamma), Fprev = f
+//          first-plain   expmv stage start: X = f, T1 = c1*(A f), Fprev = f
+//          next          X = T_j, Fprev = F_{j-1} + T_j (state kept as (T_j, F_{j-1}))
+enum Fused2Kind { k2FirstZero = 0, k2FirstBorder = 1, k2FirstPlain = 2, k2Next = 3 };
+
+struct Ring2 {
+    unsigned char* base;
+    uint64_t* bar;
+    __device__ double* x(int s) const { return reinterpret_cast<double*>(base + s * k2SlotBytes); }
+    __device__ double* f(int s) const { return reinterpret_cast<double*>(base + s * k2SlotBytes + k2XBytes); }
+    __device__ double* b(int s) const {
+        return reinterpret_cast<double*>(base + s * k2SlotBytes + k2XBytes + kOBytes);
+    }
+    __device__ uint8_t* l(int s) const { return base + s * k2SlotBytes + k2XBytes + kOBytes + k2BBytes; }
+    __device__ double* t1(int q) const {
+        return reinterpret_cast<double*>(base + k2Stages * k2SlotBytes + q * kT1Bytes);
+    }
+};
+
+__device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ring, int kind, int xbuf, int fbuf,
+                                           int bbuf, double c1, double c2, double* outT, double* outF,
+                                           double (&mx)[4], uint32_t& seq, const double* s_wtab) {
+    const StencilOp& op = p.op;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, row = tid >> 5;
+    const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
+    const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
+    const int64_t Q = static_cast<int64_t>(tiles_x) * tiles_y * op.nz;
+    const int64_t q_begin = static_cast<int64_t>(blockIdx.x) * Q / gridDim.x;
+    const int64_t q_end = static_cast<int64_t>(blockIdx.x + 1) * Q / gridDim.x;
+    const bool needX = kind != k2FirstZero;
+    const bool needF = kind == k2Next;
+    const bool needB = kind == k2FirstZero || kind == k2FirstBorder;
+    constexpr uint32_t kXTx = k2XRows * kXPitch * 8;
+    constexpr uint32_t kBTx = k2BRows * kXPitch * 8;
+    constexpr uint32_t kLTx = (kTmaTY + 2) * kLPitch;
+    if (tid == 0) fence_proxy_async_global();
+
+    for (int64_t q = q_begin; q < q_end;) {
+        const int64_t tile = q / op.nz;
+        const int z0 = static_cast<int>(q % op.nz);
+        const int z1 = static_cast<int>(min(static_cast<int64_t>(op.nz), static_cast<int64_t>(z0) + (q_end - q)));
+        q += z1 - z0;
+        const int x0 = static_cast<int>(tile % tiles_x) * kTmaTX;
+        const int y0 = static_cast<int>(tile / tiles_x) * kTmaTY;
+        const uint32_t base = seq;
+        const int pfirst = z0 - 2, plast = z1 + 1;  // planes loaded
+        const int np = plast - pfirst + 1;
+
+        auto seq_of = [&](int pl) { return base + static_cast<uint32_t>(pl - pfirst); };
+        auto slot_of = [&](int pl) { return static_cast<int>(seq_of(pl) % k2Stages); };
+        auto issue = [&](int pl) {
+            const uint32_t sq = seq_of(pl);
+            const int slot = static_cast<int>(sq % k2Stages);
+            uint64_t* bar = ring.bar + slot;
+            const bool ownF = needF && pl >= z0 && pl < z1;
+            const bool haloB = needB && pl >= z0 - 1 && pl <= z1;
+            const bool haloL = pl >= z0 - 1 && pl <= z1;
+            const uint32_t bytes = (needX ? kXTx : 0) + (ownF ? kOBytes : 0) + (haloB ? kBTx : 0) + (haloL ? kLTx : 0);
+            mbar_arrive_expect_tx(bar, bytes);
+            if (needX) tma_load_3d(ring.x(slot), &p.x2map[xbuf], x0 - kXHalo, y0 - 2, pl, bar);
+            if (ownF) tma_load_3d(ring.f(slot), &p.omap[fbuf], x0, y0, pl, bar);
+            if (haloB) tma_load_3d(ring.b(slot), &p.xmap[bbuf], x0 - kXHalo, y0 - 1, pl, bar);
+            if (haloL) tma_load_3d(ring.l(slot), &p.l2map, x0 - kLHaloX, y0 - 1, pl, bar);
+        };
+        auto wait_plane = [&](int pl) {
+            const uint32_t sq = seq_of(pl);
+            mbar_wait(ring.bar + sq % k2Stages, (sq / k2Stages) & 1u);
+        };
+
+        if (tid == 0) {
+            const int pre = min(k2Stages, np);
+            for (int k = 0; k < pre; ++k) issue(pfirst + k);
+        }
+
+        // Phase A: T1 on the halo-1 region of plane pl (needs X planes pl-1..pl+1, labels and
+        // b/gamma of plane pl).  Ring slot of T1(pl) = pl mod 3 (pl + 3 keeps it non-negative).
+        auto phaseA = [&](int pl) {
+            double* T1 = ring.t1((pl + 3) % 3);
+            const bool zin = pl >= 0 && pl < op.nz;
+            const double* Xm = needX ? ring.x(slot_of(pl - 1)) : nullptr;
+            const double* Xc = needX ? ring.x(slot_of(pl)) : nullptr;
+            const double* Xp = needX ? ring.x(slot_of(pl + 1)) : nullptr;
+            const uint8_t* L = ring.l(slot_of(pl));
+            const double* B = needB ? ring.b(slot_of(pl)) : nullptr;
+            const bool hz0 = pl > 0, hz1 = pl < op.nz - 1;
+            for (int qq = tid; qq < kT1Rows * kT1Pitch; qq += kSolveThreads) {
+                const int r = qq / kT1Pitch, cc = qq - r * kT1Pitch;
+                const int gx = x0 - 1 + cc, gy = y0 - 1 + r;
+                double val = 0.0;
+                if (zin && gx >= 0 && gx < op.nx && gy >= 0 && gy < op.ny) {
+                    RowCoef rc;
+                    rc.w = s_wtab[L[r * kLPitch + cc + kLHaloX - 1]];
+                    rc.live = rc.w != 0.0;
+                    double sc;
+                    if (kind == k2FirstZero) {
+                        sc = __dadd_rn(0.0, B[r * kXPitch + cc + 1]);
+                    } else {
+                        const int xi = (r + 1) * kXPitch + cc + 1;  // X tile origin (x0-2, y0-2)
+                        const int cnt = (gx > 0) + (gx < op.nx - 1) + (gy > 0) + (gy < op.ny - 1) + hz0 + hz1;
+                        sc = row_apply(rc, cnt, Xm[xi], Xc[xi - kXPitch], Xc[xi - 1], Xc[xi], Xc[xi + 1],
+                                       Xc[xi + kXPitch], Xp[xi]);
+                        if (kind == k2FirstBorder) sc = __dadd_rn(sc, B[r * kXPitch + cc + 1]);
+                    }
+                    val = __dmul_rn(c1, sc);
+                }
+                T1[qq] = val;
+            }
+        };
+
+        // prologue: T1 for planes z0-1 and z0
+        wait_plane(z0 - 2);
+        wait_plane(z0 - 1);
+        wait_plane(z0);
+        phaseA(z0 - 1);
+        wait_plane(z0 + 1);
+        phaseA(z0);
+        __syncthreads();
+        if (tid == 0) {
+            if (pfirst + k2Stages <= plast) issue(pfirst + k2Stages);
+            if (pfirst + 1 + k2Stages <= plast) issue(pfirst + 1 + k2Stages);
+        }
+
+        const int j = y0 + row;
+        const bool hy0 = j > 0, hy1 = j < op.ny - 1;
+        for (int z = z0; z < z1; ++z) {
+            wait_plane(z + 2);
+            phaseA(z + 1);
+            __syncthreads();
+            // Phase B: own voxels of plane z
+            const double* T1m = ring.t1((z + 2) % 3);
+            const double* T1c = ring.t1(z % 3);
+            const double* T1p = ring.t1((z + 1) % 3);
+            const int sc_ = slot_of(z);
+            const double* Xc = ring.x(sc_);
+            const double* Fo = ring.f(sc_);
+            const uint8_t* L = ring.l(sc_);
+            const bool hz0 = z > 0, hz1 = z < op.nz - 1;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int lx = lane + 32 * c;
+                const int i = x0 + lx;
+                if (i < op.nx && j < op.ny) {
+                    const int ti = (row + 1) * kT1Pitch + lx + 1;
+                    RowCoef rc;
+                    rc.w = s_wtab[L[(row + 1) * kLPitch + lx + kLHaloX]];
+                    rc.live = rc.w != 0.0;
+                    const int cnt = (i > 0) + (i < op.nx - 1) + hy0 + hy1 + hz0 + hz1;
+                    const double t1 = T1c[ti];
+                    const double acc = row_apply(rc, cnt, T1m[ti], T1c[ti - kT1Pitch], T1c[ti - 1], t1, T1c[ti + 1],
+                                                 T1c[ti + kT1Pitch], T1p[ti]);
+                    const double t2 = __dmul_rn(c2, acc);
+                    double fprev;
+                    if (kind == k2FirstZero) {
+                        fprev = 0.0;
+                    } else {
+                        const double xc = Xc[(row + 2) * kXPitch + lx + kXHalo];
+                        fprev = (kind == k2Next) ? __dadd_rn(Fo[row * kTmaTX + lx], xc) : xc;
+                    }
+                    const double f1 = __dadd_rn(fprev, t1);
+                    const double f2 = __dadd_rn(f1, t2);
+                    const int64_t v = i + static_cast<int64_t>(j) * op.sy + static_cast<int64_t>(z) * op.sz;
+                    outT[v] = t2;
+                    outF[v] = f1;
+                    mx[0] = nan_dropping_max(mx[0], fabs(t1));
+                    mx[1] = nan_dropping_max(mx[1], fabs(f1));
+                    mx[2] = nan_dropping_max(mx[2], fabs(t2));
+                    mx[3] = nan_dropping_max(mx[3], fabs(f2));
+                }
+            }
+            __syncthreads();  // plane z's slot and T1(z-1) are free
+            if (tid == 0) {
+                const int nxt = z + k2Stages;  // slot of plane z is reused for plane z + stages
+                if (nxt <= plast) issue(nxt);
+            }
+        }
+        seq = base + static_cast<uint32_t>(np);
+    }
+    fence_proxy_async_global();
+}
+
 enum TermKind { kFirstZero, kFirstBorder, kFirstPlain, kNext };
 
 }  // namespace
@@ -284,14 +479,16 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
     const StencilOp& op = p.op;
     if (op.pal)
         for (int q = threadIdx.x; q < 256; q += blockDim.x) sm.wtab[q] = __ldg(op.wtab + q);
-    Ring ring{dyn, reinterpret_cast<uint64_t*>(dyn + kTmaStages * kSlotBytes)};
+    Ring ring{dyn, sm.bar1};
+    Ring2 ring2{dyn, sm.bar2};
     if (p.use_tma && threadIdx.x == 0) {
-        for (int s = 0; s < kTmaStages; ++s) mbar_init(ring.bar + s, 1);
+        for (int s = 0; s < kTmaStages; ++s) mbar_init(sm.bar1 + s, 1);
+        for (int s = 0; s < k2Stages; ++s) mbar_init(sm.bar2 + s, 1);
         mbar_fence_init();
         for (int b = 0; b < kNumBufs; ++b) tma_prefetch_desc(&p.xmap[b]);
     }
     __syncthreads();
-    uint32_t seq = 0;
+    uint32_t seq = 0, seq2 = 0;
     // Grid barrier; with TMA, first order this thread's generic global writes before any
     // later async-proxy (TMA) read of them.
     auto gsync = [&]() {
@@ -532,82 +729,172 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
 
         // ------------------------------------------------------------- K4: Taylor terms
         const double tau_s = __ddiv_rn(t, static_cast<double>(s_st));  // expact.cpp:73
-        int fcur = bordered ? -1 : kBufG;  // -1: f = e_{n+1} (all zero) for the bordered action
-        int tprev = -1;
-        int fsel = 0, tsel = 0;
         double prev = prev0;
         int64_t total_terms = 0;
-        for (int stage = 0; stage < s_st; ++stage) {
-            int used = 0;
-            for (int j = 1; j <= m_deg; ++j) {
-                const double c = __ddiv_rn(tau_s, static_cast<double>(j));  // expact.cpp:83
-                const TermKind kind =
-                    j > 1 ? kNext : (fcur < 0 ? kFirstZero : (bordered ? kFirstBorder : kFirstPlain));
-                const int fout = kBufF0 + fsel;
-                const int tout = kBufT0 + tsel;
-                double* Fo = p.buf[fout];
-                double* To = p.buf[tout];
-                double mt = 0.0, mf = 0.0;
-                // term = c * (A~ term); f += term   (expact.cpp:82-87)
-                auto emit = [&](int64_t v, double sc, double fin) {
-                    const double tn = __dmul_rn(c, sc);
-                    const double fn = __dadd_rn(fin, tn);
-                    To[v] = tn;
-                    Fo[v] = fn;
-                    mt = nan_dropping_max(mt, fabs(tn));
-                    mf = nan_dropping_max(mf, fabs(fn));
-                };
-                if (kind == kFirstZero) {
-                    // A~ e_{n+1} = the border column b/gamma; f was e_{n+1}
-                    sweep_points(op, [&](int64_t v) { emit(v, __dadd_rn(0.0, G[v]), 0.0); });
-                } else if (kind == kFirstBorder) {
-                    // the border entry (column n, b_i/gamma) is last in its row; term_n = 1 only
-                    // on a stage's first term (expact.cpp:137-138, :96)
-                    stencil(fcur, -1, kBufG, [&](int64_t v, double acc, double f, double, double bg) {
-                        emit(v, __dadd_rn(acc, bg), f);
-                    });
-                } else if (kind == kFirstPlain) {
-                    stencil(fcur, -1, -1, [&](int64_t v, double acc, double f, double, double) { emit(v, acc, f); });
-                } else {
-                    stencil(tprev, fcur, -1, [&](int64_t v, double acc, double, double f, double) { emit(v, acc, f); });
+        int fres = -1, tres = -1;  // stage result: F[fres] (+ T[tres] when tres >= 0, implicit)
+        // Reads the next slot round; returns false (after flagging) on a non-finite series.
+        auto finite_or_fail = [&](double cur, double fnorm) {
+            if (!isfinite(cur) || !isfinite(fnorm)) {  // expact.cpp:90-91
+                if (leader) {
+                    p.status[0] = GS_ENUMERIC;
+                    p.status[1] = 2;
                 }
-                push_max2(mt, mf);
-                sync_round();
-                ++used;
-                fcur = fout;
-                tprev = tout;
-                fsel ^= 1;
-                tsel ^= 1;
-                const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
-                const double cur = slot_read(sl + 0);
-                double fnorm = slot_read(sl + 1);
-                if (bordered) fnorm = nan_dropping_max(fnorm, 1.0);  // f_n == 1 (expact.cpp:89)
-                if (!isfinite(cur) || !isfinite(fnorm)) {             // expact.cpp:90-91
-                    if (leader) {
-                        p.status[0] = GS_ENUMERIC;
-                        p.status[1] = 2;
-                    }
-                    return;
-                }
-                if (__dadd_rn(prev, cur) <= __dmul_rn(p.tol, fnorm)) {  // expact.cpp:93
-                    prev = fnorm;  // next stage: term = f, ||term|| = ||f|| (expact.cpp:80, :96)
-                    break;
-                }
-                prev = (j == m_deg) ? fnorm : cur;
+                return false;
             }
-            total_terms += used;
-            if (info && stage < kMaxLoggedStages) info->terms[stage] = used;
+            return true;
+        };
+        if (p.use_tma) {
+            // Fused two-term sweeps; the decisions are taken term by term exactly as the
+            // reference's loop (expact.cpp:81-95), on the four maxima of each sweep.
+            int fsel = 0, tsel = 0;
+            for (int stage = 0; stage < s_st; ++stage) {
+                int fstart;  // buffer holding this stage's starting f (the stencil input)
+                if (stage == 0) {
+                    fstart = bordered ? -1 : kBufG;
+                } else if (tres >= 0) {
+                    // previous stage ended on its implicit F2: materialise f = F1 + T2
+                    const double* Fa = p.buf[fres];
+                    const double* Tb = p.buf[tres];
+                    const int fo = (fres == kBufF0) ? kBufF1 : kBufF0;
+                    double* Fw = p.buf[fo];
+                    sweep_points(op, [&](int64_t v) { Fw[v] = __dadd_rn(Fa[v], Tb[v]); });
+                    gsync();
+                    fstart = fo;
+                } else {
+                    fstart = fres;
+                }
+                if (fstart == kBufF0) fsel = 1;
+                else if (fstart == kBufF1) fsel = 0;
+                int used = 0;
+                int kind = fstart < 0 ? k2FirstZero : (bordered ? k2FirstBorder : k2FirstPlain);
+                int xb = fstart, fb = -1;
+                bool ended = false;
+                while (!ended) {
+                    const double c1 = __ddiv_rn(tau_s, static_cast<double>(used + 1));  // expact.cpp:83
+                    const double c2 = __ddiv_rn(tau_s, static_cast<double>(used + 2));
+                    const int fout = kBufF0 + fsel, tout = kBufT0 + tsel;
+                    double mx[4] = {0.0, 0.0, 0.0, 0.0};
+                    sweep2_tma(p, ring2, kind, xb < 0 ? 0 : xb, fb < 0 ? 0 : fb, kBufG, c1, c2, p.buf[tout],
+                               p.buf[fout], mx, seq2, sm.wtab);
+                    block_reduce<4, true>(mx, sm);
+                    if (threadIdx.x == 0) {
+                        unsigned long long* sl = p.slots + (round % 3) * 4;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (mx[q] > 0.0) atomicMax(sl + q, static_cast<unsigned long long>(__double_as_longlong(mx[q])));
+                    }
+                    sync_round();
+                    const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
+                    double cur[2] = {slot_read(sl + 0), slot_read(sl + 2)};
+                    double fn[2] = {slot_read(sl + 1), slot_read(sl + 3)};
+                    if (bordered) {
+                        fn[0] = nan_dropping_max(fn[0], 1.0);  // f_n == 1 (expact.cpp:89)
+                        fn[1] = nan_dropping_max(fn[1], 1.0);
+                    }
+                    // term used+1 (result F1, explicit)
+                    ++used;
+                    if (!finite_or_fail(cur[0], fn[0])) return;
+                    if (__dadd_rn(prev, cur[0]) <= __dmul_rn(p.tol, fn[0]) || used == m_deg) {
+                        prev = fn[0];
+                        fres = fout;
+                        tres = -1;
+                        ended = true;
+                        break;
+                    }
+                    prev = cur[0];
+                    // term used+1 (result F2 = F1 + T2, implicit)
+                    ++used;
+                    if (!finite_or_fail(cur[1], fn[1])) return;
+                    if (__dadd_rn(prev, cur[1]) <= __dmul_rn(p.tol, fn[1]) || used == m_deg) {
+                        prev = fn[1];
+                        fres = fout;
+                        tres = tout;
+                        ended = true;
+                        break;
+                    }
+                    prev = cur[1];
+                    kind = k2Next;
+                    xb = tout;
+                    fb = fout;
+                    fsel ^= 1;
+                    tsel ^= 1;
+                }
+                total_terms += used;
+                if (info && stage < kMaxLoggedStages) info->terms[stage] = used;
+            }
+        } else {
+            int fcur = bordered ? -1 : kBufG;  // -1: f = e_{n+1} (all zero) for the bordered action
+            int tprev = -1;
+            int fsel = 0, tsel = 0;
+            for (int stage = 0; stage < s_st; ++stage) {
+                int used = 0;
+                for (int j = 1; j <= m_deg; ++j) {
+                    const double c = __ddiv_rn(tau_s, static_cast<double>(j));  // expact.cpp:83
+                    const TermKind kind =
+                        j > 1 ? kNext : (fcur < 0 ? kFirstZero : (bordered ? kFirstBorder : kFirstPlain));
+                    const int fout = kBufF0 + fsel;
+                    const int tout = kBufT0 + tsel;
+                    double* Fo = p.buf[fout];
+                    double* To = p.buf[tout];
+                    double mt = 0.0, mf = 0.0;
+                    // term = c * (A~ term); f += term   (expact.cpp:82-87)
+                    auto emit = [&](int64_t v, double sc, double fin) {
+                        const double tn = __dmul_rn(c, sc);
+                        const double fn = __dadd_rn(fin, tn);
+                        To[v] = tn;
+                        Fo[v] = fn;
+                        mt = nan_dropping_max(mt, fabs(tn));
+                        mf = nan_dropping_max(mf, fabs(fn));
+                    };
+                    if (kind == kFirstZero) {
+                        // A~ e_{n+1} = the border column b/gamma; f was e_{n+1}
+                        sweep_points(op, [&](int64_t v) { emit(v, __dadd_rn(0.0, G[v]), 0.0); });
+                    } else if (kind == kFirstBorder) {
+                        // the border entry (column n, b_i/gamma) is last in its row; term_n = 1 only
+                        // on a stage's first term (expact.cpp:137-138, :96)
+                        stencil(fcur, -1, kBufG, [&](int64_t v, double acc, double f, double, double bg) {
+                            emit(v, __dadd_rn(acc, bg), f);
+                        });
+                    } else if (kind == kFirstPlain) {
+                        stencil(fcur, -1, -1, [&](int64_t v, double acc, double f, double, double) { emit(v, acc, f); });
+                    } else {
+                        stencil(tprev, fcur, -1, [&](int64_t v, double acc, double, double f, double) { emit(v, acc, f); });
+                    }
+                    push_max2(mt, mf);
+                    sync_round();
+                    ++used;
+                    fcur = fout;
+                    tprev = tout;
+                    fsel ^= 1;
+                    tsel ^= 1;
+                    const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
+                    const double cur = slot_read(sl + 0);
+                    double fnorm = slot_read(sl + 1);
+                    if (bordered) fnorm = nan_dropping_max(fnorm, 1.0);  // f_n == 1 (expact.cpp:89)
+                    if (!finite_or_fail(cur, fnorm)) return;
+                    if (__dadd_rn(prev, cur) <= __dmul_rn(p.tol, fnorm)) {  // expact.cpp:93
+                        prev = fnorm;  // next stage: term = f, ||term|| = ||f|| (expact.cpp:80, :96)
+                        break;
+                    }
+                    prev = (j == m_deg) ? fnorm : cur;
+                }
+                total_terms += used;
+                if (info && stage < kMaxLoggedStages) info->terms[stage] = used;
+            }
+                fres = fcur;
         }
         if (info) info->total_terms = total_terms;
 
         // ------------------------------------------------ K5: output / update + metrics
-        const double* F = p.buf[fcur];
+        const double* F = p.buf[fres];
+        const double* TI = tres >= 0 ? p.buf[tres] : nullptr;  // implicit F2 = F1 + T2
+        auto yv = [&](int64_t v) { return TI ? __dadd_rn(F[v], TI[v]) : F[v]; };
         if (run) {
             const double scl = __ddiv_rn(gamma, t);  // expact.cpp:150
             double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
             sweep_points(op, [&](int64_t v) {
                 // out = u + tau * (scale * y)   (integrator.cpp:59-61, expact.cpp:151)
-                const double un = __dadd_rn(U[v], __dmul_rn(t, __dmul_rn(scl, F[v])));
+                const double un = __dadd_rn(U[v], __dmul_rn(t, __dmul_rn(scl, yv(v))));
                 U[v] = un;
                 if (p.want_metrics) metrics_local(sum, mx, mn, r2, v, un);
             });
@@ -616,7 +903,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             if (p.want_metrics) metrics_finish(step + 1, (step + 1) & 1);
         } else {
             const double scale = bordered ? __ddiv_rn(gamma, t) : 1.0;
-            sweep_points(op, [&](int64_t v) { OUT[v] = bordered ? __dmul_rn(scale, F[v]) : F[v]; });
+            sweep_points(op, [&](int64_t v) { OUT[v] = bordered ? __dmul_rn(scale, yv(v)) : yv(v); });
         }
     }
 }
