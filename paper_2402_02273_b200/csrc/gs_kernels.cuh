@@ -39,7 +39,7 @@ constexpr int kRingBytes = kTmaStages * kSlotBytes + 128;              // + barr
 // Two-term fused sweep (temporal blocking): T_{j+1} is computed on the tile plus a one-voxel
 // halo and kept in a 3-plane shared ring, T_{j+2} on the tile; the input therefore needs a
 // two-voxel halo in x, y and z.
-constexpr int k2Stages = 5;
+constexpr int k2Stages = 6;
 constexpr int k2XRows = kTmaTY + 4;                                     // y halo 2
 constexpr int k2XBytes = (k2XRows * kXPitch * 8 + 127) / 128 * 128;    // 20 x 68 doubles
 constexpr int k2BRows = kTmaTY + 2;                                     // y halo 1
@@ -51,7 +51,8 @@ constexpr int k2SlotBytes = k2XBytes + kOBytes + k2BBytes + k2LBytes;
 constexpr int kT1Pitch = kTmaTX + 2;
 constexpr int kT1Rows = kTmaTY + 2;
 constexpr int kT1Bytes = kT1Rows * kT1Pitch * 8;
-constexpr int k2RingBytes = k2Stages * k2SlotBytes + 3 * kT1Bytes + 128;
+constexpr int kT1Planes = 2;  // T1(z) is read from shared memory only in the iteration after it is written
+constexpr int k2RingBytes = k2Stages * k2SlotBytes + kT1Planes * kT1Bytes + 128;
 constexpr int kDynSmemBytes = kRingBytes > k2RingBytes ? kRingBytes : k2RingBytes;
 
 struct SolveParams {

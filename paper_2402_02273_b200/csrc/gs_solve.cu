@@ -309,9 +309,14 @@ struct Ring2 {
 __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ring, int kind, int xbuf, int fbuf,
                                            int bbuf, double c1, double c2, double* outT, double* outF,
                                            double (&mx)[4], uint32_t& seq, const double* s_wtab) {
+    // Register-blocked layout: thread t owns column xl = t % 64 and rows ry0 = 2*(t/64), ry0+1 of
+    // the 64 x 16 tile for the whole z-march, so its z-1/z/z+1 values of X and T1 and its own
+    // y-neighbour live in registers; x-neighbours and the outer y-neighbours come from shared
+    // memory.  The 164 halo-ring points of T1 are computed by threads 0..163 from shared memory.
     const StencilOp& op = p.op;
     const int tid = threadIdx.x;
-    const int lane = tid & 31, row = tid >> 5;
+    const int xl = tid & (kTmaTX - 1);
+    const int ry0 = 2 * (tid / kTmaTX);
     const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
     const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
     const int64_t Q = static_cast<int64_t>(tiles_x) * tiles_y * op.nz;
@@ -323,6 +328,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
     constexpr uint32_t kXTx = k2XRows * kXPitch * 8;
     constexpr uint32_t kBTx = k2BRows * kXPitch * 8;
     constexpr uint32_t kLTx = (kTmaTY + 2) * kLPitch;
+    constexpr int kRing = 2 * (kTmaTX + 2) + 2 * kTmaTY;  // 164 halo-ring points of T1
     if (tid == 0) fence_proxy_async_global();
 
     for (int64_t q = q_begin; q < q_end;) {
@@ -362,22 +368,74 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             for (int k = 0; k < pre; ++k) issue(pfirst + k);
         }
 
-        // Phase A: T1 on the halo-1 region of plane pl (needs X planes pl-1..pl+1, labels and
-        // b/gamma of plane pl).  Ring slot of T1(pl) = pl mod 3 (pl + 3 keeps it non-negative).
-        auto phaseA = [&](int pl) {
-            double* T1 = ring.t1((pl + 3) % 3);
+        const int gx = x0 + xl;
+        const int gy0 = y0 + ry0;
+        const bool inx = gx < op.nx;
+        const bool in_r[2] = {inx && gy0 < op.ny, inx && gy0 + 1 < op.ny};
+        const bool hx0 = gx > 0, hx1 = gx < op.nx - 1;
+        const int hyc[2] = {(gy0 > 0) + (gy0 < op.ny - 1), (gy0 + 1 > 0) + (gy0 + 1 < op.ny - 1)};
+        // own rows' X at planes (p-1, p, p+1) relative to the phase-A plane; own T1 at (z-1, z, z+1)
+        double xa[2] = {0.0, 0.0}, xb[2] = {0.0, 0.0}, xn[2] = {0.0, 0.0};
+        double ta[2] = {0.0, 0.0}, tb[2] = {0.0, 0.0};
+        double lwB[2] = {0.0, 0.0};  // w of plane z (own rows), loaded by phase A of plane z
+        auto load_own_x = [&](int pl, double (&dst)[2]) {
+            if (!needX) return;
+            const double* X = ring.x(slot_of(pl));
+            dst[0] = X[(ry0 + 2) * kXPitch + xl + kXHalo];
+            dst[1] = X[(ry0 + 3) * kXPitch + xl + kXHalo];
+        };
+
+        // Phase A: T1 of plane pl for the own rows (registers xm/xc/xp hold X of planes pl-1, pl,
+        // pl+1) and for the halo ring (from shared memory); writes T1's shared plane.
+        auto phaseA = [&](int pl, const double (&xm)[2], const double (&xc)[2], const double (&xp)[2],
+                          double (&t1)[2], double (&lw)[2]) {
+            double* T1 = ring.t1((pl + 2) % kT1Planes);
             const bool zin = pl >= 0 && pl < op.nz;
-            const double* Xm = needX ? ring.x(slot_of(pl - 1)) : nullptr;
-            const double* Xc = needX ? ring.x(slot_of(pl)) : nullptr;
-            const double* Xp = needX ? ring.x(slot_of(pl + 1)) : nullptr;
-            const uint8_t* L = ring.l(slot_of(pl));
-            const double* B = needB ? ring.b(slot_of(pl)) : nullptr;
-            const bool hz0 = pl > 0, hz1 = pl < op.nz - 1;
-            for (int qq = tid; qq < kT1Rows * kT1Pitch; qq += kSolveThreads) {
-                const int r = qq / kT1Pitch, cc = qq - r * kT1Pitch;
-                const int gx = x0 - 1 + cc, gy = y0 - 1 + r;
+            const int sp = slot_of(pl);
+            const double* Xc = needX ? ring.x(sp) : nullptr;
+            const uint8_t* L = ring.l(sp);
+            const double* B = needB ? ring.b(sp) : nullptr;
+            const int hz = (pl > 0) + (pl < op.nz - 1);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int ry = ry0 + k;
                 double val = 0.0;
-                if (zin && gx >= 0 && gx < op.nx && gy >= 0 && gy < op.ny) {
+                const double w = s_wtab[L[(ry + 1) * kLPitch + xl + kLHaloX]];
+                lw[k] = w;
+                if (zin && in_r[k]) {
+                    RowCoef rc;
+                    rc.w = w;
+                    rc.live = w != 0.0;
+                    double sc;
+                    if (kind == k2FirstZero) {
+                        sc = __dadd_rn(0.0, B[(ry + 1) * kXPitch + xl + kXHalo]);
+                    } else {
+                        const int xi = (ry + 2) * kXPitch + xl + kXHalo;
+                        const double ym = (k == 0) ? Xc[xi - kXPitch] : xc[0];
+                        const double yp = (k == 1) ? Xc[xi + kXPitch] : xc[1];
+                        const int cnt = hx0 + hx1 + hyc[k] + hz;
+                        sc = row_apply(rc, cnt, xm[k], ym, Xc[xi - 1], xc[k], Xc[xi + 1], yp, xp[k]);
+                        if (kind == k2FirstBorder) sc = __dadd_rn(sc, B[(ry + 1) * kXPitch + xl + kXHalo]);
+                    }
+                    val = __dmul_rn(c1, sc);
+                }
+                t1[k] = val;
+                T1[(ry + 1) * kT1Pitch + xl + 1] = val;
+            }
+            if (tid < kRing) {
+                // ring point: rows -1 and 16 (66 each), then columns -1 and 64 for rows 0..15
+                int r, cc;
+                if (tid < 2 * (kTmaTX + 2)) {
+                    r = tid < kTmaTX + 2 ? 0 : kTmaTY + 1;
+                    cc = tid < kTmaTX + 2 ? tid : tid - (kTmaTX + 2);
+                } else {
+                    const int e = tid - 2 * (kTmaTX + 2);
+                    r = 1 + (e >> 1);
+                    cc = (e & 1) ? kTmaTX + 1 : 0;
+                }
+                const int rgx = x0 - 1 + cc, rgy = y0 - 1 + r;
+                double val = 0.0;
+                if (zin && rgx >= 0 && rgx < op.nx && rgy >= 0 && rgy < op.ny) {
                     RowCoef rc;
                     rc.w = s_wtab[L[r * kLPitch + cc + kLHaloX - 1]];
                     rc.live = rc.w != 0.0;
@@ -385,81 +443,92 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                     if (kind == k2FirstZero) {
                         sc = __dadd_rn(0.0, B[r * kXPitch + cc + 1]);
                     } else {
-                        const int xi = (r + 1) * kXPitch + cc + 1;  // X tile origin (x0-2, y0-2)
-                        const int cnt = (gx > 0) + (gx < op.nx - 1) + (gy > 0) + (gy < op.ny - 1) + hz0 + hz1;
+                        const double* Xm = ring.x(slot_of(pl - 1));
+                        const double* Xp = ring.x(slot_of(pl + 1));
+                        const int xi = (r + 1) * kXPitch + cc + 1;
+                        const int cnt = (rgx > 0) + (rgx < op.nx - 1) + (rgy > 0) + (rgy < op.ny - 1) + hz;
                         sc = row_apply(rc, cnt, Xm[xi], Xc[xi - kXPitch], Xc[xi - 1], Xc[xi], Xc[xi + 1],
                                        Xc[xi + kXPitch], Xp[xi]);
                         if (kind == k2FirstBorder) sc = __dadd_rn(sc, B[r * kXPitch + cc + 1]);
                     }
                     val = __dmul_rn(c1, sc);
                 }
-                T1[qq] = val;
+                T1[r * kT1Pitch + cc] = val;
             }
         };
 
-        // prologue: T1 for planes z0-1 and z0
+        // prologue: T1 of planes z0-1 and z0
         wait_plane(z0 - 2);
         wait_plane(z0 - 1);
         wait_plane(z0);
-        phaseA(z0 - 1);
+        double xz[2] = {0.0, 0.0};
+        load_own_x(z0 - 2, xz);
+        load_own_x(z0 - 1, xa);
+        load_own_x(z0, xb);
+        double lwA[2];
+        phaseA(z0 - 1, xz, xa, xb, ta, lwA);
         wait_plane(z0 + 1);
-        phaseA(z0);
+        load_own_x(z0 + 1, xn);
+        phaseA(z0, xa, xb, xn, tb, lwB);
+        // now: xa <- X(z0), xb <- X(z0+1)
+        xa[0] = xb[0];
+        xa[1] = xb[1];
+        xb[0] = xn[0];
+        xb[1] = xn[1];
         __syncthreads();
         if (tid == 0) {
             if (pfirst + k2Stages <= plast) issue(pfirst + k2Stages);
             if (pfirst + 1 + k2Stages <= plast) issue(pfirst + 1 + k2Stages);
         }
 
-        const int j = y0 + row;
-        const bool hy0 = j > 0, hy1 = j < op.ny - 1;
         for (int z = z0; z < z1; ++z) {
             wait_plane(z + 2);
-            phaseA(z + 1);
-            __syncthreads();
-            // Phase B: own voxels of plane z
-            const double* T1m = ring.t1((z + 2) % 3);
-            const double* T1c = ring.t1(z % 3);
-            const double* T1p = ring.t1((z + 1) % 3);
-            const int sc_ = slot_of(z);
-            const double* Xc = ring.x(sc_);
-            const double* Fo = ring.f(sc_);
-            const uint8_t* L = ring.l(sc_);
-            const bool hz0 = z > 0, hz1 = z < op.nz - 1;
+            load_own_x(z + 2, xn);
+            double tc[2];
+            double lwN[2];
+            phaseA(z + 1, xa, xb, xn, tc, lwN);
+            // Phase B: own voxels of plane z; T1(z) in-plane neighbours from shared memory
+            const double* T1s = ring.t1((z + 2) % kT1Planes);
+            const double* Fo = ring.f(slot_of(z));
+            const int hz = (z > 0) + (z < op.nz - 1);
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int lx = lane + 32 * c;
-                const int i = x0 + lx;
-                if (i < op.nx && j < op.ny) {
-                    const int ti = (row + 1) * kT1Pitch + lx + 1;
-                    RowCoef rc;
-                    rc.w = s_wtab[L[(row + 1) * kLPitch + lx + kLHaloX]];
-                    rc.live = rc.w != 0.0;
-                    const int cnt = (i > 0) + (i < op.nx - 1) + hy0 + hy1 + hz0 + hz1;
-                    const double t1 = T1c[ti];
-                    const double acc = row_apply(rc, cnt, T1m[ti], T1c[ti - kT1Pitch], T1c[ti - 1], t1, T1c[ti + 1],
-                                                 T1c[ti + kT1Pitch], T1p[ti]);
-                    const double t2 = __dmul_rn(c2, acc);
-                    double fprev;
-                    if (kind == k2FirstZero) {
-                        fprev = 0.0;
-                    } else {
-                        const double xc = Xc[(row + 2) * kXPitch + lx + kXHalo];
-                        fprev = (kind == k2Next) ? __dadd_rn(Fo[row * kTmaTX + lx], xc) : xc;
-                    }
-                    const double f1 = __dadd_rn(fprev, t1);
-                    const double f2 = __dadd_rn(f1, t2);
-                    const int64_t v = i + static_cast<int64_t>(j) * op.sy + static_cast<int64_t>(z) * op.sz;
-                    outT[v] = t2;
-                    outF[v] = f1;
-                    mx[0] = nan_dropping_max(mx[0], fabs(t1));
-                    mx[1] = nan_dropping_max(mx[1], fabs(f1));
-                    mx[2] = nan_dropping_max(mx[2], fabs(t2));
-                    mx[3] = nan_dropping_max(mx[3], fabs(f2));
-                }
+            for (int k = 0; k < 2; ++k) {
+                if (!in_r[k]) continue;
+                const int ry = ry0 + k;
+                const int ti = (ry + 1) * kT1Pitch + xl + 1;
+                RowCoef rc;
+                rc.w = lwB[k];
+                rc.live = rc.w != 0.0;
+                const double ym = (k == 0) ? T1s[ti - kT1Pitch] : tb[0];
+                const double yp = (k == 1) ? T1s[ti + kT1Pitch] : tb[1];
+                const int cnt = hx0 + hx1 + hyc[k] + hz;
+                const double acc = row_apply(rc, cnt, ta[k], ym, T1s[ti - 1], tb[k], T1s[ti + 1], yp, tc[k]);
+                const double t2 = __dmul_rn(c2, acc);
+                double fprev;
+                if (kind == k2FirstZero) fprev = 0.0;
+                else if (kind == k2Next) fprev = __dadd_rn(Fo[ry * kTmaTX + xl], xa[k]);
+                else fprev = xa[k];
+                const double f1 = __dadd_rn(fprev, tb[k]);
+                const double f2 = __dadd_rn(f1, t2);
+                const int64_t v = gx + static_cast<int64_t>(gy0 + k) * op.sy + static_cast<int64_t>(z) * op.sz;
+                outT[v] = t2;
+                outF[v] = f1;
+                mx[0] = nan_dropping_max(mx[0], fabs(tb[k]));
+                mx[1] = nan_dropping_max(mx[1], fabs(f1));
+                mx[2] = nan_dropping_max(mx[2], fabs(t2));
+                mx[3] = nan_dropping_max(mx[3], fabs(f2));
             }
-            __syncthreads();  // plane z's slot and T1(z-1) are free
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                xa[k] = xb[k];
+                xb[k] = xn[k];
+                ta[k] = tb[k];
+                tb[k] = tc[k];
+                lwB[k] = lwN[k];
+            }
+            __syncthreads();  // plane z's slot and T1(z)'s shared plane are free
             if (tid == 0) {
-                const int nxt = z + k2Stages;  // slot of plane z is reused for plane z + stages
+                const int nxt = z + k2Stages;
                 if (nxt <= plast) issue(nxt);
             }
         }
