@@ -71,6 +71,20 @@ __device__ __forceinline__ double row_apply(const RowCoef& c, int cnt, double xz
     return c.live ? acc : 0.0;   // empty row (stencil.cpp:22)
 }
 
+// Same row with the diagonal's (double)(-cnt) precomputed by the caller (exact small integer).
+__device__ __forceinline__ double row_apply_nc(double w, bool live, double negcnt, double xzm, double xym, double xxm,
+                                               double xc, double xxp, double xyp, double xzp) {
+    const double diag = __dmul_rn(negcnt, w);
+    double acc = __dadd_rn(0.0, __dmul_rn(w, xzm));
+    acc = __dadd_rn(acc, __dmul_rn(w, xym));
+    acc = __dadd_rn(acc, __dmul_rn(w, xxm));
+    acc = __dadd_rn(acc, __dmul_rn(diag, xc));
+    acc = __dadd_rn(acc, __dmul_rn(w, xxp));
+    acc = __dadd_rn(acc, __dmul_rn(w, xyp));
+    acc = __dadd_rn(acc, __dmul_rn(w, xzp));
+    return live ? acc : 0.0;
+}
+
 // ---------------------------------------------------------------------------------
 // Order-free reductions
 // ---------------------------------------------------------------------------------

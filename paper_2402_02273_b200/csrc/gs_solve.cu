@@ -306,29 +306,53 @@ struct Ring2 {
     }
 };
 
-__device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ring, int kind, int xbuf, int fbuf,
-                                           int bbuf, double c1, double c2, double* outT, double* outF,
-                                           double (&mx)[4], uint32_t& seq, const double* s_wtab) {
+template <int KIND>
+__device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ring, int xbuf, int fbuf, int bbuf,
+                                           double c1, double c2, double* outT, double* outF, double (&mx)[4],
+                                           uint32_t& seq, uint32_t& phase_mask, const double* s_wtab) {
     // Register-blocked layout: thread t owns column xl = t % 64 and rows ry0 = 2*(t/64), ry0+1 of
     // the 64 x 16 tile for the whole z-march, so its z-1/z/z+1 values of X and T1 and its own
     // y-neighbour live in registers; x-neighbours and the outer y-neighbours come from shared
     // memory.  The 164 halo-ring points of T1 are computed by threads 0..163 from shared memory.
+    // All per-thread shared-memory offsets are fixed per tile; ring slots rotate by increment and
+    // barrier parities are tracked in a bit mask (identical in every thread).
+    constexpr bool needX = KIND != k2FirstZero;
+    constexpr bool needF = KIND == k2Next;
+    constexpr bool needB = KIND == k2FirstZero || KIND == k2FirstBorder;
+    constexpr uint32_t kXTx = k2XRows * kXPitch * 8;
+    constexpr uint32_t kBTx = k2BRows * kXPitch * 8;
+    constexpr uint32_t kLTx = (kTmaTY + 2) * kLPitch;
+    constexpr int kRing = 2 * (kTmaTX + 2) + 2 * kTmaTY;  // 164 halo-ring points of T1
     const StencilOp& op = p.op;
     const int tid = threadIdx.x;
     const int xl = tid & (kTmaTX - 1);
     const int ry0 = 2 * (tid / kTmaTX);
+    const int oX = (ry0 + 2) * kXPitch + xl + kXHalo;   // own row 0 in the X halo-2 tile
+    const int oT = (ry0 + 1) * kT1Pitch + xl + 1;       // own row 0 in a T1 plane
+    const int oL = (ry0 + 1) * kLPitch + xl + kLHaloX;  // own row 0 in the label tile
+    const int oB = (ry0 + 1) * kXPitch + xl + kXHalo;   // own row 0 in the b/gamma tile
+    const int oF = ry0 * kTmaTX + xl;                   // own row 0 in the F tile
+    // this thread's ring point (rows -1 and 16, then columns -1 and 64)
+    const bool ringer = tid < kRing;
+    int rr = 0, rc = 0;
+    if (ringer) {
+        if (tid < 2 * (kTmaTX + 2)) {
+            rr = tid < kTmaTX + 2 ? 0 : kTmaTY + 1;
+            rc = tid < kTmaTX + 2 ? tid : tid - (kTmaTX + 2);
+        } else {
+            const int e = tid - 2 * (kTmaTX + 2);
+            rr = 1 + (e >> 1);
+            rc = (e & 1) ? kTmaTX + 1 : 0;
+        }
+    }
+    const int rX = (rr + 1) * kXPitch + rc + 1, rT = rr * kT1Pitch + rc, rL = rr * kLPitch + rc + kLHaloX - 1,
+              rB = rr * kXPitch + rc + 1;
+
     const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
     const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
     const int64_t Q = static_cast<int64_t>(tiles_x) * tiles_y * op.nz;
     const int64_t q_begin = static_cast<int64_t>(blockIdx.x) * Q / gridDim.x;
     const int64_t q_end = static_cast<int64_t>(blockIdx.x + 1) * Q / gridDim.x;
-    const bool needX = kind != k2FirstZero;
-    const bool needF = kind == k2Next;
-    const bool needB = kind == k2FirstZero || kind == k2FirstBorder;
-    constexpr uint32_t kXTx = k2XRows * kXPitch * 8;
-    constexpr uint32_t kBTx = k2BRows * kXPitch * 8;
-    constexpr uint32_t kLTx = (kTmaTY + 2) * kLPitch;
-    constexpr int kRing = 2 * (kTmaTX + 2) + 2 * kTmaTY;  // 164 halo-ring points of T1
     if (tid == 0) fence_proxy_async_global();
 
     for (int64_t q = q_begin; q < q_end;) {
@@ -342,11 +366,8 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
         const int pfirst = z0 - 2, plast = z1 + 1;  // planes loaded
         const int np = plast - pfirst + 1;
 
-        auto seq_of = [&](int pl) { return base + static_cast<uint32_t>(pl - pfirst); };
-        auto slot_of = [&](int pl) { return static_cast<int>(seq_of(pl) % k2Stages); };
-        auto issue = [&](int pl) {
-            const uint32_t sq = seq_of(pl);
-            const int slot = static_cast<int>(sq % k2Stages);
+        auto issue = [&](int pl) {  // thread 0 only
+            const int slot = static_cast<int>((base + static_cast<uint32_t>(pl - pfirst)) % k2Stages);
             uint64_t* bar = ring.bar + slot;
             const bool ownF = needF && pl >= z0 && pl < z1;
             const bool haloB = needB && pl >= z0 - 1 && pl <= z1;
@@ -358,119 +379,105 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             if (haloB) tma_load_3d(ring.b(slot), &p.xmap[bbuf], x0 - kXHalo, y0 - 1, pl, bar);
             if (haloL) tma_load_3d(ring.l(slot), &p.l2map, x0 - kLHaloX, y0 - 1, pl, bar);
         };
-        auto wait_plane = [&](int pl) {
-            const uint32_t sq = seq_of(pl);
-            mbar_wait(ring.bar + sq % k2Stages, (sq / k2Stages) & 1u);
+        auto wait_slot = [&](int slot) {
+            mbar_wait(ring.bar + slot, (phase_mask >> slot) & 1u);
+            phase_mask ^= 1u << slot;
         };
+        auto next_slot = [](int s) { return s + 1 == k2Stages ? 0 : s + 1; };
 
         if (tid == 0) {
             const int pre = min(k2Stages, np);
             for (int k = 0; k < pre; ++k) issue(pfirst + k);
         }
 
-        const int gx = x0 + xl;
-        const int gy0 = y0 + ry0;
+        // per-segment geometry
+        const int gx = x0 + xl, gy0 = y0 + ry0;
         const bool inx = gx < op.nx;
-        const bool in_r[2] = {inx && gy0 < op.ny, inx && gy0 + 1 < op.ny};
-        const bool hx0 = gx > 0, hx1 = gx < op.nx - 1;
-        const int hyc[2] = {(gy0 > 0) + (gy0 < op.ny - 1), (gy0 + 1 > 0) + (gy0 + 1 < op.ny - 1)};
-        // own rows' X at planes (p-1, p, p+1) relative to the phase-A plane; own T1 at (z-1, z, z+1)
-        double xa[2] = {0.0, 0.0}, xb[2] = {0.0, 0.0}, xn[2] = {0.0, 0.0};
-        double ta[2] = {0.0, 0.0}, tb[2] = {0.0, 0.0};
-        double lwB[2] = {0.0, 0.0};  // w of plane z (own rows), loaded by phase A of plane z
-        auto load_own_x = [&](int pl, double (&dst)[2]) {
-            if (!needX) return;
-            const double* X = ring.x(slot_of(pl));
-            dst[0] = X[(ry0 + 2) * kXPitch + xl + kXHalo];
-            dst[1] = X[(ry0 + 3) * kXPitch + xl + kXHalo];
-        };
+        const bool in0 = inx && gy0 < op.ny, in1 = inx && gy0 + 1 < op.ny;
+        const int cxy = (gx > 0) + (gx < op.nx - 1);
+        const double ncxy0 = -static_cast<double>(cxy + (gy0 > 0) + (gy0 < op.ny - 1));
+        const double ncxy1 = -static_cast<double>(cxy + (gy0 + 1 > 0) + (gy0 + 1 < op.ny - 1));
+        const int rgx = x0 - 1 + rc, rgy = y0 - 1 + rr;
+        const bool rin = ringer && rgx >= 0 && rgx < op.nx && rgy >= 0 && rgy < op.ny;
+        const double rncxy = -static_cast<double>((rgx > 0) + (rgx < op.nx - 1) + (rgy > 0) + (rgy < op.ny - 1));
+        const int64_t v0 = gx + static_cast<int64_t>(gy0) * op.sy;
 
-        // Phase A: T1 of plane pl for the own rows (registers xm/xc/xp hold X of planes pl-1, pl,
-        // pl+1) and for the halo ring (from shared memory); writes T1's shared plane.
-        auto phaseA = [&](int pl, const double (&xm)[2], const double (&xc)[2], const double (&xp)[2],
-                          double (&t1)[2], double (&lw)[2]) {
-            double* T1 = ring.t1((pl + 2) % kT1Planes);
+        // Phase A: T1 of plane pl.  sm/sc/sp: ring slots of planes pl-1, pl, pl+1.
+        // xm/xc/xp: own rows' X at pl-1, pl, pl+1.  Writes T1's shared plane (pl & 1).
+        auto phaseA = [&](int pl, int sm_, int sc_, int sp_, const double (&xm)[2], const double (&xc)[2],
+                          const double (&xp)[2], double (&t1)[2], double (&lw)[2]) {
+            double* T1 = ring.t1((pl + 2) & 1);
             const bool zin = pl >= 0 && pl < op.nz;
-            const int sp = slot_of(pl);
-            const double* Xc = needX ? ring.x(sp) : nullptr;
-            const uint8_t* L = ring.l(sp);
-            const double* B = needB ? ring.b(sp) : nullptr;
-            const int hz = (pl > 0) + (pl < op.nz - 1);
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const int ry = ry0 + k;
-                double val = 0.0;
-                const double w = s_wtab[L[(ry + 1) * kLPitch + xl + kLHaloX]];
-                lw[k] = w;
-                if (zin && in_r[k]) {
-                    RowCoef rc;
-                    rc.w = w;
-                    rc.live = w != 0.0;
-                    double sc;
-                    if (kind == k2FirstZero) {
-                        sc = __dadd_rn(0.0, B[(ry + 1) * kXPitch + xl + kXHalo]);
-                    } else {
-                        const int xi = (ry + 2) * kXPitch + xl + kXHalo;
-                        const double ym = (k == 0) ? Xc[xi - kXPitch] : xc[0];
-                        const double yp = (k == 1) ? Xc[xi + kXPitch] : xc[1];
-                        const int cnt = hx0 + hx1 + hyc[k] + hz;
-                        sc = row_apply(rc, cnt, xm[k], ym, Xc[xi - 1], xc[k], Xc[xi + 1], yp, xp[k]);
-                        if (kind == k2FirstBorder) sc = __dadd_rn(sc, B[(ry + 1) * kXPitch + xl + kXHalo]);
-                    }
-                    val = __dmul_rn(c1, sc);
+            const double dhz = static_cast<double>((pl > 0) + (pl < op.nz - 1));
+            const double* Xc = ring.x(sc_);
+            const uint8_t* L = ring.l(sc_);
+            const double* B = ring.b(sc_);
+            const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
+            lw[0] = w0;
+            lw[1] = w1;
+            double s0, s1;
+            if (KIND == k2FirstZero) {
+                s0 = __dadd_rn(0.0, B[oB]);
+                s1 = __dadd_rn(0.0, B[oB + kXPitch]);
+            } else {
+                const double xr0m = Xc[oX - 1], xr0p = Xc[oX + 1], xr1m = Xc[oX + kXPitch - 1], xr1p = Xc[oX + kXPitch + 1];
+                const double xym0 = Xc[oX - kXPitch], xyp1 = Xc[oX + 2 * kXPitch];
+                s0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), xm[0], xym0, xr0m, xc[0], xr0p, xc[1], xp[0]);
+                s1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dhz), xm[1], xc[0], xr1m, xc[1], xr1p, xyp1, xp[1]);
+                if (KIND == k2FirstBorder) {
+                    s0 = __dadd_rn(s0, B[oB]);
+                    s1 = __dadd_rn(s1, B[oB + kXPitch]);
                 }
-                t1[k] = val;
-                T1[(ry + 1) * kT1Pitch + xl + 1] = val;
             }
-            if (tid < kRing) {
-                // ring point: rows -1 and 16 (66 each), then columns -1 and 64 for rows 0..15
-                int r, cc;
-                if (tid < 2 * (kTmaTX + 2)) {
-                    r = tid < kTmaTX + 2 ? 0 : kTmaTY + 1;
-                    cc = tid < kTmaTX + 2 ? tid : tid - (kTmaTX + 2);
+            const double v0_ = (zin && in0) ? __dmul_rn(c1, s0) : 0.0;
+            const double v1_ = (zin && in1) ? __dmul_rn(c1, s1) : 0.0;
+            t1[0] = v0_;
+            t1[1] = v1_;
+            T1[oT] = v0_;
+            T1[oT + kT1Pitch] = v1_;
+            if (ringer) {
+                const double w = s_wtab[L[rL]];
+                double sc;
+                if (KIND == k2FirstZero) {
+                    sc = __dadd_rn(0.0, B[rB]);
                 } else {
-                    const int e = tid - 2 * (kTmaTX + 2);
-                    r = 1 + (e >> 1);
-                    cc = (e & 1) ? kTmaTX + 1 : 0;
+                    const double* Xm = ring.x(sm_);
+                    const double* Xp = ring.x(sp_);
+                    sc = row_apply_nc(w, w != 0.0, __dsub_rn(rncxy, dhz), Xm[rX], Xc[rX - kXPitch], Xc[rX - 1], Xc[rX],
+                                      Xc[rX + 1], Xc[rX + kXPitch], Xp[rX]);
+                    if (KIND == k2FirstBorder) sc = __dadd_rn(sc, B[rB]);
                 }
-                const int rgx = x0 - 1 + cc, rgy = y0 - 1 + r;
-                double val = 0.0;
-                if (zin && rgx >= 0 && rgx < op.nx && rgy >= 0 && rgy < op.ny) {
-                    RowCoef rc;
-                    rc.w = s_wtab[L[r * kLPitch + cc + kLHaloX - 1]];
-                    rc.live = rc.w != 0.0;
-                    double sc;
-                    if (kind == k2FirstZero) {
-                        sc = __dadd_rn(0.0, B[r * kXPitch + cc + 1]);
-                    } else {
-                        const double* Xm = ring.x(slot_of(pl - 1));
-                        const double* Xp = ring.x(slot_of(pl + 1));
-                        const int xi = (r + 1) * kXPitch + cc + 1;
-                        const int cnt = (rgx > 0) + (rgx < op.nx - 1) + (rgy > 0) + (rgy < op.ny - 1) + hz;
-                        sc = row_apply(rc, cnt, Xm[xi], Xc[xi - kXPitch], Xc[xi - 1], Xc[xi], Xc[xi + 1],
-                                       Xc[xi + kXPitch], Xp[xi]);
-                        if (kind == k2FirstBorder) sc = __dadd_rn(sc, B[r * kXPitch + cc + 1]);
-                    }
-                    val = __dmul_rn(c1, sc);
-                }
-                T1[r * kT1Pitch + cc] = val;
+                T1[rT] = (zin && rin) ? __dmul_rn(c1, sc) : 0.0;
             }
         };
 
+        int s0 = static_cast<int>(base % k2Stages);  // slot of plane z0-2
+        int s1 = next_slot(s0), s2 = next_slot(s1), s3 = next_slot(s2);
         // prologue: T1 of planes z0-1 and z0
-        wait_plane(z0 - 2);
-        wait_plane(z0 - 1);
-        wait_plane(z0);
-        double xz[2] = {0.0, 0.0};
-        load_own_x(z0 - 2, xz);
-        load_own_x(z0 - 1, xa);
-        load_own_x(z0, xb);
-        double lwA[2];
-        phaseA(z0 - 1, xz, xa, xb, ta, lwA);
-        wait_plane(z0 + 1);
-        load_own_x(z0 + 1, xn);
-        phaseA(z0, xa, xb, xn, tb, lwB);
-        // now: xa <- X(z0), xb <- X(z0+1)
+        wait_slot(s0);
+        wait_slot(s1);
+        wait_slot(s2);
+        double xz[2] = {0.0, 0.0}, xa[2] = {0.0, 0.0}, xb[2] = {0.0, 0.0}, xn[2] = {0.0, 0.0};
+        if (needX) {
+            const double* X0 = ring.x(s0);
+            const double* X1 = ring.x(s1);
+            const double* X2 = ring.x(s2);
+            xz[0] = X0[oX];
+            xz[1] = X0[oX + kXPitch];
+            xa[0] = X1[oX];
+            xa[1] = X1[oX + kXPitch];
+            xb[0] = X2[oX];
+            xb[1] = X2[oX + kXPitch];
+        }
+        double ta[2], tb[2], lwA[2], lwB[2];
+        phaseA(z0 - 1, s0, s1, s2, xz, xa, xb, ta, lwA);
+        wait_slot(s3);
+        if (needX) {
+            const double* X3 = ring.x(s3);
+            xn[0] = X3[oX];
+            xn[1] = X3[oX + kXPitch];
+        }
+        phaseA(z0, s1, s2, s3, xa, xb, xn, tb, lwB);
         xa[0] = xb[0];
         xa[1] = xb[1];
         xb[0] = xn[0];
@@ -480,44 +487,60 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             if (pfirst + k2Stages <= plast) issue(pfirst + k2Stages);
             if (pfirst + 1 + k2Stages <= plast) issue(pfirst + 1 + k2Stages);
         }
-
+        // slots of planes z, z+1, z+2
+        int sA = s2, sB = s3, sC = next_slot(s3);
+        double* pT = outT + v0 + static_cast<int64_t>(z0) * op.sz;
+        double* pF = outF + v0 + static_cast<int64_t>(z0) * op.sz;
         for (int z = z0; z < z1; ++z) {
-            wait_plane(z + 2);
-            load_own_x(z + 2, xn);
-            double tc[2];
-            double lwN[2];
-            phaseA(z + 1, xa, xb, xn, tc, lwN);
-            // Phase B: own voxels of plane z; T1(z) in-plane neighbours from shared memory
-            const double* T1s = ring.t1((z + 2) % kT1Planes);
-            const double* Fo = ring.f(slot_of(z));
-            const int hz = (z > 0) + (z < op.nz - 1);
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                if (!in_r[k]) continue;
-                const int ry = ry0 + k;
-                const int ti = (ry + 1) * kT1Pitch + xl + 1;
-                RowCoef rc;
-                rc.w = lwB[k];
-                rc.live = rc.w != 0.0;
-                const double ym = (k == 0) ? T1s[ti - kT1Pitch] : tb[0];
-                const double yp = (k == 1) ? T1s[ti + kT1Pitch] : tb[1];
-                const int cnt = hx0 + hx1 + hyc[k] + hz;
-                const double acc = row_apply(rc, cnt, ta[k], ym, T1s[ti - 1], tb[k], T1s[ti + 1], yp, tc[k]);
-                const double t2 = __dmul_rn(c2, acc);
-                double fprev;
-                if (kind == k2FirstZero) fprev = 0.0;
-                else if (kind == k2Next) fprev = __dadd_rn(Fo[ry * kTmaTX + xl], xa[k]);
-                else fprev = xa[k];
-                const double f1 = __dadd_rn(fprev, tb[k]);
-                const double f2 = __dadd_rn(f1, t2);
-                const int64_t v = gx + static_cast<int64_t>(gy0 + k) * op.sy + static_cast<int64_t>(z) * op.sz;
-                outT[v] = t2;
-                outF[v] = f1;
-                mx[0] = nan_dropping_max(mx[0], fabs(tb[k]));
-                mx[1] = nan_dropping_max(mx[1], fabs(f1));
-                mx[2] = nan_dropping_max(mx[2], fabs(t2));
-                mx[3] = nan_dropping_max(mx[3], fabs(f2));
+            wait_slot(sC);
+            if (needX) {
+                const double* XC = ring.x(sC);
+                xn[0] = XC[oX];
+                xn[1] = XC[oX + kXPitch];
             }
+            double tc[2], lwN[2];
+            phaseA(z + 1, sA, sB, sC, xa, xb, xn, tc, lwN);
+            // Phase B: own voxels of plane z; T1(z) in-plane neighbours from shared memory
+            const double* T1s = ring.t1(z & 1);
+            const double dhz = static_cast<double>((z > 0) + (z < op.nz - 1));
+            const double y0m = T1s[oT - kT1Pitch], y1p = T1s[oT + 2 * kT1Pitch];
+            const double a0 = row_apply_nc(lwB[0], lwB[0] != 0.0, __dsub_rn(ncxy0, dhz), ta[0], y0m, T1s[oT - 1], tb[0],
+                                           T1s[oT + 1], tb[1], tc[0]);
+            const double a1 = row_apply_nc(lwB[1], lwB[1] != 0.0, __dsub_rn(ncxy1, dhz), ta[1], tb[0],
+                                           T1s[oT + kT1Pitch - 1], tb[1], T1s[oT + kT1Pitch + 1], y1p, tc[1]);
+            const double t20 = __dmul_rn(c2, a0), t21 = __dmul_rn(c2, a1);
+            double fp0, fp1;
+            if (KIND == k2FirstZero) {
+                fp0 = 0.0;
+                fp1 = 0.0;
+            } else if (KIND == k2Next) {
+                const double* Fo = ring.f(sA);
+                fp0 = __dadd_rn(Fo[oF], xa[0]);
+                fp1 = __dadd_rn(Fo[oF + kTmaTX], xa[1]);
+            } else {
+                fp0 = xa[0];
+                fp1 = xa[1];
+            }
+            const double f10 = __dadd_rn(fp0, tb[0]), f11 = __dadd_rn(fp1, tb[1]);
+            const double f20 = __dadd_rn(f10, t20), f21 = __dadd_rn(f11, t21);
+            if (in0) {
+                pT[0] = t20;
+                pF[0] = f10;
+                mx[0] = nan_dropping_max(mx[0], fabs(tb[0]));
+                mx[1] = nan_dropping_max(mx[1], fabs(f10));
+                mx[2] = nan_dropping_max(mx[2], fabs(t20));
+                mx[3] = nan_dropping_max(mx[3], fabs(f20));
+            }
+            if (in1) {
+                pT[op.sy] = t21;
+                pF[op.sy] = f11;
+                mx[0] = nan_dropping_max(mx[0], fabs(tb[1]));
+                mx[1] = nan_dropping_max(mx[1], fabs(f11));
+                mx[2] = nan_dropping_max(mx[2], fabs(t21));
+                mx[3] = nan_dropping_max(mx[3], fabs(f21));
+            }
+            pT += op.sz;
+            pF += op.sz;
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 xa[k] = xb[k];
@@ -526,6 +549,9 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 tb[k] = tc[k];
                 lwB[k] = lwN[k];
             }
+            sA = sB;
+            sB = sC;
+            sC = next_slot(sC);
             __syncthreads();  // plane z's slot and T1(z)'s shared plane are free
             if (tid == 0) {
                 const int nxt = z + k2Stages;
@@ -557,7 +583,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         for (int b = 0; b < kNumBufs; ++b) tma_prefetch_desc(&p.xmap[b]);
     }
     __syncthreads();
-    uint32_t seq = 0, seq2 = 0;
+    uint32_t seq = 0, seq2 = 0, pmask2 = 0;
     // Grid barrier; with TMA, first order this thread's generic global writes before any
     // later async-proxy (TMA) read of them.
     auto gsync = [&]() {
@@ -843,8 +869,19 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                     const double c2 = __ddiv_rn(tau_s, static_cast<double>(used + 2));
                     const int fout = kBufF0 + fsel, tout = kBufT0 + tsel;
                     double mx[4] = {0.0, 0.0, 0.0, 0.0};
-                    sweep2_tma(p, ring2, kind, xb < 0 ? 0 : xb, fb < 0 ? 0 : fb, kBufG, c1, c2, p.buf[tout],
-                               p.buf[fout], mx, seq2, sm.wtab);
+                    {
+                        const int xb_ = xb < 0 ? 0 : xb, fb_ = fb < 0 ? 0 : fb;
+                        double* oT = p.buf[tout];
+                        double* oF = p.buf[fout];
+                        if (kind == k2Next)
+                            sweep2_tma<k2Next>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                        else if (kind == k2FirstBorder)
+                            sweep2_tma<k2FirstBorder>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                        else if (kind == k2FirstZero)
+                            sweep2_tma<k2FirstZero>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                        else
+                            sweep2_tma<k2FirstPlain>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                    }
                     block_reduce<4, true>(mx, sm);
                     if (threadIdx.x == 0) {
                         unsigned long long* sl = p.slots + (round % 3) * 4;
