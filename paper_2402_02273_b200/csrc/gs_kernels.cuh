@@ -39,7 +39,7 @@ constexpr int kRingBytes = kTmaStages * kSlotBytes + 128;              // + barr
 // Two-term fused sweep (temporal blocking): T_{j+1} is computed on the tile plus a one-voxel
 // halo and kept in a 3-plane shared ring, T_{j+2} on the tile; the input therefore needs a
 // two-voxel halo in x, y and z.
-constexpr int k2Stages = 6;
+constexpr int k2Stages = 8;
 constexpr int k2XRows = kTmaTY + 4;                                     // y halo 2
 constexpr int k2XBytes = (k2XRows * kXPitch * 8 + 127) / 128 * 128;    // 20 x 68 doubles
 constexpr int k2BRows = kTmaTY + 2;                                     // y halo 1
@@ -47,11 +47,13 @@ constexpr int k2BBytes = (k2BRows * kXPitch * 8 + 127) / 128 * 128;    // 18 x 6
 constexpr int kLHaloX = 16;                                             // u8 box: 16-byte aligned start
 constexpr int kLPitch = kTmaTX + 2 * kLHaloX;                           // 96 labels per halo row
 constexpr int k2LBytes = ((kTmaTY + 2) * kLPitch + 127) / 128 * 128;   // 18 x 96 labels
-constexpr int k2SlotBytes = k2XBytes + kOBytes + k2BBytes + k2LBytes;
+// F (own, next-kind) and b/gamma (halo, first-kind) are never needed by the same sweep: one region.
+constexpr int k2FBBytes = kOBytes > k2BBytes ? kOBytes : k2BBytes;
+constexpr int k2SlotBytes = k2XBytes + k2FBBytes + k2LBytes;
 constexpr int kT1Pitch = kTmaTX + 2;
 constexpr int kT1Rows = kTmaTY + 2;
 constexpr int kT1Bytes = kT1Rows * kT1Pitch * 8;
-constexpr int kT1Planes = 2;  // T1(z) is read from shared memory only in the iteration after it is written
+constexpr int kT1Planes = 3;  // T1(z+1) is written while T1(z-1) is read; T1(z) is kept for the next iteration
 constexpr int k2RingBytes = k2Stages * k2SlotBytes + kT1Planes * kT1Bytes + 128;
 constexpr int kDynSmemBytes = kRingBytes > k2RingBytes ? kRingBytes : k2RingBytes;
 

@@ -297,10 +297,8 @@ struct Ring2 {
     uint64_t* bar;
     __device__ double* x(int s) const { return reinterpret_cast<double*>(base + s * k2SlotBytes); }
     __device__ double* f(int s) const { return reinterpret_cast<double*>(base + s * k2SlotBytes + k2XBytes); }
-    __device__ double* b(int s) const {
-        return reinterpret_cast<double*>(base + s * k2SlotBytes + k2XBytes + kOBytes);
-    }
-    __device__ uint8_t* l(int s) const { return base + s * k2SlotBytes + k2XBytes + kOBytes + k2BBytes; }
+    __device__ double* b(int s) const { return reinterpret_cast<double*>(base + s * k2SlotBytes + k2XBytes); }
+    __device__ uint8_t* l(int s) const { return base + s * k2SlotBytes + k2XBytes + k2FBBytes; }
     __device__ double* t1(int q) const {
         return reinterpret_cast<double*>(base + k2Stages * k2SlotBytes + q * kT1Bytes);
     }
@@ -406,7 +404,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
         // xm/xc/xp: own rows' X at pl-1, pl, pl+1.  Writes T1's shared plane (pl & 1).
         auto phaseA = [&](int pl, int sm_, int sc_, int sp_, const double (&xm)[2], const double (&xc)[2],
                           const double (&xp)[2], double (&t1)[2], double (&lw)[2]) {
-            double* T1 = ring.t1((pl + 2) & 1);
+            double* T1 = ring.t1((pl + 3) % kT1Planes);
             const bool zin = pl >= 0 && pl < op.nz;
             const double dhz = static_cast<double>((pl > 0) + (pl < op.nz - 1));
             const double* Xc = ring.x(sc_);
@@ -469,15 +467,16 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             xb[0] = X2[oX];
             xb[1] = X2[oX + kXPitch];
         }
-        double ta[2], tb[2], lwA[2], lwB[2];
-        phaseA(z0 - 1, s0, s1, s2, xz, xa, xb, ta, lwA);
+        // own T1 of planes z-2, z-1, z (relative to the loop's z); w unused here
+        double tm2[2] = {0.0, 0.0}, tm1[2], t0[2], lwd[2];
+        phaseA(z0 - 1, s0, s1, s2, xz, xa, xb, tm1, lwd);
         wait_slot(s3);
         if (needX) {
             const double* X3 = ring.x(s3);
             xn[0] = X3[oX];
             xn[1] = X3[oX + kXPitch];
         }
-        phaseA(z0, s1, s2, s3, xa, xb, xn, tb, lwB);
+        phaseA(z0, s1, s2, s3, xa, xb, xn, t0, lwd);
         xa[0] = xb[0];
         xa[1] = xb[1];
         xb[0] = xn[0];
@@ -487,74 +486,88 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             if (pfirst + k2Stages <= plast) issue(pfirst + k2Stages);
             if (pfirst + 1 + k2Stages <= plast) issue(pfirst + 1 + k2Stages);
         }
-        // slots of planes z, z+1, z+2
-        int sA = s2, sB = s3, sC = next_slot(s3);
+        // Iteration z: phase A makes T1(z+1) (z < z1), phase B finishes plane z-1 (z > z0) --
+        // independent work, so the two dependency chains overlap.
+        int sM = s1, sA = s2, sB = s3, sC = next_slot(s3);  // slots of planes z-1, z, z+1, z+2
         double* pT = outT + v0 + static_cast<int64_t>(z0) * op.sz;
         double* pF = outF + v0 + static_cast<int64_t>(z0) * op.sz;
-        for (int z = z0; z < z1; ++z) {
-            wait_slot(sC);
-            if (needX) {
-                const double* XC = ring.x(sC);
-                xn[0] = XC[oX];
-                xn[1] = XC[oX + kXPitch];
+        for (int z = z0; z <= z1; ++z) {
+            double tp1[2] = {0.0, 0.0};
+            if (z < z1) {
+                wait_slot(sC);
+                if (needX) {
+                    const double* XC = ring.x(sC);
+                    xn[0] = XC[oX];
+                    xn[1] = XC[oX + kXPitch];
+                }
+                double lwN[2];
+                phaseA(z + 1, sA, sB, sC, xa, xb, xn, tp1, lwN);
             }
-            double tc[2], lwN[2];
-            phaseA(z + 1, sA, sB, sC, xa, xb, xn, tc, lwN);
-            // Phase B: own voxels of plane z; T1(z) in-plane neighbours from shared memory
-            const double* T1s = ring.t1(z & 1);
-            const double dhz = static_cast<double>((z > 0) + (z < op.nz - 1));
-            const double y0m = T1s[oT - kT1Pitch], y1p = T1s[oT + 2 * kT1Pitch];
-            const double a0 = row_apply_nc(lwB[0], lwB[0] != 0.0, __dsub_rn(ncxy0, dhz), ta[0], y0m, T1s[oT - 1], tb[0],
-                                           T1s[oT + 1], tb[1], tc[0]);
-            const double a1 = row_apply_nc(lwB[1], lwB[1] != 0.0, __dsub_rn(ncxy1, dhz), ta[1], tb[0],
-                                           T1s[oT + kT1Pitch - 1], tb[1], T1s[oT + kT1Pitch + 1], y1p, tc[1]);
-            const double t20 = __dmul_rn(c2, a0), t21 = __dmul_rn(c2, a1);
-            double fp0, fp1;
-            if (KIND == k2FirstZero) {
-                fp0 = 0.0;
-                fp1 = 0.0;
-            } else if (KIND == k2Next) {
-                const double* Fo = ring.f(sA);
-                fp0 = __dadd_rn(Fo[oF], xa[0]);
-                fp1 = __dadd_rn(Fo[oF + kTmaTX], xa[1]);
-            } else {
-                fp0 = xa[0];
-                fp1 = xa[1];
+            if (z > z0) {
+                // Phase B: own voxels of plane zo = z-1
+                const int zo = z - 1;
+                const double* T1s = ring.t1((zo + 3) % kT1Planes);
+                const uint8_t* L = ring.l(sM);
+                const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
+                const double dhz = static_cast<double>((zo > 0) + (zo < op.nz - 1));
+                const double y0m = T1s[oT - kT1Pitch], y1p = T1s[oT + 2 * kT1Pitch];
+                const double a0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), tm2[0], y0m, T1s[oT - 1], tm1[0],
+                                               T1s[oT + 1], tm1[1], t0[0]);
+                const double a1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dhz), tm2[1], tm1[0],
+                                               T1s[oT + kT1Pitch - 1], tm1[1], T1s[oT + kT1Pitch + 1], y1p, t0[1]);
+                const double t20 = __dmul_rn(c2, a0), t21 = __dmul_rn(c2, a1);
+                double fp0, fp1;
+                if (KIND == k2FirstZero) {
+                    fp0 = 0.0;
+                    fp1 = 0.0;
+                } else {
+                    const double* XM = ring.x(sM);
+                    const double xo0 = XM[oX], xo1 = XM[oX + kXPitch];
+                    if (KIND == k2Next) {
+                        const double* Fo = ring.f(sM);
+                        fp0 = __dadd_rn(Fo[oF], xo0);
+                        fp1 = __dadd_rn(Fo[oF + kTmaTX], xo1);
+                    } else {
+                        fp0 = xo0;
+                        fp1 = xo1;
+                    }
+                }
+                const double f10 = __dadd_rn(fp0, tm1[0]), f11 = __dadd_rn(fp1, tm1[1]);
+                const double f20 = __dadd_rn(f10, t20), f21 = __dadd_rn(f11, t21);
+                if (in0) {
+                    pT[0] = t20;
+                    pF[0] = f10;
+                    mx[0] = nan_dropping_max(mx[0], fabs(tm1[0]));
+                    mx[1] = nan_dropping_max(mx[1], fabs(f10));
+                    mx[2] = nan_dropping_max(mx[2], fabs(t20));
+                    mx[3] = nan_dropping_max(mx[3], fabs(f20));
+                }
+                if (in1) {
+                    pT[op.sy] = t21;
+                    pF[op.sy] = f11;
+                    mx[0] = nan_dropping_max(mx[0], fabs(tm1[1]));
+                    mx[1] = nan_dropping_max(mx[1], fabs(f11));
+                    mx[2] = nan_dropping_max(mx[2], fabs(t21));
+                    mx[3] = nan_dropping_max(mx[3], fabs(f21));
+                }
+                pT += op.sz;
+                pF += op.sz;
             }
-            const double f10 = __dadd_rn(fp0, tb[0]), f11 = __dadd_rn(fp1, tb[1]);
-            const double f20 = __dadd_rn(f10, t20), f21 = __dadd_rn(f11, t21);
-            if (in0) {
-                pT[0] = t20;
-                pF[0] = f10;
-                mx[0] = nan_dropping_max(mx[0], fabs(tb[0]));
-                mx[1] = nan_dropping_max(mx[1], fabs(f10));
-                mx[2] = nan_dropping_max(mx[2], fabs(t20));
-                mx[3] = nan_dropping_max(mx[3], fabs(f20));
-            }
-            if (in1) {
-                pT[op.sy] = t21;
-                pF[op.sy] = f11;
-                mx[0] = nan_dropping_max(mx[0], fabs(tb[1]));
-                mx[1] = nan_dropping_max(mx[1], fabs(f11));
-                mx[2] = nan_dropping_max(mx[2], fabs(t21));
-                mx[3] = nan_dropping_max(mx[3], fabs(f21));
-            }
-            pT += op.sz;
-            pF += op.sz;
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 xa[k] = xb[k];
                 xb[k] = xn[k];
-                ta[k] = tb[k];
-                tb[k] = tc[k];
-                lwB[k] = lwN[k];
+                tm2[k] = tm1[k];
+                tm1[k] = t0[k];
+                t0[k] = tp1[k];
             }
+            sM = sA;
             sA = sB;
             sB = sC;
             sC = next_slot(sC);
-            __syncthreads();  // plane z's slot and T1(z)'s shared plane are free
-            if (tid == 0) {
-                const int nxt = z + k2Stages;
+            __syncthreads();  // plane z-1's slot and T1(z-1)'s shared plane are free
+            if (tid == 0 && z > z0) {
+                const int nxt = z - 1 + k2Stages;
                 if (nxt <= plast) issue(nxt);
             }
         }
