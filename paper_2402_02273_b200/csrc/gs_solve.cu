@@ -123,6 +123,27 @@ __device__ __forceinline__ void sweep_points(const StencilOp& op, Body&& body) {
     for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < op.n; v += stride) body(v);
 }
 
+// Pointwise sweep with memory-level parallelism: each warp takes 128 contiguous voxels per
+// round (lane + 32k, k = 0..3, each access fully coalesced), issues all loads first, then
+// applies.  Per-thread accumulation order is fixed (deterministic for a launch geometry).
+template <class Load, class Apply>
+__device__ __forceinline__ void sweep_points4(int64_t n, Load&& load, Apply&& apply) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    using In = decltype(load(int64_t(0)));
+    for (int64_t chunk = wg; chunk * 128 < n; chunk += nw) {
+        const int64_t b = chunk * 128 + lane;
+        In in[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (b + 32 * k < n) in[k] = load(b + 32 * k);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (b + 32 * k < n) apply(b + 32 * k, in[k]);
+    }
+}
+
 // Fallback stencil sweep (L1-cached loads, z-march in registers); used where TMA cannot
 // describe the arrays.  Tiles of 32 x (blockDim/32) columns times z-chunks of op.zc planes.
 template <class Body>
@@ -711,7 +732,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
 
     if (run && p.want_metrics) {
         double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
-        sweep_points(op, [&](int64_t v) { metrics_local(sum, mx, mn, r2, v, U[v]); });
+        sweep_points4(op.n, [&](int64_t v) { return U[v]; },
+                      [&](int64_t v, double u) { metrics_local(sum, mx, mn, r2, v, u); });
         metrics_push(sum, mx, mn, r2, 0);
         gsync();
         metrics_finish(0, 0);
@@ -742,14 +764,16 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             if (threadIdx.x == 0) p.part_b[blockIdx.x] = s[0];
         } else if (bordered) {
             double bsum = 0.0;
-            sweep_points(op, [&](int64_t v) { bsum = __dadd_rn(bsum, fabs(G[v])); });
+            sweep_points4(op.n, [&](int64_t v) { return G[v]; },
+                          [&](int64_t, double g) { bsum = __dadd_rn(bsum, fabs(g)); });
             double s[1] = {bsum};
             block_reduce<1, false>(s, sm);
             if (threadIdx.x == 0) p.part_b[blockIdx.x] = s[0];
         } else {
             // expmv: prev = ||b||_inf at stage 0 (expact.cpp:80)
             double mb = 0.0;
-            sweep_points(op, [&](int64_t v) { mb = nan_dropping_max(mb, fabs(G[v])); });
+            sweep_points4(op.n, [&](int64_t v) { return G[v]; },
+                          [&](int64_t, double g) { mb = nan_dropping_max(mb, fabs(g)); });
             push_max2(mb, 0.0);
         }
         gsync();
@@ -806,8 +830,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         if (bordered) {
             gamma = __ddiv_rn(bnorm, p.anorm);  // expact.cpp:126
             double csum = 0.0;
-            sweep_points(op, [&](int64_t v) {
-                const double b = G[v];
+            sweep_points4(op.n, [&](int64_t v) { return G[v]; }, [&](int64_t v, double b) {
                 const double bg = (b != 0.0) ? __ddiv_rn(b, gamma) : 0.0;  // expact.cpp:137-138
                 G[v] = bg;
                 csum = __dadd_rn(csum, fabs(bg));
@@ -871,7 +894,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                     const double* Tb = p.buf[tres];
                     const int fo = (fres == kBufF0) ? kBufF1 : kBufF0;
                     double* Fw = p.buf[fo];
-                    sweep_points(op, [&](int64_t v) { Fw[v] = __dadd_rn(Fa[v], Tb[v]); });
+                    sweep_points4(op.n, [&](int64_t v) { return make_double2(Fa[v], Tb[v]); },
+                                  [&](int64_t v, double2 ft) { Fw[v] = __dadd_rn(ft.x, ft.y); });
                     gsync();
                     fstart = fo;
                 } else {
@@ -1017,9 +1041,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         if (run) {
             const double scl = __ddiv_rn(gamma, t);  // expact.cpp:150
             double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
-            sweep_points(op, [&](int64_t v) {
+            sweep_points4(op.n, [&](int64_t v) { return make_double2(U[v], yv(v)); }, [&](int64_t v, double2 uy) {
                 // out = u + tau * (scale * y)   (integrator.cpp:59-61, expact.cpp:151)
-                const double un = __dadd_rn(U[v], __dmul_rn(t, __dmul_rn(scl, yv(v))));
+                const double un = __dadd_rn(uy.x, __dmul_rn(t, __dmul_rn(scl, uy.y)));
                 U[v] = un;
                 if (p.want_metrics) metrics_local(sum, mx, mn, r2, v, un);
             });
@@ -1028,7 +1052,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             if (p.want_metrics) metrics_finish(step + 1, (step + 1) & 1);
         } else {
             const double scale = bordered ? __ddiv_rn(gamma, t) : 1.0;
-            sweep_points(op, [&](int64_t v) { OUT[v] = bordered ? __dmul_rn(scale, yv(v)) : yv(v); });
+            sweep_points4(op.n, [&](int64_t v) { return yv(v); },
+                          [&](int64_t v, double y) { OUT[v] = bordered ? __dmul_rn(scale, y) : y; });
         }
     }
 }
