@@ -122,6 +122,15 @@ gs_status gs_run(gs_ctx* ctx, int n_steps, double rho, double tau, double tol, c
 gs_status gs_seed_initial(gs_ctx* ctx, const double origin[3], double amplitude, double width,
                           const double center[3], int mask, double* u);
 
+/* ---- diagnostics ---------------------------------------------------------------------- */
+/* Record a per-phase timeline (grid-barrier timestamps, ns) in subsequent launches;
+ * capacity = max records per launch, 0 disables.  Tags: 1 metrics(0), 2 RHS, 3 bordered
+ * column, 4 fused first-term sweep, 5 fused next-terms sweep, 6 implicit-f fix-up,
+ * 7 update+metrics, 8 single-term sweep, 9 degenerate branch, 15 launch start. */
+gs_status gs_set_trace(gs_ctx* ctx, int capacity);
+/* Copy the last launch's records as (tag, ns) pairs; *count receives the number of records. */
+gs_status gs_get_trace(gs_ctx* ctx, uint64_t* pairs, int capacity, int* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -77,6 +77,9 @@ struct gs_ctx {
     CUtensorMap omap[gs::kNumBufs];
     CUtensorMap x2map[gs::kNumBufs];
     CUtensorMap lmap, l2map;
+    int trace_cap = 0;
+    DevBuf trace;
+    std::vector<uint64_t> trace_host;
     std::string err;
 };
 
@@ -289,6 +292,14 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     p.status = c->status.as<int>();
     DevBuf* bufs[gs::kNumBufs] = {&c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out};
     for (int b = 0; b < gs::kNumBufs; ++b) p.buf[b] = bufs[b]->as<double>();
+    p.trace = nullptr;
+    p.trace_cap = 0;
+    if (c->trace_cap > 0) {
+        GS_CUDA(c, c->trace.alloc(sizeof(uint64_t) * 2 * c->trace_cap));
+        GS_CUDA(c, cudaMemsetAsync(c->trace.p, 0, sizeof(uint64_t) * 2 * c->trace_cap, c->stream));
+        p.trace = c->trace.as<unsigned long long>();
+        p.trace_cap = c->trace_cap;
+    }
     void* args[] = {&p};
     GS_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gs::solve_kernel), dim3(gb),
                                            dim3(gs::kSolveThreads), args, p.use_tma ? gs::kDynSmemBytes : 0,
@@ -301,6 +312,11 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     if (infos)
         GS_CUDA(c, cudaMemcpyAsync(infos, c->infos.p, sizeof(gs_step_info) * std::max(1, n_steps),
                                    cudaMemcpyDeviceToHost, c->stream));
+    if (c->trace_cap > 0) {
+        c->trace_host.assign(2 * static_cast<size_t>(c->trace_cap), 0);
+        GS_CUDA(c, cudaMemcpyAsync(c->trace_host.data(), c->trace.p, sizeof(uint64_t) * 2 * c->trace_cap,
+                                   cudaMemcpyDeviceToHost, c->stream));
+    }
     GS_CUDA(c, cudaStreamSynchronize(c->stream));
     if (status[0] != GS_OK) {
         if (status[1] == 2) return fail(c, GS_ENUMERIC, "expmv: series diverged to non-finite values; reduce t");
@@ -391,7 +407,7 @@ void gs_destroy(gs_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->pal, &c->dvox, &c->wtab, &c->dtab, &c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out,
                       &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->status, &c->metrics, &c->infos,
-                      &c->normbits})
+                      &c->normbits, &c->trace})
         b->release();
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -689,6 +705,25 @@ gs_status gs_seed_initial(gs_ctx* c, const double origin[3], double amplitude, d
                 u[v] = amplitude * std::exp(-width * sq);
                 if (mask && d[static_cast<size_t>(v)] == 0.0) u[v] = 0.0;
             }
+    return GS_OK;
+}
+
+gs_status gs_set_trace(gs_ctx* c, int capacity) {
+    if (!c || capacity < 0) return fail(c, GS_EINVAL, "gs_set_trace: bad argument");
+    c->trace_cap = capacity;
+    return GS_OK;
+}
+
+gs_status gs_get_trace(gs_ctx* c, uint64_t* pairs, int capacity, int* count) {
+    if (!c || !pairs || !count) return fail(c, GS_EINVAL, "gs_get_trace: null argument");
+    int n = 0;
+    const int have = static_cast<int>(c->trace_host.size() / 2);
+    while (n < have && n < capacity && c->trace_host[2 * n] != 0) {
+        pairs[2 * n] = c->trace_host[2 * n];
+        pairs[2 * n + 1] = c->trace_host[2 * n + 1];
+        ++n;
+    }
+    *count = n;
     return GS_OK;
 }
 

@@ -85,7 +85,13 @@ struct SolveParams {
     unsigned long long* slots;   // [3][4] rotating max slots for per-term reductions
     unsigned long long* mslots;  // [2][4] metric max/min/r2 slots (step parity)
     int* status;            // [0] gs_status, [1] detail
+    unsigned long long* trace;  // optional phase trace: (tag, globaltimer ns) pairs
+    int trace_cap;
 };
+
+// phase tags of the optional trace (leader's view, recorded after each grid barrier)
+enum TraceTag : int { kTrMetrics0 = 1, kTrRhs = 2, kTrBorder = 3, kTrFusedFirst = 4, kTrFusedNext = 5, kTrFixup = 6,
+                      kTrUpdate = 7, kTrTerm = 8, kTrBranch = 9, kTrStart = 15 };
 
 // K1: resample + classify (imaging.cpp:65-72, 118-141)
 __global__ void material_kernel(const uint8_t* stack, int w, int hgt, int slices, int nx, int ny, int nz,

@@ -626,11 +626,23 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
     uint32_t seq = 0, seq2 = 0, pmask2 = 0;
     // Grid barrier; with TMA, first order this thread's generic global writes before any
     // later async-proxy (TMA) read of them.
-    auto gsync = [&]() {
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    int ntrace = 0;
+    auto trace = [&](int tag) {
+        if (p.trace && leader && ntrace < p.trace_cap) {
+            unsigned long long tnow;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            p.trace[2 * ntrace] = static_cast<unsigned long long>(tag);
+            p.trace[2 * ntrace + 1] = tnow;
+            ++ntrace;
+        }
+    };
+    trace(kTrStart);
+    auto gsync = [&](int tag) {
         if (p.use_tma) fence_proxy_async_global();
         grid.sync();
+        trace(tag);
     };
-    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     int round = 0;  // per-term max-reduction rounds (slot rotation, identical in every CTA)
 
     // Stencil sweep dispatch: X = stencil input, F / B = own-voxel side inputs.
@@ -646,8 +658,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         }
     };
 
-    auto sync_round = [&]() {
-        gsync();
+    auto sync_round = [&](int tag) {
+        gsync(tag);
         if (leader) {
             unsigned long long* z = p.slots + ((round + 2) % 3) * 4;
             z[0] = z[1] = z[2] = z[3] = 0ull;
@@ -735,7 +747,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         sweep_points4(op.n, [&](int64_t v) { return U[v]; },
                       [&](int64_t v, double u) { metrics_local(sum, mx, mn, r2, v, u); });
         metrics_push(sum, mx, mn, r2, 0);
-        gsync();
+        gsync(kTrMetrics0);
         metrics_finish(0, 0);
     }
 
@@ -776,7 +788,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                           [&](int64_t, double g) { mb = nan_dropping_max(mb, fabs(g)); });
             push_max2(mb, 0.0);
         }
-        gsync();
+        gsync(kTrRhs);
 
         int branch = 0;
         double prev0 = 1.0;  // ||e_{n+1}||_inf for the bordered action
@@ -806,7 +818,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                     if (run) INC[v] = incr;
                     else OUT[v] = incr;
                 });
-                if (run) gsync();
+                if (run) gsync(kTrBranch);
             }
             if (run) {
                 double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
@@ -817,7 +829,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                     if (p.want_metrics) metrics_local(sum, mx, mn, r2, v, un);
                 });
                 if (p.want_metrics) metrics_push(sum, mx, mn, r2, (step + 1) & 1);
-                gsync();
+                gsync(kTrBranch);
                 if (p.want_metrics) metrics_finish(step + 1, (step + 1) & 1);
             } else if (branch != 3) {
                 sweep_points(op, [&](int64_t v) { OUT[v] = branch == 1 ? G[v] : 0.0; });
@@ -838,7 +850,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             double s[1] = {csum};
             block_reduce<1, false>(s, sm);
             if (threadIdx.x == 0) p.part_c[blockIdx.x] = s[0];
-            gsync();
+            gsync(kTrBorder);
             const double coln = grid_sum(p.part_c, p.grid_blocks, sm);
             // bordered ||.||_1 = max over columns: A's columns, then column n (sparse.cpp:39-40)
             norm_tA = __dmul_rn(fabs(t), nan_dropping_max(p.anorm, coln));
@@ -896,7 +908,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                     double* Fw = p.buf[fo];
                     sweep_points4(op.n, [&](int64_t v) { return make_double2(Fa[v], Tb[v]); },
                                   [&](int64_t v, double2 ft) { Fw[v] = __dadd_rn(ft.x, ft.y); });
-                    gsync();
+                    gsync(kTrFixup);
                     fstart = fo;
                 } else {
                     fstart = fres;
@@ -932,7 +944,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                         for (int q = 0; q < 4; ++q)
                             if (mx[q] > 0.0) atomicMax(sl + q, static_cast<unsigned long long>(__double_as_longlong(mx[q])));
                     }
-                    sync_round();
+                    sync_round(kind == k2Next ? kTrFusedNext : kTrFusedFirst);
                     const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
                     double cur[2] = {slot_read(sl + 0), slot_read(sl + 2)};
                     double fn[2] = {slot_read(sl + 1), slot_read(sl + 3)};
@@ -1010,7 +1022,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                         stencil(tprev, fcur, -1, [&](int64_t v, double acc, double, double f, double) { emit(v, acc, f); });
                     }
                     push_max2(mt, mf);
-                    sync_round();
+                    sync_round(kTrTerm);
                     ++used;
                     fcur = fout;
                     tprev = tout;
@@ -1048,7 +1060,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                 if (p.want_metrics) metrics_local(sum, mx, mn, r2, v, un);
             });
             if (p.want_metrics) metrics_push(sum, mx, mn, r2, (step + 1) & 1);
-            gsync();
+            gsync(kTrUpdate);
             if (p.want_metrics) metrics_finish(step + 1, (step + 1) & 1);
         } else {
             const double scale = bordered ? __ddiv_rn(gamma, t) : 1.0;

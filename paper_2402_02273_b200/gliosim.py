@@ -287,6 +287,19 @@ class StencilOperator:
     def stream_handle(self) -> int:
         return self.lib.gs_stream(self.ctx)
 
+    def set_trace(self, capacity: int):
+        """Record per-phase grid-barrier timestamps in later launches (diagnostics)."""
+        self._check(self.lib.gs_set_trace(self.ctx, capacity))
+        self._trace_cap = capacity
+
+    def trace(self):
+        """[(tag, ns)] of the last launch; see gliosim_b200.h for the tags."""
+        cap = getattr(self, "_trace_cap", 0)
+        buf = np.zeros(2 * max(cap, 1), dtype=np.uint64)
+        n = C.c_int()
+        self._check(self.lib.gs_get_trace(self.ctx, buf, cap, C.byref(n)))
+        return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(n.value)]
+
     def step_resident(self, rho, tau, tol, info=True):
         inf = N.GsStepInfo() if info else None
         self._check(self.lib.gs_step(self.ctx, rho, tau, tol, C.byref(inf) if inf is not None else None))
