@@ -123,23 +123,24 @@ __device__ __forceinline__ void sweep_points(const StencilOp& op, Body&& body) {
     for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < op.n; v += stride) body(v);
 }
 
-// Pointwise sweep with memory-level parallelism: each warp takes 128 contiguous voxels per
-// round (lane + 32k, k = 0..3, each access fully coalesced), issues all loads first, then
+// Pointwise sweep with memory-level parallelism: each warp takes 64 contiguous voxels per
+// round (lane + 32k, k = 0..1, each access fully coalesced), issues all loads first, then
 // applies.  Per-thread accumulation order is fixed (deterministic for a launch geometry).
 template <class Load, class Apply>
 __device__ __forceinline__ void sweep_points4(int64_t n, Load&& load, Apply&& apply) {
+    constexpr int kU = 2;  // loads in flight per thread (kept small: one register budget for the whole kernel)
     const int lane = threadIdx.x & 31;
     const int64_t wg = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     using In = decltype(load(int64_t(0)));
-    for (int64_t chunk = wg; chunk * 128 < n; chunk += nw) {
-        const int64_t b = chunk * 128 + lane;
-        In in[4];
+    for (int64_t chunk = wg; chunk * (32 * kU) < n; chunk += nw) {
+        const int64_t b = chunk * (32 * kU) + lane;
+        In in[kU];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < kU; ++k)
             if (b + 32 * k < n) in[k] = load(b + 32 * k);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < kU; ++k)
             if (b + 32 * k < n) apply(b + 32 * k, in[k]);
     }
 }
