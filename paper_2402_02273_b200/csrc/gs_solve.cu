@@ -39,7 +39,6 @@ struct Smem {
     double bcast[4];
     uint64_t bar1[kTmaStages];  // single-term ring
     uint64_t bar2[k2Stages];    // fused two-term ring
-    uint32_t st[2];             // fused-sweep ring state (sequence, parity mask) handed back by thread 0
 };
 
 struct Ring {
@@ -329,18 +328,10 @@ struct Ring2 {
     }
 };
 
-struct Max4 {
-    double v[4];
-};
-
-// __noinline__: the hot sweep gets its own register allocation, untouched by the rest of the
-// persistent kernel; every loop-carried value stays in registers (the results come back by value).
 template <int KIND>
-__device__ __noinline__ Max4 sweep2_tma(const SolveParams& p, const Ring2 ring, int xbuf, int fbuf, int bbuf,
-                                        double c1, double c2, double* outT, double* outF, uint32_t seq_in,
-                                        uint32_t pmask_in, const double* s_wtab, uint32_t* state_out) {
-    double mx[4] = {0.0, 0.0, 0.0, 0.0};
-    uint32_t seq = seq_in, phase_mask = pmask_in;
+__device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ring, int xbuf, int fbuf, int bbuf,
+                                           double c1, double c2, double* outT, double* outF, double (&mx)[4],
+                                           uint32_t& seq, uint32_t& phase_mask, const double* s_wtab) {
     // Register-blocked layout: thread t owns column xl = t % 64 and rows ry0 = 2*(t/64), ry0+1 of
     // the 64 x 16 tile for the whole z-march, so its z-1/z/z+1 values of X and T1 and its own
     // y-neighbour live in registers; x-neighbours and the outer y-neighbours come from shared
@@ -611,14 +602,6 @@ __device__ __noinline__ Max4 sweep2_tma(const SolveParams& p, const Ring2 ring, 
         seq = base + static_cast<uint32_t>(np);
     }
     fence_proxy_async_global();
-    if (threadIdx.x == 0) {
-        state_out[0] = seq;
-        state_out[1] = phase_mask;
-    }
-    Max4 r;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) r.v[q] = mx[q];
-    return r;
 }
 
 enum TermKind { kFirstZero, kFirstBorder, kFirstPlain, kNext };
@@ -946,23 +929,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                         const int xb_ = xb < 0 ? 0 : xb, fb_ = fb < 0 ? 0 : fb;
                         double* oT = p.buf[tout];
                         double* oF = p.buf[fout];
-                        Max4 r4;
                         if (kind == k2Next)
-                            r4 = sweep2_tma<k2Next>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, seq2, pmask2, sm.wtab, sm.st);
+                            sweep2_tma<k2Next>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
                         else if (kind == k2FirstBorder)
-                            r4 = sweep2_tma<k2FirstBorder>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, seq2, pmask2, sm.wtab,
-                                                           sm.st);
+                            sweep2_tma<k2FirstBorder>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
                         else if (kind == k2FirstZero)
-                            r4 = sweep2_tma<k2FirstZero>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, seq2, pmask2, sm.wtab,
-                                                         sm.st);
+                            sweep2_tma<k2FirstZero>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
                         else
-                            r4 = sweep2_tma<k2FirstPlain>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, seq2, pmask2, sm.wtab,
-                                                          sm.st);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) mx[q] = r4.v[q];
-                        __syncthreads();
-                        seq2 = sm.st[0];
-                        pmask2 = sm.st[1];
+                            sweep2_tma<k2FirstPlain>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
                     }
                     block_reduce<4, true>(mx, sm);
                     if (threadIdx.x == 0) {
