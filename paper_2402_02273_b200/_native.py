@@ -93,11 +93,13 @@ def load(path: str | None = None):
     L.gs_step_host.argtypes = [vp, _dp, C.c_double, C.c_double, C.c_double, _dp, C.POINTER(GsStepInfo)]
     L.gs_run.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_double, _d3, _d3, C.c_double, vp, vp]
     L.gs_seed_initial.argtypes = [vp, _d3, C.c_double, C.c_double, _d3, C.c_int, _dp]
-    L.gs_set_trace.argtypes = [vp, C.c_int]
-    L.gs_get_trace.argtypes = [vp, np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS"), C.c_int,
-                               C.POINTER(C.c_int)]
+    if hasattr(L, "gs_set_trace"):  # diagnostics
+        L.gs_set_trace.argtypes = [vp, C.c_int]
+        L.gs_get_trace.argtypes = [vp, np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS"), C.c_int,
+                                   C.POINTER(C.c_int)]
     for name in EXPORTS:
-        if name not in ("gs_destroy", "gs_last_error", "gs_num_points", "gs_stream", "gs_state_device_ptr"):
+        if name not in ("gs_destroy", "gs_last_error", "gs_num_points", "gs_stream", "gs_state_device_ptr") \
+                and hasattr(L, name):
             getattr(L, name).restype = C.c_int
     if path == LIB_PATH:
         _lib = L

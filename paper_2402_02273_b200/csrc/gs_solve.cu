@@ -123,28 +123,6 @@ __device__ __forceinline__ void sweep_points(const StencilOp& op, Body&& body) {
     for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < op.n; v += stride) body(v);
 }
 
-// Pointwise sweep with memory-level parallelism: each warp takes 64 contiguous voxels per
-// round (lane + 32k, k = 0..1, each access fully coalesced), issues all loads first, then
-// applies.  Per-thread accumulation order is fixed (deterministic for a launch geometry).
-template <class Load, class Apply>
-__device__ __forceinline__ void sweep_points4(int64_t n, Load&& load, Apply&& apply) {
-    constexpr int kU = 2;  // loads in flight per thread (kept small: one register budget for the whole kernel)
-    const int lane = threadIdx.x & 31;
-    const int64_t wg = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    using In = decltype(load(int64_t(0)));
-    for (int64_t chunk = wg; chunk * (32 * kU) < n; chunk += nw) {
-        const int64_t b = chunk * (32 * kU) + lane;
-        In in[kU];
-#pragma unroll
-        for (int k = 0; k < kU; ++k)
-            if (b + 32 * k < n) in[k] = load(b + 32 * k);
-#pragma unroll
-        for (int k = 0; k < kU; ++k)
-            if (b + 32 * k < n) apply(b + 32 * k, in[k]);
-    }
-}
-
 // Fallback stencil sweep (L1-cached loads, z-march in registers); used where TMA cannot
 // describe the arrays.  Tiles of 32 x (blockDim/32) columns times z-chunks of op.zc planes.
 template <class Body>
@@ -511,30 +489,34 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             if (pfirst + 1 + k2Stages <= plast) issue(pfirst + 1 + k2Stages);
         }
         // Iteration z: phase A makes T1(z+1) (z < z1), phase B finishes plane z-1 (z > z0) --
-        // independent work, so the two dependency chains overlap.  Register rings of three:
-        // iteration z with r = (z - z0) % 3 finds X(z) in X3[r], X(z+1) in X3[r+1] and loads
-        // X(z+2) into X3[r+2]; T1(z-1) in T3[r], T1(z) in T3[r+1], T1(z-2) in T3[r+2], which
-        // phase A then overwrites with T1(z+1).  Unrolling by three makes every index static.
-        double X3[3][2] = {{xa[0], xa[1]}, {xb[0], xb[1]}, {0.0, 0.0}};
-        double T3[3][2] = {{tm1[0], tm1[1]}, {t0[0], t0[1]}, {0.0, 0.0}};
+        // independent work, so the two dependency chains overlap.
         int sM = s1, sA = s2, sB = s3, sC = next_slot(s3);  // slots of planes z-1, z, z+1, z+2
         double* pT = outT + v0 + static_cast<int64_t>(z0) * op.sz;
         double* pF = outF + v0 + static_cast<int64_t>(z0) * op.sz;
-        auto iter = [&](int z, auto rconst) {
-            constexpr int r = decltype(rconst)::value;
-            constexpr int r1 = (r + 1) % 3, r2 = (r + 2) % 3;
+        for (int z = z0; z <= z1; ++z) {
+            double tp1[2] = {0.0, 0.0};
+            if (z < z1) {
+                wait_slot(sC);
+                if (needX) {
+                    const double* XC = ring.x(sC);
+                    xn[0] = XC[oX];
+                    xn[1] = XC[oX + kXPitch];
+                }
+                double lwN[2];
+                phaseA(z + 1, sA, sB, sC, xa, xb, xn, tp1, lwN);
+            }
             if (z > z0) {
-                // Phase B: own voxels of plane zo = z-1 (T1 of zo-1, zo, zo+1 in T3[r2], T3[r], T3[r1])
+                // Phase B: own voxels of plane zo = z-1
                 const int zo = z - 1;
                 const double* T1s = ring.t1((zo + 3) % kT1Planes);
                 const uint8_t* L = ring.l(sM);
                 const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
                 const double dhz = static_cast<double>((zo > 0) + (zo < op.nz - 1));
                 const double y0m = T1s[oT - kT1Pitch], y1p = T1s[oT + 2 * kT1Pitch];
-                const double a0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), T3[r2][0], y0m, T1s[oT - 1],
-                                               T3[r][0], T1s[oT + 1], T3[r][1], T3[r1][0]);
-                const double a1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dhz), T3[r2][1], T3[r][0],
-                                               T1s[oT + kT1Pitch - 1], T3[r][1], T1s[oT + kT1Pitch + 1], y1p, T3[r1][1]);
+                const double a0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), tm2[0], y0m, T1s[oT - 1], tm1[0],
+                                               T1s[oT + 1], tm1[1], t0[0]);
+                const double a1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dhz), tm2[1], tm1[0],
+                                               T1s[oT + kT1Pitch - 1], tm1[1], T1s[oT + kT1Pitch + 1], y1p, t0[1]);
                 const double t20 = __dmul_rn(c2, a0), t21 = __dmul_rn(c2, a1);
                 double fp0, fp1;
                 if (KIND == k2FirstZero) {
@@ -552,37 +534,34 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                         fp1 = xo1;
                     }
                 }
-                const double f10 = __dadd_rn(fp0, T3[r][0]), f11 = __dadd_rn(fp1, T3[r][1]);
+                const double f10 = __dadd_rn(fp0, tm1[0]), f11 = __dadd_rn(fp1, tm1[1]);
                 const double f20 = __dadd_rn(f10, t20), f21 = __dadd_rn(f11, t21);
-                // fmax drops NaN like std::max(m, |x|) (m is never NaN): expact.cpp:15-19
                 if (in0) {
                     pT[0] = t20;
                     pF[0] = f10;
-                    mx[0] = fmax(mx[0], fabs(T3[r][0]));
-                    mx[1] = fmax(mx[1], fabs(f10));
-                    mx[2] = fmax(mx[2], fabs(t20));
-                    mx[3] = fmax(mx[3], fabs(f20));
+                    mx[0] = nan_dropping_max(mx[0], fabs(tm1[0]));
+                    mx[1] = nan_dropping_max(mx[1], fabs(f10));
+                    mx[2] = nan_dropping_max(mx[2], fabs(t20));
+                    mx[3] = nan_dropping_max(mx[3], fabs(f20));
                 }
                 if (in1) {
                     pT[op.sy] = t21;
                     pF[op.sy] = f11;
-                    mx[0] = fmax(mx[0], fabs(T3[r][1]));
-                    mx[1] = fmax(mx[1], fabs(f11));
-                    mx[2] = fmax(mx[2], fabs(t21));
-                    mx[3] = fmax(mx[3], fabs(f21));
+                    mx[0] = nan_dropping_max(mx[0], fabs(tm1[1]));
+                    mx[1] = nan_dropping_max(mx[1], fabs(f11));
+                    mx[2] = nan_dropping_max(mx[2], fabs(t21));
+                    mx[3] = nan_dropping_max(mx[3], fabs(f21));
                 }
                 pT += op.sz;
                 pF += op.sz;
             }
-            if (z < z1) {
-                wait_slot(sC);
-                if (needX) {
-                    const double* XC = ring.x(sC);
-                    X3[r2][0] = XC[oX];
-                    X3[r2][1] = XC[oX + kXPitch];
-                }
-                double lwN[2];
-                phaseA(z + 1, sA, sB, sC, X3[r], X3[r1], X3[r2], T3[r2], lwN);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                xa[k] = xb[k];
+                xb[k] = xn[k];
+                tm2[k] = tm1[k];
+                tm1[k] = t0[k];
+                t0[k] = tp1[k];
             }
             sM = sA;
             sA = sB;
@@ -593,11 +572,6 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 const int nxt = z - 1 + k2Stages;
                 if (nxt <= plast) issue(nxt);
             }
-        };
-        for (int zb = z0; zb <= z1; zb += 3) {
-            iter(zb, std::integral_constant<int, 0>{});
-            if (zb + 1 <= z1) iter(zb + 1, std::integral_constant<int, 1>{});
-            if (zb + 2 <= z1) iter(zb + 2, std::integral_constant<int, 2>{});
         }
         seq = base + static_cast<uint32_t>(np);
     }
@@ -745,8 +719,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
 
     if (run && p.want_metrics) {
         double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
-        sweep_points4(op.n, [&](int64_t v) { return U[v]; },
-                      [&](int64_t v, double u) { metrics_local(sum, mx, mn, r2, v, u); });
+        sweep_points(op, [&](int64_t v) { metrics_local(sum, mx, mn, r2, v, U[v]); });
         metrics_push(sum, mx, mn, r2, 0);
         gsync(kTrMetrics0);
         metrics_finish(0, 0);
@@ -777,16 +750,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             if (threadIdx.x == 0) p.part_b[blockIdx.x] = s[0];
         } else if (bordered) {
             double bsum = 0.0;
-            sweep_points4(op.n, [&](int64_t v) { return G[v]; },
-                          [&](int64_t, double g) { bsum = __dadd_rn(bsum, fabs(g)); });
+            sweep_points(op, [&](int64_t v) { bsum = __dadd_rn(bsum, fabs(G[v])); });
             double s[1] = {bsum};
             block_reduce<1, false>(s, sm);
             if (threadIdx.x == 0) p.part_b[blockIdx.x] = s[0];
         } else {
             // expmv: prev = ||b||_inf at stage 0 (expact.cpp:80)
             double mb = 0.0;
-            sweep_points4(op.n, [&](int64_t v) { return G[v]; },
-                          [&](int64_t, double g) { mb = nan_dropping_max(mb, fabs(g)); });
+            sweep_points(op, [&](int64_t v) { mb = nan_dropping_max(mb, fabs(G[v])); });
             push_max2(mb, 0.0);
         }
         gsync(kTrRhs);
@@ -843,7 +814,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         if (bordered) {
             gamma = __ddiv_rn(bnorm, p.anorm);  // expact.cpp:126
             double csum = 0.0;
-            sweep_points4(op.n, [&](int64_t v) { return G[v]; }, [&](int64_t v, double b) {
+            sweep_points(op, [&](int64_t v) {
+                const double b = G[v];
                 const double bg = (b != 0.0) ? __ddiv_rn(b, gamma) : 0.0;  // expact.cpp:137-138
                 G[v] = bg;
                 csum = __dadd_rn(csum, fabs(bg));
@@ -907,8 +879,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
                     const double* Tb = p.buf[tres];
                     const int fo = (fres == kBufF0) ? kBufF1 : kBufF0;
                     double* Fw = p.buf[fo];
-                    sweep_points4(op.n, [&](int64_t v) { return make_double2(Fa[v], Tb[v]); },
-                                  [&](int64_t v, double2 ft) { Fw[v] = __dadd_rn(ft.x, ft.y); });
+                    sweep_points(op, [&](int64_t v) { Fw[v] = __dadd_rn(Fa[v], Tb[v]); });
                     gsync(kTrFixup);
                     fstart = fo;
                 } else {
@@ -1054,9 +1025,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         if (run) {
             const double scl = __ddiv_rn(gamma, t);  // expact.cpp:150
             double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
-            sweep_points4(op.n, [&](int64_t v) { return make_double2(U[v], yv(v)); }, [&](int64_t v, double2 uy) {
+            sweep_points(op, [&](int64_t v) {
                 // out = u + tau * (scale * y)   (integrator.cpp:59-61, expact.cpp:151)
-                const double un = __dadd_rn(uy.x, __dmul_rn(t, __dmul_rn(scl, uy.y)));
+                const double un = __dadd_rn(U[v], __dmul_rn(t, __dmul_rn(scl, yv(v))));
                 U[v] = un;
                 if (p.want_metrics) metrics_local(sum, mx, mn, r2, v, un);
             });
@@ -1065,8 +1036,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             if (p.want_metrics) metrics_finish(step + 1, (step + 1) & 1);
         } else {
             const double scale = bordered ? __ddiv_rn(gamma, t) : 1.0;
-            sweep_points4(op.n, [&](int64_t v) { return yv(v); },
-                          [&](int64_t v, double y) { OUT[v] = bordered ? __dmul_rn(scale, y) : y; });
+            sweep_points(op, [&](int64_t v) { OUT[v] = bordered ? __dmul_rn(scale, yv(v)) : yv(v); });
         }
     }
 }
