@@ -54,7 +54,7 @@ struct gs_ctx {
     int64_t n = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 0;
-    int capacity = 0;  // co-resident CTAs of solve_kernel
+    int capacity = 0;  // co-resident CTAs of taylor_kernel
 
     // operator
     DevBuf pal, dvox, wtab, dtab;   // palette indices, fp64 D (fallback), w table, D table
@@ -68,7 +68,7 @@ struct gs_ctx {
     // vectors
     DevBuf u, g, f0, f1, t0, t1, out;
     // scratch
-    DevBuf part_b, part_c, part_u, slots, mslots, status, metrics, infos, normbits;
+    DevBuf part_b, part_c, part_u, slots, mslots, ctrl, metrics, infos, normbits;
 
     gs::StencilOp op{};
     int grid_blocks = 0;
@@ -251,18 +251,24 @@ void fill_rtab(double tol, double* rtab) {
     }
 }
 
+// Grid sizes of the launch sequence.  prep/taylor: one CTA per SM (the TMA rings take most
+// of shared memory); border/update/metrics: streaming kernels, two CTAs per SM.
+int stream_blocks(const gs_ctx* c) { return 2 * c->num_sms; }
+
 gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* metrics, gs_step_info* infos) {
-    const int gb = c->grid_blocks;
-    GS_CUDA(c, c->part_b.alloc(sizeof(double) * gb));
-    GS_CUDA(c, c->part_c.alloc(sizeof(double) * gb));
-    GS_CUDA(c, c->part_u.alloc(sizeof(double) * gb));
+    const int gb = c->grid_blocks;        // prep / taylor (co-resident)
+    const int sb = stream_blocks(c);      // border / update / metrics
+    const int pb = std::max(gb, sb);
+    GS_CUDA(c, c->part_b.alloc(sizeof(double) * pb));
+    GS_CUDA(c, c->part_c.alloc(sizeof(double) * pb));
+    GS_CUDA(c, c->part_u.alloc(sizeof(double) * pb));
     GS_CUDA(c, c->slots.alloc(sizeof(unsigned long long) * 12));
-    GS_CUDA(c, c->mslots.alloc(sizeof(unsigned long long) * 8));
-    GS_CUDA(c, c->status.alloc(sizeof(int) * 2));
+    GS_CUDA(c, c->mslots.alloc(sizeof(unsigned long long) * 4));
+    GS_CUDA(c, c->ctrl.alloc(sizeof(gs::Ctrl)));
     GS_CUDA(c, cudaMemsetAsync(c->slots.p, 0, sizeof(unsigned long long) * 12, c->stream));
-    const unsigned long long ms_init[8] = {0ull, ~0ull, 0ull, 0ull, 0ull, ~0ull, 0ull, 0ull};
+    const unsigned long long ms_init[4] = {0ull, ~0ull, 0ull, 0ull};
     GS_CUDA(c, cudaMemcpyAsync(c->mslots.p, ms_init, sizeof ms_init, cudaMemcpyHostToDevice, c->stream));
-    GS_CUDA(c, cudaMemsetAsync(c->status.p, 0, sizeof(int) * 2, c->stream));
+    GS_CUDA(c, cudaMemsetAsync(c->ctrl.p, 0, sizeof(gs::Ctrl), c->stream));
     if (metrics) GS_CUDA(c, c->metrics.alloc(sizeof(double) * 4 * (n_steps + 1)));
     if (infos) {
         GS_CUDA(c, c->infos.alloc(sizeof(gs_step_info) * std::max(1, n_steps)));
@@ -289,7 +295,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     p.part_u = c->part_u.as<double>();
     p.slots = c->slots.as<unsigned long long>();
     p.mslots = c->mslots.as<unsigned long long>();
-    p.status = c->status.as<int>();
+    p.ctrl = c->ctrl.as<gs::Ctrl>();
     DevBuf* bufs[gs::kNumBufs] = {&c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out};
     for (int b = 0; b < gs::kNumBufs; ++b) p.buf[b] = bufs[b]->as<double>();
     p.trace = nullptr;
@@ -300,12 +306,32 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
         p.trace = c->trace.as<unsigned long long>();
         p.trace_cap = c->trace_cap;
     }
-    void* args[] = {&p};
-    GS_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gs::solve_kernel), dim3(gb),
-                                           dim3(gs::kSolveThreads), args, p.use_tma ? gs::kDynSmemBytes : 0,
-                                           c->stream));
-    int status[2] = {0, 0};
-    GS_CUDA(c, cudaMemcpyAsync(status, c->status.p, sizeof status, cudaMemcpyDeviceToHost, c->stream));
+    const size_t dyn = p.use_tma ? gs::kDynSmemBytes : 0;
+    const dim3 blk(gs::kSolveThreads);
+    if (p.mode == gs::kModeApply) {
+        gs::prep_kernel<<<gb, blk, dyn, c->stream>>>(p, 0);
+        GS_CUDA(c, cudaGetLastError());
+    } else {
+        const int steps = p.mode == gs::kModeRun ? n_steps : 1;
+        if (p.mode == gs::kModeRun && metrics) {
+            gs::metrics_kernel<<<sb, blk, 0, c->stream>>>(p);
+            GS_CUDA(c, cudaGetLastError());
+        }
+        for (int step = 0; step < steps; ++step) {
+            gs::prep_kernel<<<gb, blk, dyn, c->stream>>>(p, step);
+            GS_CUDA(c, cudaGetLastError());
+            gs::border_kernel<<<sb, blk, 0, c->stream>>>(p, gb, step);
+            GS_CUDA(c, cudaGetLastError());
+            int border_blocks = sb;
+            void* args[] = {&p, &border_blocks, &step};
+            GS_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gs::taylor_kernel), dim3(gb), blk, args, dyn,
+                                                   c->stream));
+            gs::update_kernel<<<sb, blk, 0, c->stream>>>(p, step);
+            GS_CUDA(c, cudaGetLastError());
+        }
+    }
+    gs::Ctrl ctrl{};
+    GS_CUDA(c, cudaMemcpyAsync(&ctrl, c->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, c->stream));
     if (metrics)
         GS_CUDA(c, cudaMemcpyAsync(metrics, c->metrics.p, sizeof(double) * 4 * (n_steps + 1), cudaMemcpyDeviceToHost,
                                    c->stream));
@@ -318,9 +344,9 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
                                    cudaMemcpyDeviceToHost, c->stream));
     }
     GS_CUDA(c, cudaStreamSynchronize(c->stream));
-    if (status[0] != GS_OK) {
-        if (status[1] == 2) return fail(c, GS_ENUMERIC, "expmv: series diverged to non-finite values; reduce t");
-        if (status[0] == GS_EINVAL)
+    if (ctrl.status != GS_OK) {
+        if (ctrl.detail == 2) return fail(c, GS_ENUMERIC, "expmv: series diverged to non-finite values; reduce t");
+        if (ctrl.status == GS_EINVAL)
             return fail(c, GS_EINVAL, "select_params: operator norm must be finite and nonnegative");
         return fail(c, GS_ENUMERIC, "select_params: scaled operator norm too large for any stage count");
     }
@@ -370,11 +396,11 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
         return GS_ECUDA;
     }
     c->num_sms = prop.multiProcessorCount;
-    if ((e = cudaFuncSetAttribute(gs::solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kDynSmemBytes)) !=
-        cudaSuccess)
-        return bail(e, "cudaFuncSetAttribute(smem)");
+    for (const void* fn : {reinterpret_cast<const void*>(gs::taylor_kernel), reinterpret_cast<const void*>(gs::prep_kernel)})
+        if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kDynSmemBytes)) != cudaSuccess)
+            return bail(e, "cudaFuncSetAttribute(smem)");
     int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::solve_kernel, gs::kSolveThreads,
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::taylor_kernel, gs::kSolveThreads,
                                                            gs::kDynSmemBytes)) != cudaSuccess)
         return bail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) {
@@ -406,7 +432,7 @@ void gs_destroy(gs_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->pal, &c->dvox, &c->wtab, &c->dtab, &c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out,
-                      &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->status, &c->metrics, &c->infos,
+                      &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->ctrl, &c->metrics, &c->infos,
                       &c->normbits, &c->trace})
         b->release();
     if (c->stream) cudaStreamDestroy(c->stream);

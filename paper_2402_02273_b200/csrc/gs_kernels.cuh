@@ -57,6 +57,16 @@ constexpr int kT1Planes = 3;  // T1(z+1) is written while T1(z-1) is read; T1(z)
 constexpr int k2RingBytes = k2Stages * k2SlotBytes + kT1Planes * kT1Bytes + 128;
 constexpr int kDynSmemBytes = kRingBytes > k2RingBytes ? kRingBytes : k2RingBytes;
 
+// Device-resident control block shared by the kernels of one launch sequence.
+struct Ctrl {
+    double bnorm, gamma, prev0;
+    int branch;           // 0 Taylor, 1 t == 0, 2 ||b||_1 == 0, 3 small norm
+    int status, detail;   // gs_status of the first failure (later kernels return at once)
+    int fres, tres;       // Taylor result: F[fres] (+ T[tres] when implicit)
+    unsigned int ticket;  // last-block-done counter (metrics)
+    int ntrace;
+};
+
 struct SolveParams {
     // TMA descriptors (64-byte aligned by type): halo-box and own-box maps per vector, labels
     CUtensorMap xmap[kNumBufs];
@@ -84,7 +94,7 @@ struct SolveParams {
     double* part_u;         // [grid] block partial sums of u (metrics)
     unsigned long long* slots;   // [3][4] rotating max slots for per-term reductions
     unsigned long long* mslots;  // [2][4] metric max/min/r2 slots (step parity)
-    int* status;            // [0] gs_status, [1] detail
+    Ctrl* ctrl;
     unsigned long long* trace;  // optional phase trace: (tag, globaltimer ns) pairs
     int trace_cap;
 };
@@ -100,7 +110,12 @@ __global__ void material_kernel(const uint8_t* stack, int w, int hgt, int slices
 __global__ void colsum_norm_kernel(StencilOp op, unsigned long long* out_bits);
 // Per-voxel D(x) reconstruction (for gs_get_diffusion in palette mode)
 __global__ void expand_palette_kernel(const uint8_t* pal, const double* dtab, int64_t n, double* d);
-// The persistent exponential-Euler kernel (cooperative launch)
-__global__ void solve_kernel(const __grid_constant__ SolveParams p);
+// The exponential-Euler step as a launch sequence (gs_solve.cu):
+//   [metrics_kernel] -> per step: prep_kernel -> border_kernel -> taylor_kernel (cooperative) -> update_kernel
+__global__ void metrics_kernel(const __grid_constant__ SolveParams p);
+__global__ void prep_kernel(const __grid_constant__ SolveParams p, int step);
+__global__ void border_kernel(const __grid_constant__ SolveParams p, int prep_blocks, int step);
+__global__ void taylor_kernel(const __grid_constant__ SolveParams p, int border_blocks, int step);
+__global__ void update_kernel(const __grid_constant__ SolveParams p, int step);
 
 }  // namespace gs

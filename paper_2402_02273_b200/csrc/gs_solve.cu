@@ -580,84 +580,56 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
 
 enum TermKind { kFirstZero, kFirstBorder, kFirstPlain, kNext };
 
-}  // namespace
-
-__global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_constant__ SolveParams p) {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ Smem sm;
-    extern __shared__ __align__(128) unsigned char dyn[];
-    const StencilOp& op = p.op;
-    if (op.pal)
-        for (int q = threadIdx.x; q < 256; q += blockDim.x) sm.wtab[q] = __ldg(op.wtab + q);
-    Ring ring{dyn, sm.bar1};
-    Ring2 ring2{dyn, sm.bar2};
-    if (p.use_tma && threadIdx.x == 0) {
+// Per-block setup shared by the kernels: w table in shared memory, mbarriers for TMA.
+__device__ __forceinline__ void block_setup(const SolveParams& p, Smem& sm, bool with_tma) {
+    if (p.op.pal)
+        for (int q = threadIdx.x; q < 256; q += blockDim.x) sm.wtab[q] = __ldg(p.op.wtab + q);
+    if (with_tma && threadIdx.x == 0) {
         for (int s = 0; s < kTmaStages; ++s) mbar_init(sm.bar1 + s, 1);
         for (int s = 0; s < k2Stages; ++s) mbar_init(sm.bar2 + s, 1);
         mbar_fence_init();
         for (int b = 0; b < kNumBufs; ++b) tma_prefetch_desc(&p.xmap[b]);
     }
     __syncthreads();
-    uint32_t seq = 0, seq2 = 0, pmask2 = 0;
-    // Grid barrier; with TMA, first order this thread's generic global writes before any
-    // later async-proxy (TMA) read of them.
-    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    int ntrace = 0;
-    auto trace = [&](int tag) {
-        if (p.trace && leader && ntrace < p.trace_cap) {
+}
+
+__device__ __forceinline__ void trace_mark(const SolveParams& p, int tag) {
+    if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int k = atomicAdd(&p.ctrl->ntrace, 1);
+        if (k < p.trace_cap) {
             unsigned long long tnow;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
-            p.trace[2 * ntrace] = static_cast<unsigned long long>(tag);
-            p.trace[2 * ntrace + 1] = tnow;
-            ++ntrace;
+            p.trace[2 * k] = static_cast<unsigned long long>(tag);
+            p.trace[2 * k + 1] = tnow;
         }
-    };
-    trace(kTrStart);
-    auto gsync = [&](int tag) {
-        if (p.use_tma) fence_proxy_async_global();
-        grid.sync();
-        trace(tag);
-    };
-    int round = 0;  // per-term max-reduction rounds (slot rotation, identical in every CTA)
+    }
+}
 
-    // Stencil sweep dispatch: X = stencil input, F / B = own-voxel side inputs.
-    auto stencil = [&](int xb, int fb, int bb, auto&& body) {
-        const bool nf = fb >= 0, nb = bb >= 0;
-        if (p.use_tma) {
-            if (nf && nb) sweep_tma<true, true>(p, ring, xb, fb, bb, seq, sm.wtab, body);
-            else if (nf) sweep_tma<true, false>(p, ring, xb, fb, 0, seq, sm.wtab, body);
-            else if (nb) sweep_tma<false, true>(p, ring, xb, 0, bb, seq, sm.wtab, body);
-            else sweep_tma<false, false>(p, ring, xb, 0, 0, seq, sm.wtab, body);
-        } else {
-            sweep_l1(op, p.buf[xb], nf ? p.buf[fb] : nullptr, nb ? p.buf[bb] : nullptr, sm.wtab, body);
-        }
-    };
+// Single-term stencil sweep dispatch (TMA ring or L1 fallback).
+template <class Body>
+__device__ __forceinline__ void stencil_sweep(const SolveParams& p, Smem& sm, const Ring& ring, uint32_t& seq, int xb,
+                                              int fb, int bb, Body&& body) {
+    const bool nf = fb >= 0, nb = bb >= 0;
+    if (p.use_tma) {
+        if (nf && nb) sweep_tma<true, true>(p, ring, xb, fb, bb, seq, sm.wtab, body);
+        else if (nf) sweep_tma<true, false>(p, ring, xb, fb, 0, seq, sm.wtab, body);
+        else if (nb) sweep_tma<false, true>(p, ring, xb, 0, bb, seq, sm.wtab, body);
+        else sweep_tma<false, false>(p, ring, xb, 0, 0, seq, sm.wtab, body);
+    } else {
+        sweep_l1(p.op, p.buf[xb], nf ? p.buf[fb] : nullptr, nb ? p.buf[bb] : nullptr, sm.wtab, body);
+    }
+}
 
-    auto sync_round = [&](int tag) {
-        gsync(tag);
-        if (leader) {
-            unsigned long long* z = p.slots + ((round + 2) % 3) * 4;
-            z[0] = z[1] = z[2] = z[3] = 0ull;
-        }
-        ++round;
-    };
-    auto push_max2 = [&](double a, double b) {
-        double v[2] = {a, b};
-        block_reduce<2, true>(v, sm);
-        if (threadIdx.x == 0) {
-            unsigned long long* s = p.slots + (round % 3) * 4;
-            if (v[0] > 0.0) atomicMax(s + 0, static_cast<unsigned long long>(__double_as_longlong(v[0])));
-            if (v[1] > 0.0) atomicMax(s + 1, static_cast<unsigned long long>(__double_as_longlong(v[1])));
-        }
-    };
-
-    // compute_metrics (integrator.cpp:65-89): the sum in a fixed tree (the reference's serial
-    // sum differs in the last bits), max/min/front radius exactly.
-    auto metrics_local = [&](double& sum, double& mx, double& mn, double& r2, int64_t v, double u) {
+// compute_metrics (integrator.cpp:65-89) accumulation: the sum in a fixed tree (the
+// reference's serial sum differs in the last bits), max/min/front radius exactly.
+struct MetricAcc {
+    double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
+    __device__ __forceinline__ void add(const SolveParams& p, int64_t v, double u) {
         sum = __dadd_rn(sum, u);
         mx = nan_dropping_max(mx, u);
         mn = (u < mn) ? u : mn;
         if (u >= p.front_threshold) {
+            const StencilOp& op = p.op;
             const int i = static_cast<int>(v % op.nx);
             const int j = static_cast<int>((v / op.nx) % op.ny);
             const int k = static_cast<int>(v / op.sz);
@@ -667,377 +639,487 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
             r2 = nan_dropping_max(r2, d2);
         }
-    };
-    auto metrics_push = [&](double sum, double mx, double mn, double r2, int parity) {
-        double s[1] = {sum};
-        block_reduce<1, false>(s, sm);
-        if (threadIdx.x == 0) p.part_u[blockIdx.x] = s[0];
-        const double mxw = warp_max(mx);
-        double mnw = mn;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double q = __shfl_xor_sync(0xffffffffu, mnw, o);
-            mnw = (q < mnw) ? q : mnw;
-        }
-        const double r2w = warp_max(r2);
-        if ((threadIdx.x & 31) == 0) {
-            unsigned long long* ms = p.mslots + parity * 4;
-            atomicMax(ms + 0, ordered_key(mxw));
-            atomicMin(ms + 1, ordered_key(mnw));
-            if (r2w > 0.0) atomicMax(ms + 2, static_cast<unsigned long long>(__double_as_longlong(r2w)));
-        }
-    };
-    auto metrics_finish = [&](int node, int parity) {
-        const double sum = grid_sum(p.part_u, p.grid_blocks, sm);
-        if (leader) {
-            unsigned long long* ms = p.mslots + parity * 4;
-            const double cell = __dmul_rn(__dmul_rn(p.h, p.h), p.h);
-            double* out = p.metrics + 4 * node;
-            out[0] = __dmul_rn(cell, sum);
-            out[1] = from_ordered_key(__ldcg(ms + 0));
-            out[2] = from_ordered_key(__ldcg(ms + 1));
-            out[3] = sqrt(__longlong_as_double(static_cast<long long>(__ldcg(ms + 2))));
-            ms[0] = 0ull;
-            ms[1] = ~0ull;
-            ms[2] = 0ull;
-        }
-    };
+    }
+};
 
-    double* const U = p.buf[kBufU];
+// Block-reduce the metric accumulators; the last block to finish (ticket) finalises node
+// `node` from the per-block partials in a fixed order (deterministic for the launch size).
+__device__ void metrics_commit(const SolveParams& p, Smem& sm, MetricAcc& a, int node) {
+    double s[1] = {a.sum};
+    block_reduce<1, false>(s, sm);
+    const double mxw = warp_max(a.mx);
+    double mnw = a.mn;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double q = __shfl_xor_sync(0xffffffffu, mnw, o);
+        mnw = (q < mnw) ? q : mnw;
+    }
+    const double r2w = warp_max(a.r2);
+    unsigned long long* ms = p.mslots;
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(ms + 0, ordered_key(mxw));
+        atomicMin(ms + 1, ordered_key(mnw));
+        if (r2w > 0.0) atomicMax(ms + 2, static_cast<unsigned long long>(__double_as_longlong(r2w)));
+    }
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        p.part_u[blockIdx.x] = s[0];
+        __threadfence();
+        last = atomicAdd(&p.ctrl->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const double sum = grid_sum(p.part_u, gridDim.x, sm);
+    if (threadIdx.x == 0) {
+        const double cell = __dmul_rn(__dmul_rn(p.h, p.h), p.h);
+        double* out = p.metrics + 4 * node;
+        out[0] = __dmul_rn(cell, sum);
+        out[1] = from_ordered_key(__ldcg(ms + 0));
+        out[2] = from_ordered_key(__ldcg(ms + 1));
+        out[3] = sqrt(__longlong_as_double(static_cast<long long>(__ldcg(ms + 2))));
+        ms[0] = 0ull;
+        ms[1] = ~0ull;
+        ms[2] = 0ull;
+        p.ctrl->ticket = 0u;
+        __threadfence();
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// k_metrics: compute_metrics of the resident state (run node 0)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSolveThreads) metrics_kernel(const __grid_constant__ SolveParams p) {
+    __shared__ Smem sm;
+    if (p.ctrl->status) return;
+    const double* U = p.buf[kBufU];
+    MetricAcc a;
+    sweep_points(p.op, [&](int64_t v) { a.add(p, v, U[v]); });
+    metrics_commit(p, sm, a, 0);
+}
+
+// ------------------------------------------------------------------------------------------
+// K2 prep: RHS g = A u + rho u(1-u) and ||g||_1 partials (run); ||b||_1 / ||b||_inf
+// partials (phi1v / expmv); y = A x (apply)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSolveThreads, 1) prep_kernel(const __grid_constant__ SolveParams p, int step) {
+    __shared__ Smem sm;
+    extern __shared__ __align__(128) unsigned char dyn[];
+    if (p.ctrl->status) return;
+    block_setup(p, sm, p.use_tma);
+    if (step == 0) trace_mark(p, kTrStart);
+    Ring ring{dyn, sm.bar1};
+    uint32_t seq = 0;
     double* const G = p.buf[kBufG];
     double* const OUT = p.buf[kBufOut];
-
-    // -------------------------------------------------------------- y = A x
     if (p.mode == kModeApply) {
-        stencil(kBufG, -1, -1, [&](int64_t v, double acc, double, double, double) { OUT[v] = acc; });
+        stencil_sweep(p, sm, ring, seq, kBufG, -1, -1, [&](int64_t v, double acc, double, double, double) { OUT[v] = acc; });
+        return;
+    }
+    double part = 0.0;
+    if (p.mode == kModeRun) {
+        // g = A u; g += rho*u*(1-u)   (integrator.cpp:54-57)
+        stencil_sweep(p, sm, ring, seq, kBufU, -1, -1, [&](int64_t v, double acc, double u, double, double) {
+            const double g = __dadd_rn(acc, __dmul_rn(__dmul_rn(p.rho, u), __dsub_rn(1.0, u)));
+            G[v] = g;
+            part = __dadd_rn(part, fabs(g));
+        });
+    } else if (p.mode == kModePhi1v) {
+        sweep_points(p.op, [&](int64_t v) { part = __dadd_rn(part, fabs(G[v])); });  // expact.cpp:110
+    } else {
+        sweep_points(p.op, [&](int64_t v) { part = nan_dropping_max(part, fabs(G[v])); });  // expact.cpp:80
+    }
+    double s[1] = {part};
+    if (p.mode == kModeExpmv) block_reduce<1, true>(s, sm);
+    else block_reduce<1, false>(s, sm);
+    if (threadIdx.x == 0) p.part_b[blockIdx.x] = s[0];
+    if (p.use_tma) fence_proxy_async_global();
+}
+
+// ------------------------------------------------------------------------------------------
+// bordered column: ||b||_1, the degenerate branches, gamma and b/gamma + its column sum
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_constant__ SolveParams p, int prep_blocks,
+                                                               int step) {
+    __shared__ Smem sm;
+    Ctrl* ctrl = p.ctrl;
+    if (ctrl->status) return;
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    gs_step_info* info = (p.infos && leader) ? p.infos + step : nullptr;
+    const double t = p.tau;
+    double* const G = p.buf[kBufG];
+    if (p.mode == kModeExpmv) {
+        // prev = ||b||_inf (max of the partials: order-free)
+        if (threadIdx.x == 0) {
+            double m = 0.0;
+            for (int b = 0; b < prep_blocks; ++b) m = nan_dropping_max(m, __ldcg(p.part_b + b));
+            if (leader) {
+                ctrl->prev0 = m;
+                ctrl->branch = 0;
+                ctrl->gamma = 0.0;
+            }
+        }
+        if (info) {
+            info->branch = 0;
+            info->anorm = p.anorm;
+        }
+        return;
+    }
+    const double bnorm = grid_sum(p.part_b, prep_blocks, sm);  // expact.cpp:110 (tree order)
+    int branch = 0;
+    if (t == 0.0) branch = 1;                                  // expact.cpp:108
+    else if (bnorm == 0.0) branch = 2;                         // expact.cpp:111
+    else if (__dmul_rn(fabs(t), p.anorm) <= 1e-8) branch = 3;  // expact.cpp:114
+    const double gamma = branch == 0 ? __ddiv_rn(bnorm, p.anorm) : 0.0;  // expact.cpp:126
+    if (leader) {
+        ctrl->bnorm = bnorm;
+        ctrl->branch = branch;
+        ctrl->gamma = gamma;
+        ctrl->prev0 = 1.0;  // ||e_{n+1}||_inf
+    }
+    if (info) {
+        info->s = info->m = 1;
+        info->branch = branch;
+        info->total_terms = 0;
+        info->anorm = p.anorm;
+        info->bnorm = bnorm;
+        info->gamma = gamma;
+        info->coln = info->norm_tA = 0.0;
+    }
+    if (branch != 0) return;
+    // b/gamma in place where b != 0 (expact.cpp:137-138) and its column sum (sparse.cpp:36-38)
+    double csum = 0.0;
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t n = p.op.n;
+    const int64_t n2 = n >> 1;
+    double2* G2 = reinterpret_cast<double2*>(G);
+    auto bg = [&](double b) { return (b != 0.0) ? __ddiv_rn(b, gamma) : 0.0; };
+    constexpr int U = 4;
+    for (int64_t i = tid; i < n2; i += U * stride) {
+        double2 g[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+            if (i + k * stride < n2) g[k] = G2[i + k * stride];
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+            if (i + k * stride < n2) {
+                const double2 r = make_double2(bg(g[k].x), bg(g[k].y));
+                G2[i + k * stride] = r;
+                csum = __dadd_rn(csum, fabs(r.x));
+                csum = __dadd_rn(csum, fabs(r.y));
+            }
+    }
+    if ((n & 1) && tid == 0) {
+        const double r = bg(G[n - 1]);
+        G[n - 1] = r;
+        csum = __dadd_rn(csum, fabs(r));
+    }
+    double s[1] = {csum};
+    block_reduce<1, false>(s, sm);
+    if (threadIdx.x == 0) p.part_c[blockIdx.x] = s[0];
+    if (p.use_tma) fence_proxy_async_global();
+}
+
+// ------------------------------------------------------------------------------------------
+// K4 Taylor loop (cooperative, persistent): (s, m) on device, then the stages of fused
+// two-term sweeps (TMA) or single-term sweeps (fallback) with the in-kernel termination
+// test; grid barriers between terms.  The small-norm branch's stencil pass lives here too.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_constant__ SolveParams p,
+                                                                  int border_blocks, int step) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ Smem sm;
+    extern __shared__ __align__(128) unsigned char dyn[];
+    Ctrl* ctrl = p.ctrl;
+    if (ctrl->status) return;
+    const StencilOp& op = p.op;
+    block_setup(p, sm, p.use_tma);
+    Ring ring{dyn, sm.bar1};
+    Ring2 ring2{dyn, sm.bar2};
+    uint32_t seq = 0, seq2 = 0, pmask2 = 0;
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    gs_step_info* info = (p.infos && leader) ? p.infos + step : nullptr;
+    // Grid barrier; with TMA, first order this thread's generic global writes before any
+    // later async-proxy (TMA) read of them.
+    auto gsync = [&](int tag) {
+        if (p.use_tma) fence_proxy_async_global();
+        grid.sync();
+        trace_mark(p, tag);
+    };
+    int round = 0;  // per-term max-reduction rounds (slot rotation, identical in every CTA)
+    auto sync_round = [&](int tag) {
+        gsync(tag);
+        if (leader) {
+            unsigned long long* z = p.slots + ((round + 2) % 3) * 4;
+            z[0] = z[1] = z[2] = z[3] = 0ull;
+        }
+        ++round;
+    };
+    double* const G = p.buf[kBufG];
+    const bool bordered = p.mode != kModeExpmv;
+    const double t = p.tau;
+    const int branch = __ldcg(&ctrl->branch);
+    if (leader) {
+        ctrl->fres = -1;
+        ctrl->tres = -1;
+    }
+    if (branch != 0) {
+        if (branch == 3) {
+            // incr = b + 0.5*t*(A b)   (expact.cpp:117-121), into T0
+            double* INC = p.buf[kBufT0];
+            const double ht = __dmul_rn(0.5, t);
+            stencil_sweep(p, sm, ring, seq, kBufG, -1, -1, [&](int64_t v, double acc, double b, double, double) {
+                INC[v] = __dadd_rn(b, __dmul_rn(ht, acc));
+            });
+        }
         return;
     }
 
-    const bool run = p.mode == kModeRun;
-    const bool bordered = p.mode != kModeExpmv;
-    const double t = p.tau;
-
-    if (run && p.want_metrics) {
-        double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
-        sweep_points(op, [&](int64_t v) { metrics_local(sum, mx, mn, r2, v, U[v]); });
-        metrics_push(sum, mx, mn, r2, 0);
-        gsync(kTrMetrics0);
-        metrics_finish(0, 0);
+    // ------------------------------------------- bordered column norm and (s, m)
+    const double gamma = __ldcg(&ctrl->gamma);
+    double norm_tA;
+    if (bordered) {
+        const double coln = grid_sum(p.part_c, border_blocks, sm);
+        // bordered ||.||_1 = max over columns: A's columns, then column n (sparse.cpp:39-40)
+        norm_tA = __dmul_rn(fabs(t), nan_dropping_max(p.anorm, coln));
+        if (info) info->coln = coln;
+    } else {
+        norm_tA = __dmul_rn(fabs(t), p.anorm);
+    }
+    int s_st = 1, m_deg = 1;
+    const int sel = select_params_dev(norm_tA, p.rtab, &s_st, &m_deg);
+    if (info) {
+        info->norm_tA = norm_tA;
+        info->s = s_st;
+        info->m = m_deg;
+    }
+    if (sel != GS_OK) {
+        if (leader) {
+            ctrl->status = sel;
+            ctrl->detail = 1;  // select_params
+        }
+        return;  // uniform across CTAs
     }
 
-    const int n_steps = run ? p.n_steps : 1;
-    for (int step = 0; step < n_steps; ++step) {
-        gs_step_info* info = (p.infos && leader) ? p.infos + step : nullptr;
-        if (info) {
-            info->s = info->m = 1;
-            info->branch = 0;
-            info->total_terms = 0;
-            info->anorm = p.anorm;
-            info->bnorm = info->coln = info->gamma = info->norm_tA = 0.0;
-        }
-        double bnorm = 0.0;
-        // ---------------------------------------------------------- K2: RHS + ||b||_1
-        if (run) {
-            // g = A u; g += rho*u*(1-u)   (integrator.cpp:54-57)
-            double bsum = 0.0;
-            stencil(kBufU, -1, -1, [&](int64_t v, double acc, double u, double, double) {
-                const double g = __dadd_rn(acc, __dmul_rn(__dmul_rn(p.rho, u), __dsub_rn(1.0, u)));
-                G[v] = g;
-                bsum = __dadd_rn(bsum, fabs(g));
-            });
-            double s[1] = {bsum};
-            block_reduce<1, false>(s, sm);
-            if (threadIdx.x == 0) p.part_b[blockIdx.x] = s[0];
-        } else if (bordered) {
-            double bsum = 0.0;
-            sweep_points(op, [&](int64_t v) { bsum = __dadd_rn(bsum, fabs(G[v])); });
-            double s[1] = {bsum};
-            block_reduce<1, false>(s, sm);
-            if (threadIdx.x == 0) p.part_b[blockIdx.x] = s[0];
-        } else {
-            // expmv: prev = ||b||_inf at stage 0 (expact.cpp:80)
-            double mb = 0.0;
-            sweep_points(op, [&](int64_t v) { mb = nan_dropping_max(mb, fabs(G[v])); });
-            push_max2(mb, 0.0);
-        }
-        gsync(kTrRhs);
-
-        int branch = 0;
-        double prev0 = 1.0;  // ||e_{n+1}||_inf for the bordered action
-        if (bordered) {
-            bnorm = grid_sum(p.part_b, p.grid_blocks, sm);
-            if (info) info->bnorm = bnorm;
-            if (t == 0.0) branch = 1;                                  // expact.cpp:108
-            else if (bnorm == 0.0) branch = 2;                         // expact.cpp:111
-            else if (__dmul_rn(fabs(t), p.anorm) <= 1e-8) branch = 3;  // expact.cpp:114
-        } else {
-            prev0 = slot_read(p.slots + (round % 3) * 4);
+    // ------------------------------------------------------------- K4: Taylor terms
+    const double tau_s = __ddiv_rn(t, static_cast<double>(s_st));  // expact.cpp:73
+    double prev = __ldcg(&ctrl->prev0);
+    int64_t total_terms = 0;
+    int fres = -1, tres = -1;  // stage result: F[fres] (+ T[tres] when tres >= 0, implicit)
+    auto finite_or_fail = [&](double cur, double fnorm) {
+        if (!isfinite(cur) || !isfinite(fnorm)) {  // expact.cpp:90-91
             if (leader) {
-                unsigned long long* z = p.slots + ((round + 2) % 3) * 4;
-                z[0] = z[1] = z[2] = z[3] = 0ull;
+                ctrl->status = GS_ENUMERIC;
+                ctrl->detail = 2;
             }
-            ++round;
+            return false;
         }
-        if (info) info->branch = branch;
-
-        if (branch != 0) {
-            double* INC = p.buf[kBufT0];
-            if (branch == 3) {
-                // incr = b + 0.5*t*(A b)   (expact.cpp:117-121)
-                const double ht = __dmul_rn(0.5, t);
-                stencil(kBufG, -1, -1, [&](int64_t v, double acc, double b, double, double) {
-                    const double incr = __dadd_rn(b, __dmul_rn(ht, acc));
-                    if (run) INC[v] = incr;
-                    else OUT[v] = incr;
-                });
-                if (run) gsync(kTrBranch);
+        return true;
+    };
+    if (p.use_tma) {
+        // Fused two-term sweeps; the decisions are taken term by term exactly as the
+        // reference's loop (expact.cpp:81-95), on the four maxima of each sweep.
+        int fsel = 0, tsel = 0;
+        for (int stage = 0; stage < s_st; ++stage) {
+            int fstart;  // buffer holding this stage's starting f (the stencil input)
+            if (stage == 0) {
+                fstart = bordered ? -1 : kBufG;
+            } else if (tres >= 0) {
+                // previous stage ended on its implicit F2: materialise f = F1 + T2
+                const double* Fa = p.buf[fres];
+                const double* Tb = p.buf[tres];
+                const int fo = (fres == kBufF0) ? kBufF1 : kBufF0;
+                double* Fw = p.buf[fo];
+                sweep_points(op, [&](int64_t v) { Fw[v] = __dadd_rn(Fa[v], Tb[v]); });
+                gsync(kTrFixup);
+                fstart = fo;
+            } else {
+                fstart = fres;
             }
-            if (run) {
-                double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
-                sweep_points(op, [&](int64_t v) {
-                    const double incr = branch == 1 ? G[v] : branch == 2 ? 0.0 : INC[v];
-                    const double un = __dadd_rn(U[v], __dmul_rn(t, incr));
-                    U[v] = un;
-                    if (p.want_metrics) metrics_local(sum, mx, mn, r2, v, un);
-                });
-                if (p.want_metrics) metrics_push(sum, mx, mn, r2, (step + 1) & 1);
-                gsync(kTrBranch);
-                if (p.want_metrics) metrics_finish(step + 1, (step + 1) & 1);
-            } else if (branch != 3) {
-                sweep_points(op, [&](int64_t v) { OUT[v] = branch == 1 ? G[v] : 0.0; });
-            }
-            continue;
-        }
-
-        // ------------------------------------------- bordered column b/gamma and (s, m)
-        double gamma = 0.0, norm_tA;
-        if (bordered) {
-            gamma = __ddiv_rn(bnorm, p.anorm);  // expact.cpp:126
-            double csum = 0.0;
-            sweep_points(op, [&](int64_t v) {
-                const double b = G[v];
-                const double bg = (b != 0.0) ? __ddiv_rn(b, gamma) : 0.0;  // expact.cpp:137-138
-                G[v] = bg;
-                csum = __dadd_rn(csum, fabs(bg));
-            });
-            double s[1] = {csum};
-            block_reduce<1, false>(s, sm);
-            if (threadIdx.x == 0) p.part_c[blockIdx.x] = s[0];
-            gsync(kTrBorder);
-            const double coln = grid_sum(p.part_c, p.grid_blocks, sm);
-            // bordered ||.||_1 = max over columns: A's columns, then column n (sparse.cpp:39-40)
-            norm_tA = __dmul_rn(fabs(t), nan_dropping_max(p.anorm, coln));
-            if (info) {
-                info->coln = coln;
-                info->gamma = gamma;
-            }
-        } else {
-            norm_tA = __dmul_rn(fabs(t), p.anorm);
-        }
-        int s_st = 1, m_deg = 1;
-        const int sel = select_params_dev(norm_tA, p.rtab, &s_st, &m_deg);
-        if (info) {
-            info->norm_tA = norm_tA;
-            info->s = s_st;
-            info->m = m_deg;
-        }
-        if (sel != GS_OK) {
-            if (leader) {
-                p.status[0] = sel;
-                p.status[1] = 1;  // select_params
-            }
-            return;  // uniform across CTAs
-        }
-
-        // ------------------------------------------------------------- K4: Taylor terms
-        const double tau_s = __ddiv_rn(t, static_cast<double>(s_st));  // expact.cpp:73
-        double prev = prev0;
-        int64_t total_terms = 0;
-        int fres = -1, tres = -1;  // stage result: F[fres] (+ T[tres] when tres >= 0, implicit)
-        // Reads the next slot round; returns false (after flagging) on a non-finite series.
-        auto finite_or_fail = [&](double cur, double fnorm) {
-            if (!isfinite(cur) || !isfinite(fnorm)) {  // expact.cpp:90-91
-                if (leader) {
-                    p.status[0] = GS_ENUMERIC;
-                    p.status[1] = 2;
+            if (fstart == kBufF0) fsel = 1;
+            else if (fstart == kBufF1) fsel = 0;
+            int used = 0;
+            int kind = fstart < 0 ? k2FirstZero : (bordered ? k2FirstBorder : k2FirstPlain);
+            int xb = fstart, fb = -1;
+            while (true) {
+                const double c1 = __ddiv_rn(tau_s, static_cast<double>(used + 1));  // expact.cpp:83
+                const double c2 = __ddiv_rn(tau_s, static_cast<double>(used + 2));
+                const int fout = kBufF0 + fsel, tout = kBufT0 + tsel;
+                double mx[4] = {0.0, 0.0, 0.0, 0.0};
+                {
+                    const int xb_ = xb < 0 ? 0 : xb, fb_ = fb < 0 ? 0 : fb;
+                    double* oT = p.buf[tout];
+                    double* oF = p.buf[fout];
+                    if (kind == k2Next)
+                        sweep2_tma<k2Next>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                    else if (kind == k2FirstBorder)
+                        sweep2_tma<k2FirstBorder>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                    else if (kind == k2FirstZero)
+                        sweep2_tma<k2FirstZero>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                    else
+                        sweep2_tma<k2FirstPlain>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
                 }
-                return false;
-            }
-            return true;
-        };
-        if (p.use_tma) {
-            // Fused two-term sweeps; the decisions are taken term by term exactly as the
-            // reference's loop (expact.cpp:81-95), on the four maxima of each sweep.
-            int fsel = 0, tsel = 0;
-            for (int stage = 0; stage < s_st; ++stage) {
-                int fstart;  // buffer holding this stage's starting f (the stencil input)
-                if (stage == 0) {
-                    fstart = bordered ? -1 : kBufG;
-                } else if (tres >= 0) {
-                    // previous stage ended on its implicit F2: materialise f = F1 + T2
-                    const double* Fa = p.buf[fres];
-                    const double* Tb = p.buf[tres];
-                    const int fo = (fres == kBufF0) ? kBufF1 : kBufF0;
-                    double* Fw = p.buf[fo];
-                    sweep_points(op, [&](int64_t v) { Fw[v] = __dadd_rn(Fa[v], Tb[v]); });
-                    gsync(kTrFixup);
-                    fstart = fo;
-                } else {
-                    fstart = fres;
-                }
-                if (fstart == kBufF0) fsel = 1;
-                else if (fstart == kBufF1) fsel = 0;
-                int used = 0;
-                int kind = fstart < 0 ? k2FirstZero : (bordered ? k2FirstBorder : k2FirstPlain);
-                int xb = fstart, fb = -1;
-                bool ended = false;
-                while (!ended) {
-                    const double c1 = __ddiv_rn(tau_s, static_cast<double>(used + 1));  // expact.cpp:83
-                    const double c2 = __ddiv_rn(tau_s, static_cast<double>(used + 2));
-                    const int fout = kBufF0 + fsel, tout = kBufT0 + tsel;
-                    double mx[4] = {0.0, 0.0, 0.0, 0.0};
-                    {
-                        const int xb_ = xb < 0 ? 0 : xb, fb_ = fb < 0 ? 0 : fb;
-                        double* oT = p.buf[tout];
-                        double* oF = p.buf[fout];
-                        if (kind == k2Next)
-                            sweep2_tma<k2Next>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
-                        else if (kind == k2FirstBorder)
-                            sweep2_tma<k2FirstBorder>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
-                        else if (kind == k2FirstZero)
-                            sweep2_tma<k2FirstZero>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
-                        else
-                            sweep2_tma<k2FirstPlain>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
-                    }
-                    block_reduce<4, true>(mx, sm);
-                    if (threadIdx.x == 0) {
-                        unsigned long long* sl = p.slots + (round % 3) * 4;
+                block_reduce<4, true>(mx, sm);
+                if (threadIdx.x == 0) {
+                    unsigned long long* sl = p.slots + (round % 3) * 4;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            if (mx[q] > 0.0) atomicMax(sl + q, static_cast<unsigned long long>(__double_as_longlong(mx[q])));
-                    }
-                    sync_round(kind == k2Next ? kTrFusedNext : kTrFusedFirst);
-                    const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
-                    double cur[2] = {slot_read(sl + 0), slot_read(sl + 2)};
-                    double fn[2] = {slot_read(sl + 1), slot_read(sl + 3)};
-                    if (bordered) {
-                        fn[0] = nan_dropping_max(fn[0], 1.0);  // f_n == 1 (expact.cpp:89)
-                        fn[1] = nan_dropping_max(fn[1], 1.0);
-                    }
-                    // term used+1 (result F1, explicit)
-                    ++used;
-                    if (!finite_or_fail(cur[0], fn[0])) return;
-                    if (__dadd_rn(prev, cur[0]) <= __dmul_rn(p.tol, fn[0]) || used == m_deg) {
-                        prev = fn[0];
-                        fres = fout;
-                        tres = -1;
-                        ended = true;
-                        break;
-                    }
-                    prev = cur[0];
-                    // term used+1 (result F2 = F1 + T2, implicit)
-                    ++used;
-                    if (!finite_or_fail(cur[1], fn[1])) return;
-                    if (__dadd_rn(prev, cur[1]) <= __dmul_rn(p.tol, fn[1]) || used == m_deg) {
-                        prev = fn[1];
-                        fres = fout;
-                        tres = tout;
-                        ended = true;
-                        break;
-                    }
-                    prev = cur[1];
-                    kind = k2Next;
-                    xb = tout;
-                    fb = fout;
-                    fsel ^= 1;
-                    tsel ^= 1;
+                    for (int q = 0; q < 4; ++q)
+                        if (mx[q] > 0.0) atomicMax(sl + q, static_cast<unsigned long long>(__double_as_longlong(mx[q])));
                 }
-                total_terms += used;
-                if (info && stage < kMaxLoggedStages) info->terms[stage] = used;
-            }
-        } else {
-            int fcur = bordered ? -1 : kBufG;  // -1: f = e_{n+1} (all zero) for the bordered action
-            int tprev = -1;
-            int fsel = 0, tsel = 0;
-            for (int stage = 0; stage < s_st; ++stage) {
-                int used = 0;
-                for (int j = 1; j <= m_deg; ++j) {
-                    const double c = __ddiv_rn(tau_s, static_cast<double>(j));  // expact.cpp:83
-                    const TermKind kind =
-                        j > 1 ? kNext : (fcur < 0 ? kFirstZero : (bordered ? kFirstBorder : kFirstPlain));
-                    const int fout = kBufF0 + fsel;
-                    const int tout = kBufT0 + tsel;
-                    double* Fo = p.buf[fout];
-                    double* To = p.buf[tout];
-                    double mt = 0.0, mf = 0.0;
-                    // term = c * (A~ term); f += term   (expact.cpp:82-87)
-                    auto emit = [&](int64_t v, double sc, double fin) {
-                        const double tn = __dmul_rn(c, sc);
-                        const double fn = __dadd_rn(fin, tn);
-                        To[v] = tn;
-                        Fo[v] = fn;
-                        mt = nan_dropping_max(mt, fabs(tn));
-                        mf = nan_dropping_max(mf, fabs(fn));
-                    };
-                    if (kind == kFirstZero) {
-                        // A~ e_{n+1} = the border column b/gamma; f was e_{n+1}
-                        sweep_points(op, [&](int64_t v) { emit(v, __dadd_rn(0.0, G[v]), 0.0); });
-                    } else if (kind == kFirstBorder) {
-                        // the border entry (column n, b_i/gamma) is last in its row; term_n = 1 only
-                        // on a stage's first term (expact.cpp:137-138, :96)
-                        stencil(fcur, -1, kBufG, [&](int64_t v, double acc, double f, double, double bg) {
-                            emit(v, __dadd_rn(acc, bg), f);
-                        });
-                    } else if (kind == kFirstPlain) {
-                        stencil(fcur, -1, -1, [&](int64_t v, double acc, double f, double, double) { emit(v, acc, f); });
-                    } else {
-                        stencil(tprev, fcur, -1, [&](int64_t v, double acc, double, double f, double) { emit(v, acc, f); });
-                    }
-                    push_max2(mt, mf);
-                    sync_round(kTrTerm);
-                    ++used;
-                    fcur = fout;
-                    tprev = tout;
-                    fsel ^= 1;
-                    tsel ^= 1;
-                    const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
-                    const double cur = slot_read(sl + 0);
-                    double fnorm = slot_read(sl + 1);
-                    if (bordered) fnorm = nan_dropping_max(fnorm, 1.0);  // f_n == 1 (expact.cpp:89)
-                    if (!finite_or_fail(cur, fnorm)) return;
-                    if (__dadd_rn(prev, cur) <= __dmul_rn(p.tol, fnorm)) {  // expact.cpp:93
-                        prev = fnorm;  // next stage: term = f, ||term|| = ||f|| (expact.cpp:80, :96)
-                        break;
-                    }
-                    prev = (j == m_deg) ? fnorm : cur;
+                sync_round(kind == k2Next ? kTrFusedNext : kTrFusedFirst);
+                const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
+                double cur[2] = {slot_read(sl + 0), slot_read(sl + 2)};
+                double fn[2] = {slot_read(sl + 1), slot_read(sl + 3)};
+                if (bordered) {
+                    fn[0] = nan_dropping_max(fn[0], 1.0);  // f_n == 1 (expact.cpp:89)
+                    fn[1] = nan_dropping_max(fn[1], 1.0);
                 }
-                total_terms += used;
-                if (info && stage < kMaxLoggedStages) info->terms[stage] = used;
+                // term used+1 (result F1, explicit)
+                ++used;
+                if (!finite_or_fail(cur[0], fn[0])) return;
+                if (__dadd_rn(prev, cur[0]) <= __dmul_rn(p.tol, fn[0]) || used == m_deg) {
+                    prev = fn[0];
+                    fres = fout;
+                    tres = -1;
+                    break;
+                }
+                prev = cur[0];
+                // term used+1 (result F2 = F1 + T2, implicit)
+                ++used;
+                if (!finite_or_fail(cur[1], fn[1])) return;
+                if (__dadd_rn(prev, cur[1]) <= __dmul_rn(p.tol, fn[1]) || used == m_deg) {
+                    prev = fn[1];
+                    fres = fout;
+                    tres = tout;
+                    break;
+                }
+                prev = cur[1];
+                kind = k2Next;
+                xb = tout;
+                fb = fout;
+                fsel ^= 1;
+                tsel ^= 1;
             }
-                fres = fcur;
+            total_terms += used;
+            if (info && stage < kMaxLoggedStages) info->terms[stage] = used;
         }
-        if (info) info->total_terms = total_terms;
+    } else {
+        // Single-term sweeps (shapes the TMA path cannot describe)
+        int fcur = bordered ? -1 : kBufG;  // -1: f = e_{n+1} (all zero) for the bordered action
+        int tprev = -1;
+        int fsel = 0, tsel = 0;
+        for (int stage = 0; stage < s_st; ++stage) {
+            int used = 0;
+            for (int j = 1; j <= m_deg; ++j) {
+                const double c = __ddiv_rn(tau_s, static_cast<double>(j));  // expact.cpp:83
+                const TermKind kind = j > 1 ? kNext : (fcur < 0 ? kFirstZero : (bordered ? kFirstBorder : kFirstPlain));
+                const int fout = kBufF0 + fsel;
+                const int tout = kBufT0 + tsel;
+                double* Fo = p.buf[fout];
+                double* To = p.buf[tout];
+                double mt = 0.0, mf = 0.0;
+                // term = c * (A~ term); f += term   (expact.cpp:82-87)
+                auto emit = [&](int64_t v, double sc, double fin) {
+                    const double tn = __dmul_rn(c, sc);
+                    const double fnv = __dadd_rn(fin, tn);
+                    To[v] = tn;
+                    Fo[v] = fnv;
+                    mt = nan_dropping_max(mt, fabs(tn));
+                    mf = nan_dropping_max(mf, fabs(fnv));
+                };
+                if (kind == kFirstZero) {
+                    // A~ e_{n+1} = the border column b/gamma; f was e_{n+1}
+                    sweep_points(op, [&](int64_t v) { emit(v, __dadd_rn(0.0, G[v]), 0.0); });
+                } else if (kind == kFirstBorder) {
+                    // the border entry (column n, b_i/gamma) is last in its row; term_n = 1 only
+                    // on a stage's first term (expact.cpp:137-138, :96)
+                    stencil_sweep(p, sm, ring, seq, fcur, -1, kBufG, [&](int64_t v, double acc, double f, double, double bg) {
+                        emit(v, __dadd_rn(acc, bg), f);
+                    });
+                } else if (kind == kFirstPlain) {
+                    stencil_sweep(p, sm, ring, seq, fcur, -1, -1,
+                                  [&](int64_t v, double acc, double f, double, double) { emit(v, acc, f); });
+                } else {
+                    stencil_sweep(p, sm, ring, seq, tprev, fcur, -1,
+                                  [&](int64_t v, double acc, double, double f, double) { emit(v, acc, f); });
+                }
+                double v2[2] = {mt, mf};
+                block_reduce<2, true>(v2, sm);
+                if (threadIdx.x == 0) {
+                    unsigned long long* sl = p.slots + (round % 3) * 4;
+                    if (v2[0] > 0.0) atomicMax(sl + 0, static_cast<unsigned long long>(__double_as_longlong(v2[0])));
+                    if (v2[1] > 0.0) atomicMax(sl + 1, static_cast<unsigned long long>(__double_as_longlong(v2[1])));
+                }
+                sync_round(kTrTerm);
+                ++used;
+                fcur = fout;
+                tprev = tout;
+                fsel ^= 1;
+                tsel ^= 1;
+                const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
+                const double cur = slot_read(sl + 0);
+                double fnorm = slot_read(sl + 1);
+                if (bordered) fnorm = nan_dropping_max(fnorm, 1.0);  // f_n == 1 (expact.cpp:89)
+                if (!finite_or_fail(cur, fnorm)) return;
+                if (__dadd_rn(prev, cur) <= __dmul_rn(p.tol, fnorm)) {  // expact.cpp:93
+                    prev = fnorm;  // next stage: term = f, ||term|| = ||f|| (expact.cpp:80, :96)
+                    break;
+                }
+                prev = (j == m_deg) ? fnorm : cur;
+            }
+            total_terms += used;
+            if (info && stage < kMaxLoggedStages) info->terms[stage] = used;
+        }
+        fres = fcur;
+    }
+    if (info) info->total_terms = total_terms;
+    if (leader) {
+        ctrl->fres = fres;
+        ctrl->tres = tres;
+    }
+    if (p.use_tma) fence_proxy_async_global();
+}
 
-        // ------------------------------------------------ K5: output / update + metrics
-        const double* F = p.buf[fres];
-        const double* TI = tres >= 0 ? p.buf[tres] : nullptr;  // implicit F2 = F1 + T2
-        auto yv = [&](int64_t v) { return TI ? __dadd_rn(F[v], TI[v]) : F[v]; };
-        if (run) {
-            const double scl = __ddiv_rn(gamma, t);  // expact.cpp:150
-            double sum = 0.0, mx = -INFINITY, mn = INFINITY, r2 = 0.0;
-            sweep_points(op, [&](int64_t v) {
-                // out = u + tau * (scale * y)   (integrator.cpp:59-61, expact.cpp:151)
-                const double un = __dadd_rn(U[v], __dmul_rn(t, __dmul_rn(scl, yv(v))));
-                U[v] = un;
-                if (p.want_metrics) metrics_local(sum, mx, mn, r2, v, un);
-            });
-            if (p.want_metrics) metrics_push(sum, mx, mn, r2, (step + 1) & 1);
-            gsync(kTrUpdate);
-            if (p.want_metrics) metrics_finish(step + 1, (step + 1) & 1);
-        } else {
-            const double scale = bordered ? __ddiv_rn(gamma, t) : 1.0;
-            sweep_points(op, [&](int64_t v) { OUT[v] = bordered ? __dmul_rn(scale, yv(v)) : yv(v); });
-        }
+// ------------------------------------------------------------------------------------------
+// K5 update: u <- u + tau * (gamma/tau) * y (run, + compute_metrics) or out = scale * y
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSolveThreads) update_kernel(const __grid_constant__ SolveParams p, int step) {
+    __shared__ Smem sm;
+    const Ctrl* ctrl = p.ctrl;
+    if (__ldcg(&ctrl->status)) return;
+    const int branch = __ldcg(&ctrl->branch);
+    const int fres = __ldcg(&ctrl->fres), tres = __ldcg(&ctrl->tres);
+    const double t = p.tau;
+    const bool bordered = p.mode != kModeExpmv;
+    const double* G = p.buf[kBufG];
+    const double* F = fres >= 0 ? p.buf[fres] : G;
+    const double* TI = tres >= 0 ? p.buf[tres] : nullptr;  // implicit F2 = F1 + T2
+    const double* INC = p.buf[kBufT0];
+    double* const U = p.buf[kBufU];
+    double* const OUT = p.buf[kBufOut];
+    // phi1v's result before the step's u + tau * incr (expact.cpp:149-151 / :108-121)
+    const double scl = (branch == 0 && bordered) ? __ddiv_rn(__ldcg(&ctrl->gamma), t) : 1.0;
+    auto incr = [&](int64_t v) -> double {
+        if (branch == 1) return G[v];
+        if (branch == 2) return 0.0;
+        if (branch == 3) return INC[v];
+        const double y = TI ? __dadd_rn(F[v], TI[v]) : F[v];
+        return bordered ? __dmul_rn(scl, y) : y;
+    };
+    if (p.mode == kModeRun) {
+        MetricAcc a;
+        sweep_points(p.op, [&](int64_t v) {
+            const double un = __dadd_rn(U[v], __dmul_rn(t, incr(v)));  // integrator.cpp:59-61
+            U[v] = un;
+            if (p.want_metrics) a.add(p, v, un);
+        });
+        if (p.want_metrics) metrics_commit(p, sm, a, step + 1);
+        if (p.use_tma) fence_proxy_async_global();
+    } else {
+        sweep_points(p.op, [&](int64_t v) { OUT[v] = incr(v); });
     }
 }
 
