@@ -130,6 +130,12 @@ gs_status gs_seed_initial(gs_ctx* ctx, const double origin[3], double amplitude,
 gs_status gs_set_trace(gs_ctx* ctx, int capacity);
 /* Copy the last launch's records as (tag, ns) pairs; *count receives the number of records. */
 gs_status gs_get_trace(gs_ctx* ctx, uint64_t* pairs, int capacity, int* count);
+/* Per-kernel device time with CUDA events on the context's stream around every launch
+ * of the sequence (enable != 0).  gs_get_kernel_times returns, for the last gs_run /
+ * gs_step / gs_phi1v / gs_expmv call, total milliseconds and launch counts of:
+ * [0] prep (RHS), [1] border, [2] taylor (the Taylor-term kernel), [3] update. */
+gs_status gs_set_kernel_timing(gs_ctx* ctx, int enable);
+gs_status gs_get_kernel_times(gs_ctx* ctx, double ms[4], int launches[4]);
 
 #ifdef __cplusplus
 }

@@ -51,7 +51,7 @@ EXPORTS = [
     "gs_set_intensity", "gs_set_labels", "gs_set_diffusion", "gs_get_labels", "gs_get_diffusion",
     "gs_one_norm", "gs_apply", "gs_set_state", "gs_get_state", "gs_state_device_ptr",
     "gs_select_params", "gs_expmv", "gs_phi1v", "gs_step", "gs_step_host", "gs_run", "gs_seed_initial",
-    "gs_set_trace", "gs_get_trace",
+    "gs_set_trace", "gs_get_trace", "gs_set_kernel_timing", "gs_get_kernel_times",
 ]
 
 
@@ -97,6 +97,10 @@ def load(path: str | None = None):
         L.gs_set_trace.argtypes = [vp, C.c_int]
         L.gs_get_trace.argtypes = [vp, np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS"), C.c_int,
                                    C.POINTER(C.c_int)]
+    if hasattr(L, "gs_set_kernel_timing"):
+        L.gs_set_kernel_timing.argtypes = [vp, C.c_int]
+        L.gs_get_kernel_times.argtypes = [vp, np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS"),
+                                          np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")]
     for name in EXPORTS:
         if name not in ("gs_destroy", "gs_last_error", "gs_num_points", "gs_stream", "gs_state_device_ptr") \
                 and hasattr(L, name):

@@ -78,6 +78,10 @@ struct gs_ctx {
     CUtensorMap x2map[gs::kNumBufs];
     CUtensorMap lmap, l2map;
     int trace_cap = 0;
+    bool ktime = false;
+    double kms[4] = {0, 0, 0, 0};
+    int kcount[4] = {0, 0, 0, 0};
+    std::vector<cudaEvent_t> events;
     DevBuf trace;
     std::vector<uint64_t> trace_host;
     std::string err;
@@ -308,9 +312,29 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     }
     const size_t dyn = p.use_tma ? gs::kDynSmemBytes : 0;
     const dim3 blk(gs::kSolveThreads);
+    // optional per-kernel CUDA-event timing: record (kind, start, end) around each launch
+    std::vector<std::pair<int, int>> marks;  // (kind, event index of start)
+    auto ev = [&](int k) -> cudaError_t {
+        if (!c->ktime) return cudaSuccess;
+        const size_t need = 2 * (marks.size() + 1);
+        while (c->events.size() < need) {
+            cudaEvent_t e;
+            cudaError_t r = cudaEventCreate(&e);
+            if (r != cudaSuccess) return r;
+            c->events.push_back(e);
+        }
+        marks.push_back({k, static_cast<int>(2 * marks.size())});
+        return cudaEventRecord(c->events[marks.back().second], c->stream);
+    };
+    auto ev_end = [&]() -> cudaError_t {
+        if (!c->ktime) return cudaSuccess;
+        return cudaEventRecord(c->events[marks.back().second + 1], c->stream);
+    };
     if (p.mode == gs::kModeApply) {
+        GS_CUDA(c, ev(0));
         gs::prep_kernel<<<gb, blk, dyn, c->stream>>>(p, 0);
         GS_CUDA(c, cudaGetLastError());
+        GS_CUDA(c, ev_end());
     } else {
         const int steps = p.mode == gs::kModeRun ? n_steps : 1;
         if (p.mode == gs::kModeRun && metrics) {
@@ -318,16 +342,24 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             GS_CUDA(c, cudaGetLastError());
         }
         for (int step = 0; step < steps; ++step) {
+            GS_CUDA(c, ev(0));
             gs::prep_kernel<<<gb, blk, dyn, c->stream>>>(p, step);
             GS_CUDA(c, cudaGetLastError());
+            GS_CUDA(c, ev_end());
+            GS_CUDA(c, ev(1));
             gs::border_kernel<<<sb, blk, 0, c->stream>>>(p, gb, step);
             GS_CUDA(c, cudaGetLastError());
+            GS_CUDA(c, ev_end());
             int border_blocks = sb;
             void* args[] = {&p, &border_blocks, &step};
+            GS_CUDA(c, ev(2));
             GS_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gs::taylor_kernel), dim3(gb), blk, args, dyn,
                                                    c->stream));
+            GS_CUDA(c, ev_end());
+            GS_CUDA(c, ev(3));
             gs::update_kernel<<<sb, blk, 0, c->stream>>>(p, step);
             GS_CUDA(c, cudaGetLastError());
+            GS_CUDA(c, ev_end());
         }
     }
     gs::Ctrl ctrl{};
@@ -344,6 +376,18 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
                                    cudaMemcpyDeviceToHost, c->stream));
     }
     GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (c->ktime) {
+        for (int k = 0; k < 4; ++k) {
+            c->kms[k] = 0.0;
+            c->kcount[k] = 0;
+        }
+        for (const auto& m : marks) {
+            float ms = 0.f;
+            GS_CUDA(c, cudaEventElapsedTime(&ms, c->events[m.second], c->events[m.second + 1]));
+            c->kms[m.first] += ms;
+            c->kcount[m.first] += 1;
+        }
+    }
     if (ctrl.status != GS_OK) {
         if (ctrl.detail == 2) return fail(c, GS_ENUMERIC, "expmv: series diverged to non-finite values; reduce t");
         if (ctrl.status == GS_EINVAL)
@@ -435,6 +479,7 @@ void gs_destroy(gs_ctx* c) {
                       &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->ctrl, &c->metrics, &c->infos,
                       &c->normbits, &c->trace})
         b->release();
+    for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -731,6 +776,21 @@ gs_status gs_seed_initial(gs_ctx* c, const double origin[3], double amplitude, d
                 u[v] = amplitude * std::exp(-width * sq);
                 if (mask && d[static_cast<size_t>(v)] == 0.0) u[v] = 0.0;
             }
+    return GS_OK;
+}
+
+gs_status gs_set_kernel_timing(gs_ctx* c, int enable) {
+    if (!c) return fail(c, GS_EINVAL, "gs_set_kernel_timing: null context");
+    c->ktime = enable != 0;
+    return GS_OK;
+}
+
+gs_status gs_get_kernel_times(gs_ctx* c, double ms[4], int launches[4]) {
+    if (!c || !ms || !launches) return fail(c, GS_EINVAL, "gs_get_kernel_times: null argument");
+    for (int k = 0; k < 4; ++k) {
+        ms[k] = c->kms[k];
+        launches[k] = c->kcount[k];
+    }
     return GS_OK;
 }
 

@@ -101,7 +101,8 @@ struct SolveParams {
 
 // phase tags of the optional trace (leader's view, recorded after each grid barrier)
 enum TraceTag : int { kTrMetrics0 = 1, kTrRhs = 2, kTrBorder = 3, kTrFusedFirst = 4, kTrFusedNext = 5, kTrFixup = 6,
-                      kTrUpdate = 7, kTrTerm = 8, kTrBranch = 9, kTrStart = 15 };
+                      kTrUpdate = 7, kTrTerm = 8, kTrBranch = 9, kTrBorderIn = 10, kTrTaylorIn = 11,
+                      kTrUpdateIn = 12, kTrPrepIn = 13, kTrStart = 15 };
 
 // K1: resample + classify (imaging.cpp:65-72, 118-141)
 __global__ void material_kernel(const uint8_t* stack, int w, int hgt, int slices, int nx, int ny, int nz,

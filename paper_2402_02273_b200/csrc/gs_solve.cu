@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) prep_kernel(const __grid_con
     extern __shared__ __align__(128) unsigned char dyn[];
     if (p.ctrl->status) return;
     block_setup(p, sm, p.use_tma);
-    if (step == 0) trace_mark(p, kTrStart);
+    trace_mark(p, kTrPrepIn);
     Ring ring{dyn, sm.bar1};
     uint32_t seq = 0;
     double* const G = p.buf[kBufG];
@@ -746,6 +746,7 @@ __global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_cons
     __shared__ Smem sm;
     Ctrl* ctrl = p.ctrl;
     if (ctrl->status) return;
+    trace_mark(p, kTrBorderIn);
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     gs_step_info* info = (p.infos && leader) ? p.infos + step : nullptr;
     const double t = p.tau;
@@ -835,6 +836,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
     extern __shared__ __align__(128) unsigned char dyn[];
     Ctrl* ctrl = p.ctrl;
     if (ctrl->status) return;
+    trace_mark(p, kTrTaylorIn);
     const StencilOp& op = p.op;
     block_setup(p, sm, p.use_tma);
     Ring ring{dyn, sm.bar1};
@@ -933,7 +935,27 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                 const double* Tb = p.buf[tres];
                 const int fo = (fres == kBufF0) ? kBufF1 : kBufF0;
                 double* Fw = p.buf[fo];
-                sweep_points(op, [&](int64_t v) { Fw[v] = __dadd_rn(Fa[v], Tb[v]); });
+                {
+                    // vectorised: two double2 loads per input in flight per thread
+                    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+                    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+                    const int64_t n2 = op.n >> 1;
+                    const double2* A2 = reinterpret_cast<const double2*>(Fa);
+                    const double2* B2 = reinterpret_cast<const double2*>(Tb);
+                    double2* W2 = reinterpret_cast<double2*>(Fw);
+                    for (int64_t i = tid; i < n2; i += 2 * stride) {
+                        const bool second = i + stride < n2;
+                        const double2 a0 = A2[i], b0 = B2[i];
+                        double2 a1 = make_double2(0.0, 0.0), b1 = a1;
+                        if (second) {
+                            a1 = A2[i + stride];
+                            b1 = B2[i + stride];
+                        }
+                        W2[i] = make_double2(__dadd_rn(a0.x, b0.x), __dadd_rn(a0.y, b0.y));
+                        if (second) W2[i + stride] = make_double2(__dadd_rn(a1.x, b1.x), __dadd_rn(a1.y, b1.y));
+                    }
+                    if ((op.n & 1) && tid == 0) Fw[op.n - 1] = __dadd_rn(Fa[op.n - 1], Tb[op.n - 1]);
+                }
                 gsync(kTrFixup);
                 fstart = fo;
             } else {
@@ -1090,6 +1112,7 @@ __global__ void __launch_bounds__(kSolveThreads) update_kernel(const __grid_cons
     __shared__ Smem sm;
     const Ctrl* ctrl = p.ctrl;
     if (__ldcg(&ctrl->status)) return;
+    trace_mark(p, kTrUpdateIn);
     const int branch = __ldcg(&ctrl->branch);
     const int fres = __ldcg(&ctrl->fres), tres = __ldcg(&ctrl->tres);
     const double t = p.tau;

@@ -300,6 +300,17 @@ class StencilOperator:
         self._check(self.lib.gs_get_trace(self.ctx, buf, cap, C.byref(n)))
         return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(n.value)]
 
+    def set_kernel_timing(self, enable: bool):
+        """CUDA-event timing of every kernel launch of later calls (on the context's stream)."""
+        self._check(self.lib.gs_set_kernel_timing(self.ctx, 1 if enable else 0))
+
+    def kernel_times(self):
+        """{kernel: (total ms, launches)} of the last call: prep, border, taylor, update."""
+        ms = np.zeros(4, dtype=np.float64)
+        n = np.zeros(4, dtype=np.int32)
+        self._check(self.lib.gs_get_kernel_times(self.ctx, ms, n))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(["prep", "border", "taylor", "update"])}
+
     def step_resident(self, rho, tau, tol, info=True):
         inf = N.GsStepInfo() if info else None
         self._check(self.lib.gs_step(self.ctx, rho, tau, tol, C.byref(inf) if inf is not None else None))

@@ -14,8 +14,9 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import bench  # noqa: E402
 from paper_2402_02273_b200 import workloads as W  # noqa: E402
 
+# a record's tag names the phase that ENDS at its timestamp
 NAMES = {1: "metrics0", 2: "rhs", 3: "border", 4: "fused-first", 5: "fused-next", 6: "fixup", 7: "update",
-         8: "term", 9: "branch", 15: "start"}
+         8: "term", 9: "branch", 10: "prep(rhs)", 11: "border", 12: "taylor-tail", 13: "update/launch", 15: "start"}
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--steps", type=int, default=1)
