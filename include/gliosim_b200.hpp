@@ -1,0 +1,240 @@
+// gliosim_b200.hpp -- C++ drop-in layer over the C-ABI (include/gliosim_b200.h).
+//
+// The reference gliosim library is C++ (/root/reference/proj/include/gliosim/*.hpp); this
+// header gives its callers the same free functions with the same argument meaning, value
+// semantics and exception types, backed by the B200 kernels:
+//
+//   reference                                             here (namespace gliosim_b200)
+//   SparseOperator assemble_diffusion(const DiffusionField&)   StencilOperator assemble_diffusion(d)
+//     (stencil.hpp:20)                                          (any type with .grid.{nx,ny,nz,h} and .d)
+//   std::vector<double> expmv(t, A, b, tol, workers)           expmv(t, A, b, tol)      (expact.hpp:45-46)
+//   std::vector<double> phi1v(t, A, b, tol, workers)           phi1v(t, A, b, tol)      (expact.hpp:49-50)
+//   ActionParams select_params(norm, tol)                      select_params(norm, tol) (expact.hpp:42)
+//   std::vector<double> step(A, u, rho, tau, tol, workers)     step(A, u, rho, tau, tol) (integrator.hpp:59-60)
+//   RunResult run(cfg, d, u0, workers, sink, warn, watch)      run(cfg, d, u0, sink, warn, watch)
+//                                                               (integrator.hpp:75-77)
+//   std::invalid_argument / numeric_error / data_error         same std::invalid_argument /
+//                                                               gliosim_b200::numeric_error / data_error
+//
+// The reference's own types (SimConfig, DiffusionField, Grid) are accepted as template
+// parameters, so a reference caller switches by changing the namespace and linking
+// libgliosim_b200.so -- no reference header is needed to compile this file.
+// `workers` arguments are accepted and ignored (the reference documents that results do
+// not depend on them, sparse.hpp:27-29).
+#pragma once
+
+#include <chrono>
+#include <cstdint>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "gliosim_b200.h"
+
+namespace gliosim_b200 {
+
+struct data_error : std::runtime_error {
+    explicit data_error(const std::string& m) : std::runtime_error(m) {}
+};
+struct numeric_error : std::runtime_error {
+    explicit numeric_error(const std::string& m) : std::runtime_error(m) {}
+};
+struct device_error : std::runtime_error {
+    explicit device_error(const std::string& m) : std::runtime_error(m) {}
+};
+
+inline void check(gs_status st, const gs_ctx* ctx) {
+    if (st == GS_OK) return;
+    const std::string msg = gs_last_error(ctx);
+    switch (st) {
+        case GS_EINVAL: throw std::invalid_argument(msg);
+        case GS_ENUMERIC: throw numeric_error(msg);
+        case GS_EDATA: throw data_error(msg);
+        default: throw device_error(msg);
+    }
+}
+
+struct ActionParams {  // expact.hpp:33-37
+    int s = 1;
+    int m = 1;
+    double tol = 1e-8;
+};
+
+struct StepMetrics {  // integrator.hpp:30-37
+    int step = 0;
+    double time = 0.0, total_mass = 0.0, max_density = 0.0, min_density = 0.0, radius = 0.0;
+};
+
+struct RunTimings {  // integrator.hpp:39-43
+    double assemble_seconds = 0.0, step_seconds = 0.0, io_seconds = 0.0;
+};
+
+struct RunResult {  // integrator.hpp:45-49
+    std::vector<StepMetrics> metrics;
+    std::vector<double> u;
+    RunTimings timings;
+};
+
+using SnapshotSink = std::function<void(int, double, const std::vector<double>&)>;
+using RangeWarning = std::function<void(int, double, double)>;
+using StepWatcher = std::function<void(const StepMetrics&)>;
+
+// The device-resident, matrix-free form of the reference's SparseOperator for the
+// diffusion stencil.  Move-only (it owns the device buffers of one grid).
+class StencilOperator {
+public:
+    StencilOperator(int nx, int ny, int nz, double h, int device = 0) : nx_(nx), ny_(ny), nz_(nz), h_(h) {
+        check(gs_create(&ctx_, nx, ny, nz, h, device), nullptr);
+    }
+    StencilOperator(StencilOperator&& o) noexcept { *this = std::move(o); }
+    StencilOperator& operator=(StencilOperator&& o) noexcept {
+        std::swap(ctx_, o.ctx_);
+        nx_ = o.nx_;
+        ny_ = o.ny_;
+        nz_ = o.nz_;
+        h_ = o.h_;
+        return *this;
+    }
+    StencilOperator(const StencilOperator&) = delete;
+    StencilOperator& operator=(const StencilOperator&) = delete;
+    ~StencilOperator() {
+        if (ctx_) gs_destroy(ctx_);
+    }
+
+    int64_t dim() const { return static_cast<int64_t>(nx_) * ny_ * nz_; }   // sparse.hpp:20
+    double one_norm() const {                                                  // sparse.hpp:22
+        double v = 0.0;
+        check(gs_one_norm(ctx_, &v), ctx_);
+        return v;
+    }
+    void apply(const std::vector<double>& x, std::vector<double>& y, int = 1) const {  // sparse.hpp:29
+        if (static_cast<int64_t>(x.size()) != dim())
+            throw std::invalid_argument("SparseOperator::apply: vector length " + std::to_string(x.size()) +
+                                        " != dim " + std::to_string(dim()));
+        y.resize(x.size());
+        check(gs_apply(ctx_, x.data(), y.data()), ctx_);
+    }
+    std::vector<double> apply(const std::vector<double>& x, int workers = 1) const {
+        std::vector<double> y;
+        apply(x, y, workers);
+        return y;
+    }
+    void set_diffusion(const std::vector<double>& d) { check(gs_set_diffusion(ctx_, d.data()), ctx_); }
+    void set_labels(const std::vector<uint8_t>& l, double dw, double dg) {
+        check(gs_set_labels(ctx_, l.data(), dw, dg), ctx_);
+    }
+    gs_ctx* ctx() const { return ctx_; }
+    int nx() const { return nx_; }
+    int ny() const { return ny_; }
+    int nz() const { return nz_; }
+    double h() const { return h_; }
+
+private:
+    gs_ctx* ctx_ = nullptr;
+    int nx_ = 0, ny_ = 0, nz_ = 0;
+    double h_ = 1.0;
+};
+
+// assemble_diffusion (stencil.cpp:5-43) for any DiffusionField-like type.
+template <class DiffusionFieldT>
+StencilOperator assemble_diffusion(const DiffusionFieldT& d, int device = 0) {
+    StencilOperator op(d.grid.nx, d.grid.ny, d.grid.nz, d.grid.h, device);
+    op.set_diffusion(d.d);
+    return op;
+}
+
+inline ActionParams select_params(double norm_tA, double tol) {
+    ActionParams p;
+    p.tol = tol;
+    check(gs_select_params(norm_tA, tol, &p.s, &p.m), nullptr);
+    return p;
+}
+
+inline std::vector<double> expmv(double t, const StencilOperator& a, const std::vector<double>& b, double tol,
+                                 int = 1) {
+    if (static_cast<int64_t>(b.size()) != a.dim())
+        throw std::invalid_argument("expmv: vector length does not match operator dimension");
+    std::vector<double> out(b.size());
+    check(gs_expmv(a.ctx(), t, b.data(), tol, out.data(), nullptr), a.ctx());
+    return out;
+}
+
+inline std::vector<double> phi1v(double t, const StencilOperator& a, const std::vector<double>& b, double tol,
+                                 int = 1) {
+    if (static_cast<int64_t>(b.size()) != a.dim())
+        throw std::invalid_argument("phi1v: vector length does not match operator dimension");
+    std::vector<double> out(b.size());
+    check(gs_phi1v(a.ctx(), t, b.data(), tol, out.data(), nullptr), a.ctx());
+    return out;
+}
+
+// step (integrator.cpp:52-63).  Overwrites the operator's resident state.
+inline std::vector<double> step(const StencilOperator& a, const std::vector<double>& u, double rho, double tau,
+                                double tol, int = 1) {
+    if (static_cast<int64_t>(u.size()) != a.dim())
+        throw std::invalid_argument("phi1v: vector length does not match operator dimension");
+    std::vector<double> out(u.size());
+    check(gs_step_host(a.ctx(), u.data(), rho, tau, tol, out.data(), nullptr), a.ctx());
+    return out;
+}
+
+// run (integrator.cpp:91-138) for SimConfig- and DiffusionField-like types: the time loop on
+// the GPU (one launch sequence per snapshot segment), metrics computed on the device at every
+// node, hooks fired in the reference's order.
+template <class SimConfigT, class DiffusionFieldT>
+RunResult run(const SimConfigT& cfg, const DiffusionFieldT& d, std::vector<double> u0, int = 1,
+              const SnapshotSink& snapshot = {}, const RangeWarning& on_range = {}, const StepWatcher& on_step = {}) {
+    cfg.validate();
+    const int64_t n = static_cast<int64_t>(d.grid.nx) * d.grid.ny * d.grid.nz;
+    if (static_cast<int64_t>(u0.size()) != n)
+        throw std::invalid_argument("run: initial state length does not match the grid");
+    if (static_cast<int64_t>(d.d.size()) != n)
+        throw std::invalid_argument("run: diffusion field length does not match the grid");
+    RunResult res;
+    StencilOperator a = gliosim_b200::assemble_diffusion(d);
+    check(gs_set_state(a.ctx(), u0.data()), a.ctx());
+    const double tau = (cfg.t_end - cfg.t0) / cfg.num_steps;
+    auto time_at = [&](int k) { return k >= cfg.num_steps ? cfg.t_end : cfg.t0 + k * tau; };
+    const double origin[3] = {cfg.origin[0], cfg.origin[1], cfg.origin[2]};
+    const double center[3] = {cfg.seed_center[0], cfg.seed_center[1], cfg.seed_center[2]};
+    if (snapshot) snapshot(0, time_at(0), u0);
+    int done = 0;
+    std::vector<gs_metrics> m;
+    while (done < cfg.num_steps) {
+        int cut = cfg.num_steps;
+        if (snapshot)
+            for (int k = done + 1; k <= cfg.num_steps; ++k)
+                if (k % cfg.snapshot_every == 0 || k == cfg.num_steps) {
+                    cut = k;
+                    break;
+                }
+        const int k = cut - done;
+        m.assign(static_cast<size_t>(k) + 1, gs_metrics{});
+        const auto tic = std::chrono::steady_clock::now();
+        check(gs_run(a.ctx(), k, cfg.rho, tau, cfg.exp_tol, origin, center, cfg.front_threshold, m.data(), nullptr),
+              a.ctx());
+        res.timings.step_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - tic).count();
+        for (int q = done == 0 ? 0 : 1; q <= k; ++q) {
+            StepMetrics sm{done + q, time_at(done + q), m[q].total_mass, m[q].max_density, m[q].min_density,
+                           m[q].radius};
+            res.metrics.push_back(sm);
+            if (done + q == 0) continue;
+            if (on_step) on_step(sm);  // integrator.cpp:128-131
+            if (on_range && (sm.min_density < -0.01 || sm.max_density > 1.01))
+                on_range(sm.step, sm.min_density, sm.max_density);
+        }
+        done = cut;
+        if (snapshot) {
+            std::vector<double> u(static_cast<size_t>(n));
+            check(gs_get_state(a.ctx(), u.data()), a.ctx());
+            snapshot(cut, time_at(cut), u);
+        }
+    }
+    res.u.resize(static_cast<size_t>(n));
+    check(gs_get_state(a.ctx(), res.u.data()), a.ctx());
+    return res;
+}
+
+}  // namespace gliosim_b200

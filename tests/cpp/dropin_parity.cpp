@@ -1,0 +1,101 @@
+// dropin_parity.cpp -- TEST: the C++ drop-in (include/gliosim_b200.hpp) against the UNMODIFIED
+// reference library, called the way a reference user calls it.  Built in the build container
+// (needs /root/reference headers) by oracle/Makefile target `dropin`; the binary travels to the
+// GPU box and is run by tests/test_gpu_parity.py::test_cpp_dropin_parity.
+//
+// Same SimConfig / DiffusionField / u0 objects go to gliosim::run (reference, CPU) and to
+// gliosim_b200::run (GPU); the final state must agree to a relative L2 of 1e-8 and the
+// order-free metrics (max, min, radius) to 1e-12; step() / phi1v() / expmv() / apply() too.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "gliosim/config.hpp"
+#include "gliosim/expact.hpp"
+#include "gliosim/fields.hpp"
+#include "gliosim/integrator.hpp"
+#include "gliosim/stencil.hpp"
+#include "gliosim_b200.hpp"
+
+static double rel_l2(const std::vector<double>& a, const std::vector<double>& b) {
+    double num = 0.0, den = 0.0;
+    for (size_t i = 0; i < a.size(); ++i) {
+        num += (a[i] - b[i]) * (a[i] - b[i]);
+        den += b[i] * b[i];
+    }
+    return std::sqrt(num / (den > 0 ? den : 1.0));
+}
+
+int main() {
+    gliosim::SimConfig cfg;
+    cfg.nx = 24;
+    cfg.ny = 20;
+    cfg.nz = 16;
+    cfg.h = 200.0 / 23.0;
+    cfg.num_steps = 12;
+    cfg.t_end = cfg.t0 + 12 * 33.5;
+    cfg.snapshot_every = 5;
+    cfg.seed_center = {100.0, 80.0, 70.0};
+    cfg.seed_amplitude = 1.0;
+    cfg.seed_width = 0.01;
+    gliosim::DiffusionField d(cfg.grid());
+    for (int k = 0; k < cfg.nz; ++k)
+        for (int j = 0; j < cfg.ny; ++j)
+            for (int i = 0; i < cfg.nx; ++i) {
+                const double r = std::hypot(i - 12.0, j - 10.0);
+                d.d[static_cast<size_t>(i + cfg.nx * (j + cfg.ny * k))] =
+                    r < 6 ? cfg.d_white : (r < 9 ? cfg.d_gray : 0.0);
+            }
+    const std::vector<double> u0 = gliosim::seed_initial(d, cfg);
+    int fails = 0;
+    auto gate = [&](bool ok, const char* what, double v) {
+        std::printf("[%s] %s %.3e\n", ok ? "PASS" : "FAIL", what, v);
+        fails += !ok;
+    };
+
+    // run (integrator.hpp:75-77) with hooks
+    std::vector<int> snaps_ref, snaps_gpu, steps_gpu;
+    const gliosim::RunResult ref =
+        gliosim::run(cfg, d, u0, 1, [&](int n, double, const std::vector<double>&) { snaps_ref.push_back(n); });
+    const gliosim_b200::RunResult gpu = gliosim_b200::run(
+        cfg, d, u0, 1, [&](int n, double, const std::vector<double>&) { snaps_gpu.push_back(n); }, {},
+        [&](const gliosim_b200::StepMetrics& m) { steps_gpu.push_back(m.step); });
+    gate(rel_l2(gpu.u, ref.u) <= 1e-8, "run: final u rel L2", rel_l2(gpu.u, ref.u));
+    gate(snaps_ref == snaps_gpu, "run: snapshot cadence", 0.0);
+    gate(static_cast<int>(steps_gpu.size()) == cfg.num_steps, "run: step watcher calls", 0.0);
+    double worst = 0.0;
+    for (size_t q = 0; q < ref.metrics.size(); ++q) {
+        worst = std::fmax(worst, std::fabs(gpu.metrics[q].max_density - ref.metrics[q].max_density));
+        worst = std::fmax(worst, std::fabs(gpu.metrics[q].radius - ref.metrics[q].radius) / 200.0);
+        worst = std::fmax(worst, std::fabs(gpu.metrics[q].total_mass / ref.metrics[q].total_mass - 1.0));
+    }
+    gate(worst <= 1e-12 && gpu.metrics.size() == ref.metrics.size(), "run: metrics", worst);
+
+    // step / phi1v / expmv / apply / one_norm
+    const gliosim::SparseOperator a = gliosim::assemble_diffusion(d);
+    gliosim_b200::StencilOperator ga = gliosim_b200::assemble_diffusion(d);
+    gate(ga.one_norm() == a.one_norm(), "one_norm bitwise", ga.one_norm());
+    gate(ga.apply(u0) == a.apply(u0), "apply bitwise", 0.0);
+    const auto s_ref = gliosim::step(a, u0, cfg.rho, cfg.tau(), cfg.exp_tol);
+    const auto s_gpu = gliosim_b200::step(ga, u0, cfg.rho, cfg.tau(), cfg.exp_tol);
+    gate(rel_l2(s_gpu, s_ref) <= 1e-10, "step rel L2", rel_l2(s_gpu, s_ref));
+    const auto p_ref = gliosim::phi1v(40.0, a, u0, 1e-10);
+    const auto p_gpu = gliosim_b200::phi1v(40.0, ga, u0, 1e-10);
+    gate(rel_l2(p_gpu, p_ref) <= 1e-12, "phi1v rel L2", rel_l2(p_gpu, p_ref));
+    const auto e_ref = gliosim::expmv(40.0, a, u0, 1e-10);
+    const auto e_gpu = gliosim_b200::expmv(40.0, ga, u0, 1e-10);
+    gate(e_gpu == e_ref, "expmv bitwise", rel_l2(e_gpu, e_ref));
+    const auto sp = gliosim_b200::select_params(21.0725, 1e-8);
+    const auto sr = gliosim::select_params(21.0725, 1e-8);
+    gate(sp.s == sr.s && sp.m == sr.m, "select_params", sp.m);
+    // error behaviour: same exception types
+    bool threw = false;
+    try {
+        gliosim_b200::phi1v(1.0, ga, std::vector<double>(3, 1.0), 1e-10);
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    gate(threw, "phi1v length mismatch -> std::invalid_argument", 0.0);
+    std::printf("%s\n", fails ? "dropin parity: FAILED" : "dropin parity: all passed");
+    return fails ? 1 : 0;
+}

@@ -309,3 +309,17 @@ def test_sweep_paths_vs_oracle(G, port, shape, tma, monkeypatch):
         got_e = G.expmv(20.0, op, x, 1e-10)
         want_e, _ = port.expmv(20.0, op_o, x, 1e-10)
         assert np.array_equal(got_e, want_e)
+
+
+# ---- the C++ drop-in against the reference, called like a reference user calls it --------
+
+def test_cpp_dropin_parity():
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "dropin_parity")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_parity not built (needs the reference headers at build time)")
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(res.stdout)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "all passed" in res.stdout

@@ -97,3 +97,13 @@ def test_workloads_describe_baseline_configs():
     c4 = W.get("C4")
     assert (c4.nx, c4.ny, c4.nz, c4.steps) == (256, 256, 256, 100)
     assert c4.tau == 33.5
+
+
+def test_cpp_header_compiles_standalone(tmp_path):
+    """include/gliosim_b200.hpp needs nothing but the C-ABI header (no reference headers)."""
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "gliosim_b200.hpp"\n'
+                   'struct G { int nx = 4, ny = 4, nz = 4; double h = 1.0; };\n'
+                   'struct D { G grid; std::vector<double> d = std::vector<double>(64, 0.1); };\n'
+                   'int main() { D d; (void)&gliosim_b200::assemble_diffusion<D>; return 0; }\n')
+    subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), str(src)], check=True)
