@@ -169,7 +169,7 @@ def slab_of(w, labels, u0, depth):
     return labels[sl].copy(), u0[sl].copy()
 
 
-def cpu_reference_sample(w, labels, u0, target_s, steps=None, warmup=0, gpu_terms_of=None):
+def cpu_reference_sample(w, labels, u0, target_s, steps=None, warmup=0, gpu_terms_of=None, rho=None):
     """Time the reference's own run() loop (RunTimings::step_seconds, integrator.cpp:123-125)
     on a slab with workers = all host cores; the C port stands in only if oracle/_ref is
     absent.  `steps` fixed -> exactly that many timed steps after `warmup` untimed ones;
@@ -192,16 +192,17 @@ def cpu_reference_sample(w, labels, u0, target_s, steps=None, warmup=0, gpu_term
     center = (0.0, 0.0, 0.0)
     port = Port()
     op_p = port.stencil(shape, w.h, d_s)
+    rho = w.rho if rho is None else rho
 
     def timed(u, k):
         if k <= 0:
             return u, 0.0
         if ref:
-            u2, _, secs = ref.run(shape, w.h, d_s, u, k, w.rho, W.T0, W.T0 + k * W.TAU, W.TOL, center,
+            u2, _, secs = ref.run(shape, w.h, d_s, u, k, rho, W.T0, W.T0 + k * W.TAU, W.TOL, center,
                                   workers=cores)
             return u2, secs
         t0 = time.perf_counter()
-        u2, _, _ = port.run(op_p, u, k, w.rho, W.TAU, W.TOL, center)
+        u2, _, _ = port.run(op_p, u, k, rho, W.TAU, W.TOL, center)
         return u2, time.perf_counter() - t0
 
     u, _ = timed(u_s, warmup)
@@ -388,39 +389,141 @@ def run_ours(args, w, rank, world, local):
         dist.destroy_process_group()
 
 
+def run_ensemble(args, w, rank, world, local):
+    """C5: every bench step advances all 64 members by one exponential-Euler step; members are
+    partitioned over ranks (replicas, no data-path collective); value = member-steps/s."""
+    import torch
+    from paper_2402_02273_b200 import ensemble as E
+    from paper_2402_02273_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as D
+        D.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = D
+    members = E.members_for_rank(w.members, rank, world)
+    runner = E.EnsembleRunner(w, members, device=local)
+    runner.reset()
+    runner.run(args.warmup)
+    runner.reset()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        t0.record()
+        results = runner.run(args.steps)  # synchronous per member (gs_run returns after its stream sync)
+        t1.record()
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    table, terms = E.gather_results(results, w.members, args.steps, dist)
+    value = w.members * args.steps / (ms / 1e3)
+
+    # e2e: the drop-in step() with host buffers for every member of this rank, one ensemble step
+    e2e = None
+    if not args.no_e2e:
+        import ctypes as C
+        from paper_2402_02273_b200 import _native as N
+        pin_in = torch.empty(w.n, dtype=torch.float64, pin_memory=True)
+        pin_out = torch.empty(w.n, dtype=torch.float64, pin_memory=True)
+        info = N.GsStepInfo()
+        if dist:
+            dist.barrier()
+        tic = time.perf_counter()
+        for op, u, rho in zip(runner.ops, runner.u0, runner.rhos):
+            pin_in.numpy()[:] = u
+            rc = op.lib.gs_step_host(op.ctx, pin_in.numpy(), rho, w.tau, W.TOL, pin_out.numpy(), C.byref(info))
+            assert rc == 0
+        dt = time.perf_counter() - tic
+        if dist:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": w.members / dt, "unit": "member-steps/s", "h2d_bytes_per_step": 8 * w.n * w.members,
+               "d2h_bytes_per_step": 8 * w.n * w.members,
+               "api": "gs_step_host per member (drop-in step(): u H2D from pinned, u' D2H)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sample = cpu_reference_sample(w, runner.ops[0].labels(), runner.u0[0], args.cpu_seconds,
+                                          rho=runner.rhos[0])
+            cpu = {"value": 1.0 / float(np.mean(sample["step_times"])), "unit": "member-steps/s",
+                   "cores": sample["cores"], "kind": sample["kind"],
+                   "sample": (f"{sample['steps']} gliosim::run steps (workers={sample['cores']}) of member 0 "
+                              f"(128^3, rho={runner.rhos[0]:.4f}); one member-step each")}
+        except Exception as e:
+            cpu = {"value": None, "unit": "member-steps/s", "cores": os.cpu_count(), "kind": "unavailable",
+                   "sample": f"failed: {e}"}
+    line = {
+        "metric": "ensemble member-steps/s (64 x 128^3 fp64)", "value": value, "unit": "member-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded shell phantoms, one per member)",
+        "config": {"workload": f"{w.name}: {w.note}", "members": w.members, "grid": [w.nx, w.ny, w.nz],
+                   "members_per_rank": len(members), "parallelism": f"members partitioned over {world} rank(s)",
+                   "terms_per_member_step": float(terms.mean()),
+                   "rho_range": [float(min(runner.rhos)), float(max(runner.rhos))] if world == 1 else None,
+                   "l2": "64 resident members x 7 x 16 MiB >> L2"},
+        "gpu_launches": 4 * len(members) * args.steps + len(members),
+        "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
+        "metrics_all_finite": bool(np.isfinite(table).all()),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    runner.close()
+    if dist:
+        dist.destroy_process_group()
+
+
 def run_reference(args, w, rank, world, local):
+    """The UNMODIFIED reference (oracle/_ref: gliosim compiled from /root/reference/proj/src)
+    on the host cores; rank 0 only (other ranks exit)."""
     if rank != 0:
         return
     from paper_2402_02273_b200 import workloads as W
-    data, dims, labels = build_case(w)
-    if labels is None:
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        from oracle import Port
-        labels = Port().resample(data, dims[0], dims[1], dims[2], (w.nx, w.ny, w.nz))
-    # u0 with the reference's own seed_initial (libm), max over seeds
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import Port
     port = Port()
+    member = 0
+    data, dims, labels = build_case(w)
+    if labels is None:
+        labels = port.resample(data, dims[0], dims[1], dims[2], (w.nx, w.ny, w.nz))
     d = np.array([0.0, W.D_WHITE, W.D_GRAY, 0.0])[labels]
+    # u0 with the reference's own seed_initial (libm), max over seeds
     u0 = None
-    for c in W.seed_points(w, labels):
+    for c in W.seed_points(w, labels, member):
         ui = port.seed_initial((w.nx, w.ny, w.nz), w.h, 1.0, W.seed_width(w), c, d)
         u0 = ui if u0 is None else np.maximum(u0, ui)
-    # Taylor-term counts of the full grid for the extrapolation come from the oracle's log
-    # of the first slab step ratio; without a GPU we scale by voxels only.
-    sample = cpu_reference_sample(w, labels, u0, args.cpu_seconds, steps=args.steps, warmup=args.warmup)
-    v, full_s = extrapolate(sample, w.n)
+    rho = W.member_rho(w, member)
+    sample = cpu_reference_sample(w, labels, u0, args.cpu_seconds, steps=args.steps, warmup=args.warmup, rho=rho)
+    if w.members > 1:
+        v = 1.0 / float(np.mean(sample["step_times"]))
+        metric, unit = "ensemble member-steps/s (64 x 128^3 fp64)", "member-steps/s"
+        ms_step = 1e3 * w.members / v
+        desc = (f"{args.steps} timed gliosim::run steps (+{args.warmup} warm-up) of member 0 "
+                f"(rho={rho:.4f}); member-steps/s")
+    else:
+        v, full_s = extrapolate(sample, w.n)
+        metric = "expEuler steps/s at 256^3 fp64" if w.name.startswith("C4") else f"expEuler steps/s ({w.name})"
+        unit = "steps/s"
+        ms_step = 1e3 * full_s
+        desc = (f"{args.steps} timed gliosim::run steps (+{args.warmup} warm-up) on a "
+                f"{sample['slab_shape'][0]}x{sample['slab_shape'][1]}x{sample['slab_shape'][2]} z-slab, "
+                f"extrapolated by voxel count to {w.nx}x{w.ny}x{w.nz}")
     line = {
-        "impl": "reference", "metric": "expEuler steps/s at 256^3 fp64" if w.name.startswith("C4") else
-        f"expEuler steps/s ({w.name})", "value": v, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * full_s, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded shell phantom, BASELINE.json config)",
+        "impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if w.members > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded shell phantom, BASELINE.json config)",
         "config": {"workload": f"{w.name}: {w.note}", "grid": [w.nx, w.ny, w.nz], "parallelism": "CPU threads"},
-        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": sample["cores"], "kind": sample["kind"],
-                         "sample": (f"{args.steps} timed gliosim::step calls (+{args.warmup} warm-up) on a "
-                                    f"{sample['slab_shape'][0]}x{sample['slab_shape'][1]}x{sample['slab_shape'][2]} "
-                                    f"z-slab, extrapolated by voxel count to {w.nx}x{w.ny}x{w.nz}")},
-        "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": v, "unit": unit, "cores": sample["cores"], "kind": sample["kind"], "sample": desc},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
@@ -432,6 +535,8 @@ def main():
     w = W.get(args.config)
     if args.impl == "reference":
         run_reference(args, w, rank, world, local)
+    elif w.members > 1:
+        run_ensemble(args, w, rank, world, local)
     else:
         run_ours(args, w, rank, world, local)
 
