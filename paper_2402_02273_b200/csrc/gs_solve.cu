@@ -489,34 +489,30 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             if (pfirst + 1 + k2Stages <= plast) issue(pfirst + 1 + k2Stages);
         }
         // Iteration z: phase A makes T1(z+1) (z < z1), phase B finishes plane z-1 (z > z0) --
-        // independent work, so the two dependency chains overlap.
+        // independent work, so the two dependency chains overlap.  Register rings of three:
+        // iteration z with r = (z - z0) % 3 finds X(z) in X3[r], X(z+1) in X3[r+1] and loads
+        // X(z+2) into X3[r+2]; T1(z-1) in T3[r], T1(z) in T3[r+1], T1(z-2) in T3[r+2], which
+        // phase A then overwrites with T1(z+1).  Unrolling by three makes every index static.
+        double X3[3][2] = {{xa[0], xa[1]}, {xb[0], xb[1]}, {0.0, 0.0}};
+        double T3[3][2] = {{tm1[0], tm1[1]}, {t0[0], t0[1]}, {0.0, 0.0}};
         int sM = s1, sA = s2, sB = s3, sC = next_slot(s3);  // slots of planes z-1, z, z+1, z+2
         double* pT = outT + v0 + static_cast<int64_t>(z0) * op.sz;
         double* pF = outF + v0 + static_cast<int64_t>(z0) * op.sz;
-        for (int z = z0; z <= z1; ++z) {
-            double tp1[2] = {0.0, 0.0};
-            if (z < z1) {
-                wait_slot(sC);
-                if (needX) {
-                    const double* XC = ring.x(sC);
-                    xn[0] = XC[oX];
-                    xn[1] = XC[oX + kXPitch];
-                }
-                double lwN[2];
-                phaseA(z + 1, sA, sB, sC, xa, xb, xn, tp1, lwN);
-            }
+        auto iter = [&](int z, auto rconst) {
+            constexpr int r = decltype(rconst)::value;
+            constexpr int r1 = (r + 1) % 3, r2 = (r + 2) % 3;
             if (z > z0) {
-                // Phase B: own voxels of plane zo = z-1
+                // Phase B: own voxels of plane zo = z-1 (T1 of zo-1, zo, zo+1 in T3[r2], T3[r], T3[r1])
                 const int zo = z - 1;
                 const double* T1s = ring.t1((zo + 3) % kT1Planes);
                 const uint8_t* L = ring.l(sM);
                 const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
                 const double dhz = static_cast<double>((zo > 0) + (zo < op.nz - 1));
                 const double y0m = T1s[oT - kT1Pitch], y1p = T1s[oT + 2 * kT1Pitch];
-                const double a0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), tm2[0], y0m, T1s[oT - 1], tm1[0],
-                                               T1s[oT + 1], tm1[1], t0[0]);
-                const double a1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dhz), tm2[1], tm1[0],
-                                               T1s[oT + kT1Pitch - 1], tm1[1], T1s[oT + kT1Pitch + 1], y1p, t0[1]);
+                const double a0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), T3[r2][0], y0m, T1s[oT - 1],
+                                               T3[r][0], T1s[oT + 1], T3[r][1], T3[r1][0]);
+                const double a1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dhz), T3[r2][1], T3[r][0],
+                                               T1s[oT + kT1Pitch - 1], T3[r][1], T1s[oT + kT1Pitch + 1], y1p, T3[r1][1]);
                 const double t20 = __dmul_rn(c2, a0), t21 = __dmul_rn(c2, a1);
                 double fp0, fp1;
                 if (KIND == k2FirstZero) {
@@ -534,12 +530,13 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                         fp1 = xo1;
                     }
                 }
-                const double f10 = __dadd_rn(fp0, tm1[0]), f11 = __dadd_rn(fp1, tm1[1]);
+                const double f10 = __dadd_rn(fp0, T3[r][0]), f11 = __dadd_rn(fp1, T3[r][1]);
                 const double f20 = __dadd_rn(f10, t20), f21 = __dadd_rn(f11, t21);
+                // fmax drops NaN like std::max(m, |x|) (m is never NaN): expact.cpp:15-19
                 if (in0) {
                     pT[0] = t20;
                     pF[0] = f10;
-                    mx[0] = nan_dropping_max(mx[0], fabs(tm1[0]));
+                    mx[0] = nan_dropping_max(mx[0], fabs(T3[r][0]));
                     mx[1] = nan_dropping_max(mx[1], fabs(f10));
                     mx[2] = nan_dropping_max(mx[2], fabs(t20));
                     mx[3] = nan_dropping_max(mx[3], fabs(f20));
@@ -547,7 +544,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 if (in1) {
                     pT[op.sy] = t21;
                     pF[op.sy] = f11;
-                    mx[0] = nan_dropping_max(mx[0], fabs(tm1[1]));
+                    mx[0] = nan_dropping_max(mx[0], fabs(T3[r][1]));
                     mx[1] = nan_dropping_max(mx[1], fabs(f11));
                     mx[2] = nan_dropping_max(mx[2], fabs(t21));
                     mx[3] = nan_dropping_max(mx[3], fabs(f21));
@@ -555,13 +552,15 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 pT += op.sz;
                 pF += op.sz;
             }
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                xa[k] = xb[k];
-                xb[k] = xn[k];
-                tm2[k] = tm1[k];
-                tm1[k] = t0[k];
-                t0[k] = tp1[k];
+            if (z < z1) {
+                wait_slot(sC);
+                if (needX) {
+                    const double* XC = ring.x(sC);
+                    X3[r2][0] = XC[oX];
+                    X3[r2][1] = XC[oX + kXPitch];
+                }
+                double lwN[2];
+                phaseA(z + 1, sA, sB, sC, X3[r], X3[r1], X3[r2], T3[r2], lwN);
             }
             sM = sA;
             sA = sB;
@@ -572,6 +571,11 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 const int nxt = z - 1 + k2Stages;
                 if (nxt <= plast) issue(nxt);
             }
+        };
+        for (int zb = z0; zb <= z1; zb += 3) {
+            iter(zb, std::integral_constant<int, 0>{});
+            if (zb + 1 <= z1) iter(zb + 1, std::integral_constant<int, 1>{});
+            if (zb + 2 <= z1) iter(zb + 2, std::integral_constant<int, 2>{});
         }
         seq = base + static_cast<uint32_t>(np);
     }
