@@ -67,6 +67,14 @@ int64_t gs_num_points(const gs_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t), for callers that time or order work on it. */
 void* gs_stream(gs_ctx* ctx);
 
+/* A generic sparse operator: SparseOperator(dim, row_offsets, column_indices, coefficients)
+ * (sparse.hpp:13-38), validated with the reference's rules and messages (sparse.cpp:14-35):
+ * offs has dim+1 entries, offs[0] == 0, columns sorted and unique per row.  Every call below
+ * that takes the operator (apply, one_norm, expmv, phi1v, step, run) then applies this matrix
+ * on the GPU -- the path the reference's random-operator tests use (test_expact.cpp:79-239). */
+gs_status gs_create_csr(gs_ctx** out, int64_t dim, const int64_t* offs, const int32_t* cols, const double* vals,
+                        int device);
+
 /* ---- material map (K1) ------------------------------------------------------------ */
 /* resample + classify (imaging.cpp:65-72, 118-141) on the device from a uint8 stack
  * (x-fastest, x + y*w + z*w*hgt, imaging.hpp:21-25), then the D table of

@@ -47,7 +47,7 @@ _d3 = C.POINTER(C.c_double)
 _lib = None
 
 EXPORTS = [
-    "gs_create", "gs_destroy", "gs_last_error", "gs_num_points", "gs_stream",
+    "gs_create", "gs_create_csr", "gs_destroy", "gs_last_error", "gs_num_points", "gs_stream",
     "gs_set_intensity", "gs_set_labels", "gs_set_diffusion", "gs_get_labels", "gs_get_diffusion",
     "gs_one_norm", "gs_apply", "gs_set_state", "gs_get_state", "gs_state_device_ptr",
     "gs_select_params", "gs_expmv", "gs_phi1v", "gs_step", "gs_step_host", "gs_run", "gs_seed_initial",
@@ -66,6 +66,9 @@ def load(path: str | None = None):
     L = C.CDLL(path)
     vp = C.c_void_p
     L.gs_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, C.c_double, C.c_int]
+    L.gs_create_csr.argtypes = [C.POINTER(vp), C.c_int64,
+                                np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS"),
+                                np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS"), _dp, C.c_int]
     L.gs_destroy.argtypes = [vp]
     L.gs_destroy.restype = None
     L.gs_last_error.argtypes = [vp]

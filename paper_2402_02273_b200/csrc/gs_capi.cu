@@ -65,6 +65,10 @@ struct gs_ctx {
     double anorm = 0.0;
     bool anorm_valid = false;
 
+    // generic CSR operator (gs_create_csr)
+    bool is_csr = false;
+    DevBuf csr_offs, csr_cols, csr_vals, csc_offs, csc_abs;
+
     // vectors
     DevBuf u, g, f0, f1, t0, t1, out;
     // scratch
@@ -203,6 +207,9 @@ void fill_op(gs_ctx* c) {
     op.pal = c->palette_mode ? c->pal.as<uint8_t>() : nullptr;
     op.dvox = c->palette_mode ? nullptr : c->dvox.as<double>();
     op.wtab = c->wtab.as<double>();
+    op.csr_offs = c->is_csr ? c->csr_offs.as<int64_t>() : nullptr;
+    op.csr_cols = c->is_csr ? c->csr_cols.as<int32_t>() : nullptr;
+    op.csr_vals = c->is_csr ? c->csr_vals.as<double>() : nullptr;
 }
 
 // w table from palette D values: w = D * (1/(h*h)) exactly as stencil.cpp:8,23.
@@ -227,7 +234,12 @@ gs_status compute_anorm(gs_ctx* c) {
     GS_CUDA(c, c->normbits.alloc(sizeof(unsigned long long)));
     GS_CUDA(c, cudaMemsetAsync(c->normbits.p, 0, sizeof(unsigned long long), c->stream));
     const int blocks = static_cast<int>(std::min<int64_t>((c->n + 255) / 256, 148 * 8));
-    gs::colsum_norm_kernel<<<std::max(1, blocks), 256, 0, c->stream>>>(c->op, c->normbits.as<unsigned long long>());
+    if (c->is_csr)
+        gs::csc_norm_kernel<<<std::max(1, blocks), 256, 0, c->stream>>>(c->n, c->csc_offs.as<int64_t>(),
+                                                                         c->csc_abs.as<double>(),
+                                                                         c->normbits.as<unsigned long long>());
+    else
+        gs::colsum_norm_kernel<<<std::max(1, blocks), 256, 0, c->stream>>>(c->op, c->normbits.as<unsigned long long>());
     GS_CUDA(c, cudaGetLastError());
     unsigned long long bits = 0;
     GS_CUDA(c, cudaMemcpyAsync(&bits, c->normbits.p, sizeof bits, cudaMemcpyDeviceToHost, c->stream));
@@ -281,7 +293,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     p.op = c->op;
     p.grid_blocks = gb;
     p.anorm = c->anorm;
-    p.use_tma = (c->tma_ok && c->palette_mode && std::getenv("GS_DISABLE_TMA") == nullptr) ? 1 : 0;
+    p.use_tma = (c->tma_ok && c->palette_mode && !c->is_csr && std::getenv("GS_DISABLE_TMA") == nullptr) ? 1 : 0;
     if (p.use_tma) {
         for (int b = 0; b < gs::kNumBufs; ++b) {
             p.xmap[b] = c->xmap[b];
@@ -471,10 +483,72 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
     return GS_OK;
 }
 
+gs_status gs_create_csr(gs_ctx** out, int64_t dim, const int64_t* offs, const int32_t* cols, const double* vals,
+                        int device) {
+    if (!out || !offs) return fail(nullptr, GS_EINVAL, "gs_create_csr: null argument");
+    *out = nullptr;
+    // SparseOperator's validation, same messages (sparse.cpp:14-35)
+    if (dim < 0) return fail(nullptr, GS_EINVAL, "SparseOperator: negative dimension");
+    if (dim == 0) return fail(nullptr, GS_EINVAL, "gs_create_csr: dimension must be >= 1");
+    if (dim > INT32_MAX) return fail(nullptr, GS_EINVAL, "gs_create_csr: dimension exceeds int32 column indices");
+    if (offs[0] != 0) return fail(nullptr, GS_EINVAL, "SparseOperator: offsets/entries size mismatch");
+    const int64_t nnz = offs[dim];
+    if (nnz > 0 && (!cols || !vals)) return fail(nullptr, GS_EINVAL, "gs_create_csr: null argument");
+    for (int64_t r = 0; r < dim; ++r) {
+        if (offs[r] > offs[r + 1]) return fail(nullptr, GS_EINVAL, "SparseOperator: row offsets not monotone");
+        for (int64_t q = offs[r]; q < offs[r + 1]; ++q) {
+            if (cols[q] < 0 || cols[q] >= dim)
+                return fail(nullptr, GS_EINVAL, "SparseOperator: column index out of range");
+            if (q > offs[r] && cols[q] <= cols[q - 1])
+                return fail(nullptr, GS_EINVAL, "SparseOperator: columns not sorted unique in row " + std::to_string(r));
+        }
+    }
+    gs_ctx* c = nullptr;
+    gs_status st = gs_create(&c, static_cast<int>(dim), 1, 1, 1.0, device);
+    if (st != GS_OK) return st;
+    // transpose for the exact column sums: entries of column k in ascending row order, which is
+    // the order the reference's constructor accumulates them (sparse.cpp:36-38)
+    std::vector<int64_t> coff(static_cast<size_t>(dim) + 1, 0);
+    for (int64_t q = 0; q < nnz; ++q) ++coff[static_cast<size_t>(cols[q]) + 1];
+    for (int64_t k = 0; k < dim; ++k) coff[k + 1] += coff[k];
+    std::vector<int64_t> fillp(coff.begin(), coff.end() - 1);
+    std::vector<double> cabs(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+    for (int64_t r = 0; r < dim; ++r)
+        for (int64_t q = offs[r]; q < offs[r + 1]; ++q) cabs[static_cast<size_t>(fillp[cols[q]]++)] = std::fabs(vals[q]);
+    auto up = [&](DevBuf& b, const void* src, size_t bytes) -> cudaError_t {
+        cudaError_t e = b.alloc(std::max<size_t>(bytes, 8));
+        if (e != cudaSuccess) return e;
+        return bytes ? cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, c->stream) : cudaSuccess;
+    };
+    cudaError_t e;
+    if ((e = up(c->csr_offs, offs, sizeof(int64_t) * (dim + 1))) != cudaSuccess ||
+        (e = up(c->csr_cols, cols, sizeof(int32_t) * nnz)) != cudaSuccess ||
+        (e = up(c->csr_vals, vals, sizeof(double) * nnz)) != cudaSuccess ||
+        (e = up(c->csc_offs, coff.data(), sizeof(int64_t) * (dim + 1))) != cudaSuccess ||
+        (e = up(c->csc_abs, cabs.data(), sizeof(double) * nnz)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(c->stream)) != cudaSuccess) {
+        g_create_error = std::string("gs_create_csr: ") + cudaGetErrorString(e);
+        gs_destroy(c);
+        return GS_ECUDA;
+    }
+    c->is_csr = true;
+    c->palette_mode = false;
+    st = operator_ready(c);
+    if (st != GS_OK) {
+        g_create_error = c->err;
+        gs_destroy(c);
+        return st;
+    }
+    *out = c;
+    return GS_OK;
+}
+
 void gs_destroy(gs_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (DevBuf* b : {&c->csr_offs, &c->csr_cols, &c->csr_vals, &c->csc_offs, &c->csc_abs})
+        b->release();
     for (DevBuf* b : {&c->pal, &c->dvox, &c->wtab, &c->dtab, &c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out,
                       &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->ctrl, &c->metrics, &c->infos,
                       &c->normbits, &c->trace})
@@ -492,6 +566,7 @@ void* gs_stream(gs_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr;
 
 gs_status gs_set_intensity(gs_ctx* c, const uint8_t* stack, int w, int hgt, int slices, int t_air, int t_white,
                            int t_gray, double d_white, double d_gray) {
+    if (c && c->is_csr) return fail(c, GS_EINVAL, "operator is a generic CSR matrix (gs_create_csr)");
     if (!c || !stack) return fail(c, GS_EINVAL, "gs_set_intensity: null argument");
     if (slices < 1 || w < 1 || hgt < 1) return fail(c, GS_EDATA, "resample: degenerate stack");  // imaging.cpp:126-127
     cudaSetDevice(c->device);
@@ -514,6 +589,7 @@ gs_status gs_set_intensity(gs_ctx* c, const uint8_t* stack, int w, int hgt, int 
 }
 
 gs_status gs_set_labels(gs_ctx* c, const uint8_t* labels, double d_white, double d_gray) {
+    if (c && c->is_csr) return fail(c, GS_EINVAL, "operator is a generic CSR matrix (gs_create_csr)");
     if (!c || !labels) return fail(c, GS_EINVAL, "gs_set_labels: null argument");
     for (int64_t v = 0; v < c->n; ++v)
         if (labels[v] > 3)
@@ -528,6 +604,7 @@ gs_status gs_set_labels(gs_ctx* c, const uint8_t* labels, double d_white, double
 }
 
 gs_status gs_set_diffusion(gs_ctx* c, const double* d) {
+    if (c && c->is_csr) return fail(c, GS_EINVAL, "operator is a generic CSR matrix (gs_create_csr)");
     if (!c || !d) return fail(c, GS_EINVAL, "gs_set_diffusion: null argument");
     cudaSetDevice(c->device);
     // Palette compression: <= 256 distinct bit patterns -> uint8 index + table (1 B/voxel

@@ -30,7 +30,21 @@ struct StencilOp {
     // work decomposition: tiles of kTX x kTY columns, z-chunks of zc planes
     int tiles_x, tiles_y, zc, chunks_z;
     int64_t n_items;
+    // generic operator (SparseOperator, sparse.hpp:13-38): CSR with sorted unique columns.
+    // Non-null -> every sweep applies this matrix instead of the stencil.
+    const int64_t* csr_offs;
+    const int32_t* csr_cols;
+    const double* csr_vals;
 };
+
+// Row r of a generic CSR operator applied to x exactly as SparseOperator::apply does
+// (sparse.cpp:54-58): acc = 0; acc += val*x[col] in storage order.
+__device__ __forceinline__ double csr_row_apply(const StencilOp& op, int64_t r, const double* x) {
+    double acc = 0.0;
+    for (int64_t q = op.csr_offs[r]; q < op.csr_offs[r + 1]; ++q)
+        acc = __dadd_rn(acc, __dmul_rn(op.csr_vals[q], x[op.csr_cols[q]]));
+    return acc;
+}
 
 // Per-voxel row coefficients: w = D_v / h^2 and whether the row exists (D_v != 0).
 struct RowCoef {

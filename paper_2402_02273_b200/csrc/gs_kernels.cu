@@ -97,4 +97,18 @@ __global__ void colsum_norm_kernel(StencilOp op, unsigned long long* out_bits) {
         atomicMax(out_bits, static_cast<unsigned long long>(__double_as_longlong(best)));
 }
 
+__global__ void csc_norm_kernel(int64_t n, const int64_t* __restrict__ csc_offs, const double* __restrict__ csc_absvals,
+                                unsigned long long* out_bits) {
+    double best = 0.0;
+    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < n;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0;  // sparse.cpp:36-38
+        for (int64_t q = csc_offs[c]; q < csc_offs[c + 1]; ++q) s = __dadd_rn(s, csc_absvals[q]);
+        best = nan_dropping_max(best, s);
+    }
+    best = warp_max(best);
+    if ((threadIdx.x & 31) == 0 && best > 0.0)
+        atomicMax(out_bits, static_cast<unsigned long long>(__double_as_longlong(best)));
+}
+
 }  // namespace gs

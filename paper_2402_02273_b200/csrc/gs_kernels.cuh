@@ -109,6 +109,10 @@ __global__ void material_kernel(const uint8_t* stack, int w, int hgt, int slices
                                 int t_air, int t_white, int t_gray, uint8_t* labels);
 // K3: exact 1-norm of the stencil operator (sparse.cpp:36-40), result as ordered bits
 __global__ void colsum_norm_kernel(StencilOp op, unsigned long long* out_bits);
+// Exact 1-norm of a generic operator from its transpose (CSC, rows ascending within a column):
+// one thread per column sums |a| in the CSR storage order the reference's constructor walks.
+__global__ void csc_norm_kernel(int64_t n, const int64_t* csc_offs, const double* csc_absvals,
+                                unsigned long long* out_bits);
 // Per-voxel D(x) reconstruction (for gs_get_diffusion in palette mode)
 __global__ void expand_palette_kernel(const uint8_t* pal, const double* dtab, int64_t n, double* d);
 // The exponential-Euler step as a launch sequence (gs_solve.cu):

@@ -614,7 +614,15 @@ template <class Body>
 __device__ __forceinline__ void stencil_sweep(const SolveParams& p, Smem& sm, const Ring& ring, uint32_t& seq, int xb,
                                               int fb, int bb, Body&& body) {
     const bool nf = fb >= 0, nb = bb >= 0;
-    if (p.use_tma) {
+    if (p.op.csr_offs) {
+        // generic CSR operator: grid-stride over rows
+        const double* X = p.buf[xb];
+        const double* F = nf ? p.buf[fb] : nullptr;
+        const double* B = nb ? p.buf[bb] : nullptr;
+        sweep_points(p.op, [&](int64_t v) {
+            body(v, csr_row_apply(p.op, v, X), X[v], F ? F[v] : 0.0, B ? B[v] : 0.0);
+        });
+    } else if (p.use_tma) {
         if (nf && nb) sweep_tma<true, true>(p, ring, xb, fb, bb, seq, sm.wtab, body);
         else if (nf) sweep_tma<true, false>(p, ring, xb, fb, 0, seq, sm.wtab, body);
         else if (nb) sweep_tma<false, true>(p, ring, xb, 0, bb, seq, sm.wtab, body);

@@ -327,6 +327,24 @@ class StencilOperator:
         return m, inf
 
 
+class CsrOperator(StencilOperator):
+    """A generic SparseOperator (sparse.hpp:13-38) on the GPU: CSR with sorted, unique columns,
+    validated like the reference's constructor (sparse.cpp:14-35)."""
+
+    def __init__(self, offs, cols, vals, device: int = 0):
+        self.lib = N.load()
+        offs = np.ascontiguousarray(offs, dtype=np.int64)
+        cols = np.ascontiguousarray(cols, dtype=np.int32)
+        vals = np.ascontiguousarray(vals, dtype=np.float64)
+        n = len(offs) - 1
+        self.grid = Grid(max(n, 1), 1, 1, 1.0)
+        h = C.c_void_p()
+        rc = self.lib.gs_create_csr(C.byref(h), n, offs, cols, vals, device)
+        if rc != N.GS_OK:
+            _raise(rc, self.lib.gs_last_error(None).decode())
+        self.ctx = h
+
+
 # ------------------------------------------------------------------------------------
 # free functions with the reference's names
 # ------------------------------------------------------------------------------------

@@ -323,3 +323,81 @@ def test_cpp_dropin_parity():
     print(res.stdout)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "all passed" in res.stdout
+
+
+# ---- generic SparseOperator path: the reference's own random-operator KATs on the GPU -----
+
+def _csr(G, kat, p):
+    return G.CsrOperator(kat[p + ".offs"], kat[p + ".cols"], kat[p + ".vals"])
+
+
+@pytest.mark.parametrize("tag,phi", [("expmv_rand", False), ("phi1v_rand", True), ("accept_c1", True)])
+def test_csr_random_operator_kats(G, port, kat, tag, phi):
+    """test_expact.cpp:79-175 / acceptance.cpp:57-86 inputs: expmv bitwise vs the reference;
+    phi1v bitwise vs the oracle given the device's two sums and within 1e-12 of the reference;
+    both within the reference tests' 1e-9 of the dense oracles."""
+    for i in range(int(kat[tag + ".count"][0])):
+        p = f"{tag}.{i}"
+        t, tol, b = float(kat[p + ".t"][0]), float(kat[p + ".tol"][0]), kat[p + ".b"]
+        with _csr(G, kat, p + ".A") as op:
+            assert op.one_norm() == kat[p + ".A.norm1"][0], p
+            if phi:
+                got, info = G.phi1v(t, op, b, tol, info=True)
+                want, _ = port.phi1v(t, port.csr(kat[p + ".A.offs"], kat[p + ".A.cols"], kat[p + ".A.vals"]), b, tol,
+                                     bnorm=info.bnorm, coln=info.coln)
+                assert np.array_equal(got, want), p
+                assert rel_l2(got, kat[p + ".ref"]) <= 1e-12, p
+            else:
+                got = G.expmv(t, op, b, tol)
+                assert np.array_equal(got, kat[p + ".ref"]), p
+            dense = kat[p + ".dense"]
+            assert np.max(np.abs(got - dense)) / max(np.max(np.abs(dense)), 1e-300) <= 1e-9
+            if p + ".ref_exp" in kat:
+                assert np.array_equal(G.expmv(t, op, b, tol), kat[p + ".ref_exp"]), p
+
+
+def test_csr_apply_and_stencil_equivalence(G, kat):
+    """The assembled CSR of the stencil KATs through the generic path equals the matrix-free path."""
+    for i in range(int(kat["stencil.count"][0])):
+        p = f"stencil.{i}"
+        with _csr(G, kat, p + ".A") as op:
+            assert np.array_equal(op.apply(kat[p + ".x"]), kat[p + ".Ax"]), p
+            assert np.array_equal(G.expmv(7.5, op, kat[p + ".x"], 1e-10), kat[p + ".expmv"]), p
+
+
+def test_csr_validation_and_errors(G):
+    """SparseOperator's validation messages (sparse.cpp:14-35) and the divergence KAT
+    (test_expact.cpp:140-143: a 1x1 operator 40 at t = 100 overflows)."""
+    with pytest.raises(ValueError, match="not sorted unique in row 0"):
+        G.CsrOperator([0, 2], [0, 0], [1.0, 2.0])
+    with pytest.raises(ValueError, match="column index out of range"):
+        G.CsrOperator([0, 1], [3], [1.0])
+    with pytest.raises(ValueError, match="not monotone"):
+        G.CsrOperator([0, 2, 1], [0, 1], [1.0, 2.0])
+    with G.CsrOperator([0, 1], [0], [40.0]) as hot:
+        with pytest.raises(G.NumericError, match="non-finite"):
+            G.expmv(100.0, hot, np.array([1.0]), 1e-10)
+    # step with an empty operator = forward Euler bit for bit (test_integrator.cpp:99-106)
+    with G.CsrOperator([0, 0, 0, 0], [], []) as empty:
+        u = np.array([0.2, 0.5, 0.9])
+        assert np.array_equal(G.step(empty, u, 0.4, 0.25, 1e-10), u + 0.25 * (0.4 * u * (1.0 - u)))
+        assert np.array_equal(G.phi1v(5.0, empty, u, 1e-10), u)
+
+
+def test_csr_step_semigroup_and_linearity(G, kat):
+    """expmv semigroup (test_expact.cpp:98-106) and phi1v linearity (:177-193) on the GPU."""
+    p = "expmv_rand.3.A"
+    with _csr(G, kat, p) as op:
+        n = op.dim()
+        rng = np.random.default_rng(7)
+        b = rng.uniform(-1, 1, n)
+        nrm = op.one_norm()
+        t1, t2 = 0.8 / nrm, 1.9 / nrm
+        direct = G.expmv(t1 + t2, op, b, 1e-12)
+        chained = G.expmv(t2, op, G.expmv(t1, op, b, 1e-12), 1e-12)
+        assert np.max(np.abs(chained - direct)) <= 1e-9 * np.max(np.abs(direct))
+        b1, b2 = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+        t = 2.0 / nrm
+        lhs = G.phi1v(t, op, 0.7 * b1 - 1.3 * b2, 1e-12)
+        rhs = 0.7 * G.phi1v(t, op, b1, 1e-12) - 1.3 * G.phi1v(t, op, b2, 1e-12)
+        assert np.max(np.abs(lhs - rhs)) <= 1e-9 * np.max(np.abs(rhs))
