@@ -66,6 +66,11 @@ def dist_env():
     return rank, world, local
 
 
+def under_launcher() -> bool:
+    """torchrun (torch.distributed.run) sets these: use the process group even at world 1."""
+    return all(k in os.environ for k in ("RANK", "WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT"))
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -89,7 +94,7 @@ class Clocks:
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -235,7 +240,7 @@ def run_ours(args, w, rank, world, local):
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or under_launcher():
         import torch.distributed as D
         D.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = D
@@ -398,7 +403,7 @@ def run_ensemble(args, w, rank, world, local):
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or under_launcher():
         import torch.distributed as D
         D.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = D
