@@ -60,7 +60,8 @@ typedef struct gs_ctx gs_ctx;
  * Grid's constructor (grid.hpp:24-29). */
 gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device);
 void gs_destroy(gs_ctx* ctx);
-/* Message of the last failing call on ctx (or of the last failed gs_create when ctx is NULL). */
+/* Message of the last failing call on ctx; with ctx == NULL, of the last failing call that
+ * takes no context (gs_create, gs_select_params, the file functions) on this thread. */
 const char* gs_last_error(const gs_ctx* ctx);
 /* Number of voxels nx*ny*nz (Grid::num_points, grid.hpp:31-33). */
 int64_t gs_num_points(const gs_ctx* ctx);
@@ -144,6 +145,47 @@ gs_status gs_get_trace(gs_ctx* ctx, uint64_t* pairs, int capacity, int* count);
  * [0] prep (RHS), [1] border, [2] taylor (the Taylor-term kernel), [3] update. */
 gs_status gs_set_kernel_timing(gs_ctx* ctx, int enable);
 gs_status gs_get_kernel_times(gs_ctx* ctx, double ms[4], int launches[4]);
+
+/* ---- snapshot and metrics files (vtk.hpp:15-45, src/vtk.cpp:59-157) ------------------- */
+/* write_vtk (vtk.cpp:59-91): legacy ASCII VTK, header + one "%.17g" value per line, then,
+ * when labels != NULL, "SCALARS material int 1" and one label per line.  Byte-identical to
+ * the reference.  threads <= 0 picks the host's core count.  Errors: GS_EDATA "cannot open
+ * <path> for writing" / "write failed: <path>". */
+gs_status gs_write_vtk(const char* path, const double* u, int nx, int ny, int nz, double h, const double origin[3],
+                       const uint8_t* labels, int threads);
+/* read_vtk (vtk.cpp:93-143), same checks and messages.  With values == NULL only the header
+ * is read (dims, h, origin); otherwise capacity >= nx*ny*nz values are filled.  A trailing
+ * material array is ignored. */
+gs_status gs_read_vtk(const char* path, int dims[3], double* h, double origin[3], double* values, int64_t capacity,
+                      int threads);
+/* write_metrics_csv (vtk.cpp:145-157): "step,time_days,total_mass,max_density,radius_mm". */
+gs_status gs_write_metrics_csv(const char* path, int count, const int32_t* step, const double* time,
+                               const gs_metrics* metrics);
+/* The snapshot sink of run_to_directory (pipeline.cpp:39-45), asynchronous: opens path now
+ * (an unwritable path fails here, as write_vtk would), copies the resident state on the
+ * device, lands it in pinned host memory on a side stream and formats it on a writer
+ * thread while later steps run.  labels (nx*ny*nz codes) may be NULL and are copied.  At
+ * most 3 snapshots are in flight; the call blocks while all are busy, and reports the
+ * error of an earlier snapshot that failed. */
+gs_status gs_snapshot_vtk(gs_ctx* ctx, const char* path, const double origin[3], const uint8_t* labels);
+/* Wait for every queued snapshot; returns the first failure not yet reported. */
+gs_status gs_snapshot_flush(gs_ctx* ctx);
+
+/* ---- image and label files (imaging.hpp:28-54, src/imaging.cpp:14-116, 166-190) ------ */
+/* load_stack: binary PGM slices (P5, maxval 255), all the same size, stacked bottom first.
+ * out == NULL returns the sizes only (all files still validated); otherwise capacity >=
+ * width*height*slices bytes receive the intensities (x fastest). */
+gs_status gs_load_stack(const char* const* paths, int count, int* width, int* height, int* slices, uint8_t* out,
+                        int64_t capacity);
+/* load_raw_volume: "nx ny nz\n" then nx*ny*nz bytes.  out == NULL returns the sizes only. */
+gs_status gs_load_raw_volume(const char* path, int* width, int* height, int* slices, uint8_t* out,
+                             int64_t capacity);
+/* write_label_volume / read_label_volume: the raw format with Material codes 0..3. */
+gs_status gs_write_label_volume(const char* path, const uint8_t* labels, int nx, int ny, int nz);
+gs_status gs_read_label_volume(const char* path, int nx, int ny, int nz, uint8_t* labels);
+/* matter_fractions (imaging.cpp:155-164) of the context's device labels: white and gray
+ * shares of the tissue voxels.  GS_EDATA when there is no tissue. */
+gs_status gs_matter_fractions(gs_ctx* ctx, double* white, double* gray);
 
 #ifdef __cplusplus
 }

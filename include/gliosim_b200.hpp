@@ -13,6 +13,9 @@
 //   std::vector<double> step(A, u, rho, tau, tol, workers)     step(A, u, rho, tau, tol) (integrator.hpp:59-60)
 //   RunResult run(cfg, d, u0, workers, sink, warn, watch)      run(cfg, d, u0, sink, warn, watch)
 //                                                               (integrator.hpp:75-77)
+//   write_vtk / read_vtk / write_metrics_csv (vtk.hpp:40-48)   same names (byte-identical files)
+//   RunResult run_to_directory(cfg, d, materials, dir, ...)    run_to_directory(...) (pipeline.hpp:18-24),
+//                                                               snapshots written while the GPU steps on
 //   std::invalid_argument / numeric_error / data_error         same std::invalid_argument /
 //                                                               gliosim_b200::numeric_error / data_error
 //
@@ -25,6 +28,8 @@
 
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <filesystem>
 #include <functional>
 #include <stdexcept>
 #include <string>
@@ -180,31 +185,65 @@ inline std::vector<double> step(const StencilOperator& a, const std::vector<doub
     return out;
 }
 
-// run (integrator.cpp:91-138) for SimConfig- and DiffusionField-like types: the time loop on
-// the GPU (one launch sequence per snapshot segment), metrics computed on the device at every
-// node, hooks fired in the reference's order.
+namespace detail {
+
+// Where snapshot nodes go: the caller's SnapshotSink (a host copy per node) and/or the
+// library's asynchronous VTK writer (gs_snapshot_vtk) for run_to_directory.
+struct VtkSink {
+    std::string dir;
+    const std::vector<uint8_t>* labels = nullptr;
+};
+
 template <class SimConfigT, class DiffusionFieldT>
-RunResult run(const SimConfigT& cfg, const DiffusionFieldT& d, std::vector<double> u0, int = 1,
-              const SnapshotSink& snapshot = {}, const RangeWarning& on_range = {}, const StepWatcher& on_step = {}) {
-    cfg.validate();
+RunResult run_impl(const SimConfigT& cfg, const DiffusionFieldT& d, std::vector<double> u0,
+                   const SnapshotSink& snapshot, const RangeWarning& on_range, const StepWatcher& on_step,
+                   const VtkSink* vtk, bool seed_from_cfg = false) {
     const int64_t n = static_cast<int64_t>(d.grid.nx) * d.grid.ny * d.grid.nz;
-    if (static_cast<int64_t>(u0.size()) != n)
+    const double origin[3] = {cfg.origin[0], cfg.origin[1], cfg.origin[2]};
+    const double center[3] = {cfg.seed_center[0], cfg.seed_center[1], cfg.seed_center[2]};
+    const double gorigin[3] = {d.grid.origin[0], d.grid.origin[1], d.grid.origin[2]};
+    if (!seed_from_cfg) cfg.validate();
+    if (!seed_from_cfg && static_cast<int64_t>(u0.size()) != n)
         throw std::invalid_argument("run: initial state length does not match the grid");
     if (static_cast<int64_t>(d.d.size()) != n)
         throw std::invalid_argument("run: diffusion field length does not match the grid");
     RunResult res;
     StencilOperator a = gliosim_b200::assemble_diffusion(d);
+    if (seed_from_cfg) {  // seed_initial(d, cfg) (integrator.cpp:32-50), on the operator's own D mask
+        u0.resize(static_cast<size_t>(n));
+        check(gs_seed_initial(a.ctx(), gorigin, cfg.seed_amplitude, cfg.seed_width, center, 1, u0.data()), a.ctx());
+        cfg.validate();
+    }
     check(gs_set_state(a.ctx(), u0.data()), a.ctx());
     const double tau = (cfg.t_end - cfg.t0) / cfg.num_steps;
     auto time_at = [&](int k) { return k >= cfg.num_steps ? cfg.t_end : cfg.t0 + k * tau; };
-    const double origin[3] = {cfg.origin[0], cfg.origin[1], cfg.origin[2]};
-    const double center[3] = {cfg.seed_center[0], cfg.seed_center[1], cfg.seed_center[2]};
-    if (snapshot) snapshot(0, time_at(0), u0);
+    const bool sinks = snapshot || vtk;
+    auto emit = [&](int k, const std::vector<double>* host) {
+        const auto tic = std::chrono::steady_clock::now();
+        if (snapshot) {
+            if (host) {
+                snapshot(k, time_at(k), *host);
+            } else {
+                std::vector<double> u(static_cast<size_t>(n));
+                check(gs_get_state(a.ctx(), u.data()), a.ctx());
+                snapshot(k, time_at(k), u);
+            }
+        }
+        if (vtk) {
+            char name[32];
+            std::snprintf(name, sizeof name, "snapshot_%04d.vtk", k);
+            const std::string path = vtk->dir + "/" + name;
+            check(gs_snapshot_vtk(a.ctx(), path.c_str(), gorigin, vtk->labels ? vtk->labels->data() : nullptr),
+                  a.ctx());
+        }
+        res.timings.io_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - tic).count();
+    };
+    emit(0, &u0);
     int done = 0;
     std::vector<gs_metrics> m;
     while (done < cfg.num_steps) {
         int cut = cfg.num_steps;
-        if (snapshot)
+        if (sinks)
             for (int k = done + 1; k <= cfg.num_steps; ++k)
                 if (k % cfg.snapshot_every == 0 || k == cfg.num_steps) {
                     cut = k;
@@ -226,14 +265,118 @@ RunResult run(const SimConfigT& cfg, const DiffusionFieldT& d, std::vector<doubl
                 on_range(sm.step, sm.min_density, sm.max_density);
         }
         done = cut;
-        if (snapshot) {
-            std::vector<double> u(static_cast<size_t>(n));
-            check(gs_get_state(a.ctx(), u.data()), a.ctx());
-            snapshot(cut, time_at(cut), u);
-        }
+        if (sinks) emit(cut, nullptr);
+    }
+    if (vtk) {
+        const auto tic = std::chrono::steady_clock::now();
+        check(gs_snapshot_flush(a.ctx()), a.ctx());
+        res.timings.io_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - tic).count();
     }
     res.u.resize(static_cast<size_t>(n));
     check(gs_get_state(a.ctx(), res.u.data()), a.ctx());
+    return res;
+}
+
+}  // namespace detail
+
+// run (integrator.cpp:91-138) for SimConfig- and DiffusionField-like types: the time loop on
+// the GPU (one launch sequence per snapshot segment), metrics computed on the device at every
+// node, hooks fired in the reference's order.
+template <class SimConfigT, class DiffusionFieldT>
+RunResult run(const SimConfigT& cfg, const DiffusionFieldT& d, std::vector<double> u0, int = 1,
+              const SnapshotSink& snapshot = {}, const RangeWarning& on_range = {}, const StepWatcher& on_step = {}) {
+    return detail::run_impl(cfg, d, std::move(u0), snapshot, on_range, on_step, nullptr);
+}
+
+// ---- files (vtk.hpp:40-48): byte-identical to the reference's writers -------------------
+namespace detail {
+inline void check_free(gs_status st) { check(st, nullptr); }
+
+template <class MaterialVolumeT>
+std::vector<uint8_t> label_bytes(const MaterialVolumeT& mv) {
+    std::vector<uint8_t> out(mv.labels.size());
+    for (size_t v = 0; v < out.size(); ++v) out[v] = static_cast<uint8_t>(mv.labels[v]);
+    return out;
+}
+}  // namespace detail
+
+// write_vtk (vtk.cpp:59-91) for ScalarField- and MaterialVolume-like types.
+template <class ScalarFieldT>
+void write_vtk(const ScalarFieldT& u, const std::string& path) {
+    const auto& g = u.grid;
+    if (static_cast<int64_t>(u.values.size()) != static_cast<int64_t>(g.nx) * g.ny * g.nz)
+        throw std::invalid_argument("write_vtk: field length does not match its grid");
+    const double o[3] = {g.origin[0], g.origin[1], g.origin[2]};
+    detail::check_free(gs_write_vtk(path.c_str(), u.values.data(), g.nx, g.ny, g.nz, g.h, o, nullptr, 0));
+}
+
+template <class ScalarFieldT, class MaterialVolumeT>
+void write_vtk(const ScalarFieldT& u, const std::string& path, const MaterialVolumeT* materials) {
+    if (!materials) return write_vtk(u, path);
+    const auto& g = u.grid;
+    if (static_cast<int64_t>(u.values.size()) != static_cast<int64_t>(g.nx) * g.ny * g.nz)
+        throw std::invalid_argument("write_vtk: field length does not match its grid");
+    if (materials->labels.size() != u.values.size())
+        throw std::invalid_argument("write_vtk: material volume does not match the field grid");
+    const std::vector<uint8_t> lab = detail::label_bytes(*materials);
+    const double o[3] = {g.origin[0], g.origin[1], g.origin[2]};
+    detail::check_free(gs_write_vtk(path.c_str(), u.values.data(), g.nx, g.ny, g.nz, g.h, o, lab.data(), 0));
+}
+
+// read_vtk (vtk.cpp:93-143): ScalarFieldT needs a default constructor, .grid (nx, ny, nz, h,
+// origin) and .values, e.g. gliosim_b200::read_vtk<gliosim::ScalarField>(path).
+template <class ScalarFieldT>
+ScalarFieldT read_vtk(const std::string& path) {
+    int dims[3];
+    double h = 0.0, o[3];
+    detail::check_free(gs_read_vtk(path.c_str(), dims, &h, o, nullptr, 0, 0));
+    ScalarFieldT f;
+    f.grid = decltype(f.grid)(dims[0], dims[1], dims[2], h, {o[0], o[1], o[2]});
+    f.values.resize(static_cast<size_t>(dims[0]) * dims[1] * dims[2]);
+    detail::check_free(gs_read_vtk(path.c_str(), dims, &h, o, f.values.data(),
+                                   static_cast<int64_t>(f.values.size()), 0));
+    return f;
+}
+
+// write_metrics_csv (vtk.cpp:145-157) for any range of StepMetrics-like records.
+template <class SeriesT>
+void write_metrics_csv(const SeriesT& series, const std::string& path) {
+    std::vector<int32_t> step;
+    std::vector<double> time;
+    std::vector<gs_metrics> m;
+    for (const auto& r : series) {
+        step.push_back(r.step);
+        time.push_back(r.time);
+        m.push_back({r.total_mass, r.max_density, r.min_density, r.radius});
+    }
+    detail::check_free(gs_write_metrics_csv(path.c_str(), static_cast<int>(step.size()), step.data(), time.data(),
+                                            m.data()));
+}
+
+// run_to_directory (pipeline.cpp:30-53): seed from cfg (integrator.cpp:32-50, D-masked), run on
+// the GPU, snapshot_NNNN.vtk at every snapshot node (with the material array when given) written
+// by the library's writer thread while later steps run, then metrics.csv.
+template <class SimConfigT, class DiffusionFieldT, class MaterialVolumeT>
+RunResult run_to_directory(const SimConfigT& cfg, const DiffusionFieldT& d, const MaterialVolumeT* materials,
+                           const std::string& out_dir, int = 1, const StepWatcher& on_step = {},
+                           const RangeWarning& on_range = {}) {
+    try {
+        std::filesystem::create_directories(out_dir);
+    } catch (const std::filesystem::filesystem_error& e) {
+        throw data_error("cannot create output directory " + out_dir + ": " + e.what());
+    }
+    const int64_t n = static_cast<int64_t>(d.grid.nx) * d.grid.ny * d.grid.nz;
+    std::vector<uint8_t> lab;
+    if (materials) {
+        if (static_cast<int64_t>(materials->labels.size()) != n)
+            throw std::invalid_argument("write_vtk: material volume does not match the field grid");
+        lab = detail::label_bytes(*materials);
+    }
+    const detail::VtkSink sink{out_dir, materials ? &lab : nullptr};
+    RunResult res = detail::run_impl(cfg, d, {}, {}, on_range, on_step, &sink, true);
+    const auto tic = std::chrono::steady_clock::now();
+    write_metrics_csv(res.metrics, out_dir + "/metrics.csv");
+    res.timings.io_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - tic).count();
     return res;
 }
 

@@ -273,7 +273,7 @@ class Ref:
 
     def _check(self, rc):
         if rc:
-            raise OracleError(rc, self.lib.ref_last_error().decode())
+            raise OracleError(rc, self.lib.ref_last_error().decode("utf-8", "surrogateescape"))
 
     def step(self, shape, h, d, u, rho, tau, tol, workers=1):
         out = np.empty(len(u), dtype=np.float64)
@@ -325,6 +325,97 @@ class Ref:
 
     def classify(self, v):
         return self.lib.ref_classify(v)
+
+    # ---- file formats (vtk.cpp, imaging.cpp, pipeline.cpp) ------------------------------
+    def _files(self):
+        L = self.lib
+        if getattr(self, "_files_typed", False):
+            return L
+        cp, vp, ip = C.c_char_p, C.c_void_p, C.POINTER(C.c_int)
+        L.ref_write_vtk.argtypes = [cp, _dp, C.c_int, C.c_int, C.c_int, C.c_double, _dp, vp]
+        L.ref_read_vtk.argtypes = [cp, ip, C.POINTER(C.c_double), _dp, vp, C.c_int64]
+        L.ref_write_metrics_csv.argtypes = [cp, C.c_int, vp, vp, vp]
+        L.ref_load_stack.argtypes = [C.POINTER(cp), C.c_int, ip, vp, C.c_int64]
+        L.ref_load_raw_volume.argtypes = [cp, ip, vp, C.c_int64]
+        L.ref_write_label_volume.argtypes = [cp, _u8p, C.c_int, C.c_int, C.c_int]
+        L.ref_read_label_volume.argtypes = [cp, C.c_int, C.c_int, C.c_int, _u8p]
+        L.ref_matter_fractions.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double)]
+        L.ref_run_to_directory.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, _dp, vp, C.c_int, C.c_int,
+                                           C.c_double, C.c_double, C.c_double, C.c_double, _dp, C.c_double,
+                                           C.c_double, cp, vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        self._files_typed = True
+        return L
+
+    def write_vtk(self, path, u, shape, h, origin=(0.0, 0.0, 0.0), labels=None):
+        lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.uint8)
+        self._check(self._files().ref_write_vtk(os.fsencode(path), np.ascontiguousarray(u, dtype=np.float64),
+                                                *shape, h, np.array(origin, dtype=np.float64),
+                                                None if lab is None else lab.ctypes.data))
+
+    def read_vtk(self, path):
+        """-> (dims, h, origin, values)"""
+        L = self._files()
+        dims = (C.c_int * 3)()
+        h = C.c_double()
+        origin = np.zeros(3)
+        self._check(L.ref_read_vtk(os.fsencode(path), dims, C.byref(h), origin, None, 0))
+        vals = np.empty(dims[0] * dims[1] * dims[2])
+        self._check(L.ref_read_vtk(os.fsencode(path), dims, C.byref(h), origin, vals.ctypes.data, vals.size))
+        return tuple(dims), h.value, tuple(origin), vals
+
+    def write_metrics_csv(self, path, steps, times, m4):
+        st = np.ascontiguousarray(steps, dtype=np.int32)
+        tm = np.ascontiguousarray(times, dtype=np.float64)
+        mm = np.ascontiguousarray(m4, dtype=np.float64).reshape(-1, 4)
+        n = len(st)
+        self._check(self._files().ref_write_metrics_csv(os.fsencode(path), n, st.ctypes.data if n else None,
+                                                        tm.ctypes.data if n else None,
+                                                        mm.ctypes.data if n else None))
+
+    def load_stack(self, paths):
+        L = self._files()
+        arr = (C.c_char_p * max(1, len(paths)))(*[os.fsencode(p) for p in paths])
+        dims = (C.c_int * 3)()
+        self._check(L.ref_load_stack(arr, len(paths), dims, None, 0))
+        out = np.empty(dims[0] * dims[1] * dims[2], dtype=np.uint8)
+        self._check(L.ref_load_stack(arr, len(paths), dims, out.ctypes.data, out.size))
+        return tuple(dims), out
+
+    def load_raw_volume(self, path):
+        L = self._files()
+        dims = (C.c_int * 3)()
+        self._check(L.ref_load_raw_volume(os.fsencode(path), dims, None, 0))
+        out = np.empty(dims[0] * dims[1] * dims[2], dtype=np.uint8)
+        self._check(L.ref_load_raw_volume(os.fsencode(path), dims, out.ctypes.data, out.size))
+        return tuple(dims), out
+
+    def write_label_volume(self, path, labels, shape):
+        self._check(self._files().ref_write_label_volume(os.fsencode(path),
+                                                         np.ascontiguousarray(labels, dtype=np.uint8), *shape))
+
+    def read_label_volume(self, path, shape):
+        out = np.empty(shape[0] * shape[1] * shape[2], dtype=np.uint8)
+        self._check(self._files().ref_read_label_volume(os.fsencode(path), *shape, out))
+        return out
+
+    def matter_fractions(self, labels, shape):
+        w, g = C.c_double(), C.c_double()
+        self._check(self._files().ref_matter_fractions(np.ascontiguousarray(labels, dtype=np.uint8), *shape,
+                                                       C.byref(w), C.byref(g)))
+        return w.value, g.value
+
+    def run_to_directory(self, shape, h, d, labels, n_steps, snapshot_every, rho, t0, t_end, tol, center,
+                         amplitude, width, out_dir):
+        n = shape[0] * shape[1] * shape[2]
+        u = np.empty(n)
+        ss, io = C.c_double(), C.c_double()
+        lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.uint8)
+        self._check(self._files().ref_run_to_directory(
+            *shape, h, np.ascontiguousarray(d, dtype=np.float64), None if lab is None else lab.ctypes.data,
+            n_steps, snapshot_every, rho, t0, t_end, tol, np.array(center, dtype=np.float64), amplitude, width,
+            os.fsencode(out_dir), u.ctypes.data, C.byref(ss), C.byref(io)))
+        return u, ss.value, io.value
 
     def select_params(self, norm, tol):
         s, m = C.c_int(), C.c_int()

@@ -21,6 +21,7 @@
 #include "gliosim/pipeline.hpp"
 #include "gliosim/sparse.hpp"
 #include "gliosim/stencil.hpp"
+#include "gliosim/vtk.hpp"
 
 namespace {
 
@@ -234,6 +235,136 @@ int ref_stencil_step(int nx, int ny, int nz, double h, const double* d, const do
         gliosim::SparseOperator a = gliosim::assemble_diffusion(field(nx, ny, nz, h, d));
         std::vector<double> r = gliosim::step(a, std::vector<double>(u, u + a.dim()), rho, tau, tol, workers);
         std::memcpy(out, r.data(), sizeof(double) * r.size());
+    });
+}
+
+// ---- file formats (vtk.cpp, imaging.cpp, pipeline.cpp) ------------------------------
+int ref_write_vtk(const char* path, const double* u, int nx, int ny, int nz, double h, const double* origin,
+                  const uint8_t* labels) {
+    return guard([&] {
+        gliosim::Grid g(nx, ny, nz, h, {origin[0], origin[1], origin[2]});
+        gliosim::ScalarField f{g, std::vector<double>(u, u + g.num_points())};
+        if (labels) {
+            gliosim::MaterialVolume mv(g);
+            for (size_t v = 0; v < mv.labels.size(); ++v) mv.labels[v] = static_cast<gliosim::Material>(labels[v]);
+            gliosim::write_vtk(f, path, &mv);
+        } else {
+            gliosim::write_vtk(f, path);
+        }
+    });
+}
+
+// values == NULL: header only
+int ref_read_vtk(const char* path, int* dims, double* h, double* origin, double* values, int64_t capacity) {
+    return guard([&] {
+        gliosim::ScalarField f = gliosim::read_vtk(path);
+        dims[0] = f.grid.nx;
+        dims[1] = f.grid.ny;
+        dims[2] = f.grid.nz;
+        *h = f.grid.h;
+        for (int a = 0; a < 3; ++a) origin[a] = f.grid.origin[a];
+        if (values) {
+            if (capacity < static_cast<int64_t>(f.values.size())) throw std::invalid_argument("capacity");
+            std::memcpy(values, f.values.data(), sizeof(double) * f.values.size());
+        }
+    });
+}
+
+int ref_write_metrics_csv(const char* path, int count, const int* step, const double* time, const double* m4) {
+    return guard([&] {
+        std::vector<gliosim::StepMetrics> s(static_cast<size_t>(count));
+        for (int i = 0; i < count; ++i) {
+            s[i].step = step[i];
+            s[i].time = time[i];
+            s[i].total_mass = m4[4 * i + 0];
+            s[i].max_density = m4[4 * i + 1];
+            s[i].min_density = m4[4 * i + 2];
+            s[i].radius = m4[4 * i + 3];
+        }
+        gliosim::write_metrics_csv(s, path);
+    });
+}
+
+int ref_load_stack(const char* const* paths, int count, int* dims, uint8_t* out, int64_t capacity) {
+    return guard([&] {
+        gliosim::ImageStack st = gliosim::load_stack(std::vector<std::string>(paths, paths + count));
+        dims[0] = st.width;
+        dims[1] = st.height;
+        dims[2] = st.num_slices;
+        if (out) {
+            if (capacity < static_cast<int64_t>(st.intensities.size())) throw std::invalid_argument("capacity");
+            std::memcpy(out, st.intensities.data(), st.intensities.size());
+        }
+    });
+}
+
+int ref_load_raw_volume(const char* path, int* dims, uint8_t* out, int64_t capacity) {
+    return guard([&] {
+        gliosim::ImageStack st = gliosim::load_raw_volume(path);
+        dims[0] = st.width;
+        dims[1] = st.height;
+        dims[2] = st.num_slices;
+        if (out) {
+            if (capacity < static_cast<int64_t>(st.intensities.size())) throw std::invalid_argument("capacity");
+            std::memcpy(out, st.intensities.data(), st.intensities.size());
+        }
+    });
+}
+
+int ref_write_label_volume(const char* path, const uint8_t* labels, int nx, int ny, int nz) {
+    return guard([&] {
+        gliosim::MaterialVolume mv(gliosim::Grid(nx, ny, nz, 1.0));
+        for (size_t v = 0; v < mv.labels.size(); ++v) mv.labels[v] = static_cast<gliosim::Material>(labels[v]);
+        gliosim::write_label_volume(mv, path);
+    });
+}
+
+int ref_read_label_volume(const char* path, int nx, int ny, int nz, uint8_t* labels) {
+    return guard([&] {
+        gliosim::MaterialVolume mv = gliosim::read_label_volume(path, gliosim::Grid(nx, ny, nz, 1.0));
+        for (size_t v = 0; v < mv.labels.size(); ++v) labels[v] = static_cast<uint8_t>(mv.labels[v]);
+    });
+}
+
+int ref_matter_fractions(const uint8_t* labels, int nx, int ny, int nz, double* white, double* gray) {
+    return guard([&] {
+        gliosim::MaterialVolume mv(gliosim::Grid(nx, ny, nz, 1.0));
+        for (size_t v = 0; v < mv.labels.size(); ++v) mv.labels[v] = static_cast<gliosim::Material>(labels[v]);
+        const gliosim::MatterFractions f = gliosim::matter_fractions(mv);
+        *white = f.white;
+        *gray = f.gray;
+    });
+}
+
+// run_to_directory (pipeline.cpp:30-53) with a DiffusionField d and optional labels.
+// io_seconds: the reference's RunTimings::io_seconds (snapshot + csv time).
+int ref_run_to_directory(int nx, int ny, int nz, double h, const double* d, const uint8_t* labels, int n_steps,
+                         int snapshot_every, double rho, double t0, double t_end, double tol, const double* center,
+                         double amplitude, double width, const char* out_dir, double* u_out, double* step_seconds,
+                         double* io_seconds) {
+    return guard([&] {
+        gliosim::SimConfig cfg;
+        cfg.nx = nx;
+        cfg.ny = ny;
+        cfg.nz = nz;
+        cfg.h = h;
+        cfg.rho = rho;
+        cfg.t0 = t0;
+        cfg.t_end = t_end;
+        cfg.num_steps = n_steps;
+        cfg.snapshot_every = snapshot_every;
+        cfg.exp_tol = tol;
+        cfg.seed_center = {center[0], center[1], center[2]};
+        cfg.seed_amplitude = amplitude;
+        cfg.seed_width = width;
+        gliosim::DiffusionField f = field(nx, ny, nz, h, d);
+        gliosim::MaterialVolume mv(f.grid);
+        if (labels)
+            for (size_t v = 0; v < mv.labels.size(); ++v) mv.labels[v] = static_cast<gliosim::Material>(labels[v]);
+        gliosim::RunResult r = gliosim::run_to_directory(cfg, f, labels ? &mv : nullptr, out_dir);
+        if (u_out) std::memcpy(u_out, r.u.data(), sizeof(double) * r.u.size());
+        if (step_seconds) *step_seconds = r.timings.step_seconds;
+        if (io_seconds) *io_seconds = r.timings.io_seconds;
     });
 }
 

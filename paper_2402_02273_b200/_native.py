@@ -52,6 +52,9 @@ EXPORTS = [
     "gs_one_norm", "gs_apply", "gs_set_state", "gs_get_state", "gs_state_device_ptr",
     "gs_select_params", "gs_expmv", "gs_phi1v", "gs_step", "gs_step_host", "gs_run", "gs_seed_initial",
     "gs_set_trace", "gs_get_trace", "gs_set_kernel_timing", "gs_get_kernel_times",
+    "gs_write_vtk", "gs_read_vtk", "gs_write_metrics_csv", "gs_snapshot_vtk", "gs_snapshot_flush",
+    "gs_load_stack", "gs_load_raw_volume", "gs_write_label_volume", "gs_read_label_volume",
+    "gs_matter_fractions",
 ]
 
 
@@ -104,6 +107,18 @@ def load(path: str | None = None):
         L.gs_set_kernel_timing.argtypes = [vp, C.c_int]
         L.gs_get_kernel_times.argtypes = [vp, np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS"),
                                           np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")]
+    if hasattr(L, "gs_write_vtk"):  # file formats (vtk.cpp, imaging.cpp)
+        cp, ip, i64 = C.c_char_p, C.POINTER(C.c_int), C.c_int64
+        L.gs_write_vtk.argtypes = [cp, _dp, C.c_int, C.c_int, C.c_int, C.c_double, _d3, vp, C.c_int]
+        L.gs_read_vtk.argtypes = [cp, ip, _d3, _d3, vp, i64, C.c_int]
+        L.gs_write_metrics_csv.argtypes = [cp, C.c_int, vp, vp, vp]
+        L.gs_snapshot_vtk.argtypes = [vp, cp, _d3, vp]
+        L.gs_snapshot_flush.argtypes = [vp]
+        L.gs_load_stack.argtypes = [C.POINTER(cp), C.c_int, ip, ip, ip, vp, i64]
+        L.gs_load_raw_volume.argtypes = [cp, ip, ip, ip, vp, i64]
+        L.gs_write_label_volume.argtypes = [cp, _u8p, C.c_int, C.c_int, C.c_int]
+        L.gs_read_label_volume.argtypes = [cp, C.c_int, C.c_int, C.c_int, _u8p]
+        L.gs_matter_fractions.argtypes = [vp, _d3, _d3]
     for name in EXPORTS:
         if name not in ("gs_destroy", "gs_last_error", "gs_num_points", "gs_stream", "gs_state_device_ptr") \
                 and hasattr(L, name):

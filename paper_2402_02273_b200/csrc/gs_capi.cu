@@ -11,13 +11,18 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gliosim_b200.h"
+#include "gs_io.hpp"
 #include "gs_kernels.cuh"
 
 namespace {
@@ -45,7 +50,30 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
+// Asynchronous snapshot sink (gs_snapshot_vtk): a device copy of the state per slot, a
+// pinned host copy landed by the side stream, and one writer thread per context.
+constexpr int kSnapSlots = 3;
+
+struct SnapSlot {
+    DevBuf dev;
+    double* host = nullptr;      // pinned
+    cudaEvent_t ready = nullptr; // host copy complete
+    bool busy = false;
+};
+
+struct SnapJob {
+    int slot = 0;
+    std::FILE* f = nullptr;
+    std::string path;
+    double origin[3] = {0, 0, 0};
+    std::vector<uint8_t> labels;
+};
+
 }  // namespace
+
+namespace gsio {
+void set_free_error(const std::string& msg) { g_create_error = msg; }
+}  // namespace gsio
 
 struct gs_ctx {
     int device = 0;
@@ -89,6 +117,18 @@ struct gs_ctx {
     DevBuf trace;
     std::vector<uint64_t> trace_host;
     std::string err;
+
+    // snapshot pipeline
+    SnapSlot snap[kSnapSlots];
+    cudaStream_t snap_stream = nullptr;
+    cudaEvent_t snap_after = nullptr;
+    std::thread snap_thread;
+    std::mutex snap_mu;
+    std::condition_variable snap_cv;
+    std::deque<SnapJob> snap_q;
+    bool snap_stop = false;
+    gs_status snap_code = GS_OK;
+    std::string snap_err;
 };
 
 namespace {
@@ -546,6 +586,21 @@ gs_status gs_create_csr(gs_ctx** out, int64_t dim, const int64_t* offs, const in
 void gs_destroy(gs_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->snap_thread.joinable()) {
+        {
+            std::lock_guard<std::mutex> lk(c->snap_mu);
+            c->snap_stop = true;
+        }
+        c->snap_cv.notify_all();
+        c->snap_thread.join();
+    }
+    for (SnapSlot& s : c->snap) {
+        s.dev.release();
+        if (s.host) cudaFreeHost(s.host);
+        if (s.ready) cudaEventDestroy(s.ready);
+    }
+    if (c->snap_after) cudaEventDestroy(c->snap_after);
+    if (c->snap_stream) cudaStreamDestroy(c->snap_stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->csr_offs, &c->csr_cols, &c->csr_vals, &c->csc_offs, &c->csc_abs})
         b->release();
@@ -887,6 +942,147 @@ gs_status gs_get_trace(gs_ctx* c, uint64_t* pairs, int capacity, int* count) {
         ++n;
     }
     *count = n;
+    return GS_OK;
+}
+
+gs_status gs_snapshot_vtk(gs_ctx* c, const char* path, const double origin[3], const uint8_t* labels) {
+    if (!c || !path || !origin) return fail(c, GS_EINVAL, "gs_snapshot_vtk: null argument");
+    cudaSetDevice(c->device);
+    // open now so an unwritable path fails at this snapshot, as write_vtk does (vtk.cpp:66-68)
+    std::FILE* f = std::fopen(path, "w");
+    if (!f) return fail(c, GS_EDATA, std::string("cannot open ") + path + " for writing");
+    int slot = -1;
+    {
+        std::unique_lock<std::mutex> lk(c->snap_mu);
+        c->snap_cv.wait(lk, [&] {
+            if (c->snap_code != GS_OK) return true;
+            for (int s = 0; s < kSnapSlots; ++s)
+                if (!c->snap[s].busy) return true;
+            return false;
+        });
+        if (c->snap_code != GS_OK) {  // an earlier snapshot failed: report it here
+            std::fclose(f);
+            const gs_status code = c->snap_code;
+            c->snap_code = GS_OK;
+            return fail(c, code, c->snap_err);
+        }
+        for (int s = 0; s < kSnapSlots && slot < 0; ++s)
+            if (!c->snap[s].busy) slot = s;
+        c->snap[slot].busy = true;
+    }
+    SnapSlot& sl = c->snap[slot];
+    const size_t bytes = sizeof(double) * static_cast<size_t>(c->n);
+    auto release = [&](cudaError_t e, const char* where) {
+        std::fclose(f);
+        {
+            std::lock_guard<std::mutex> lk(c->snap_mu);
+            sl.busy = false;
+        }
+        return cuda_fail(c, e, where);
+    };
+    cudaError_t e = cudaSuccess;
+    if (!c->snap_stream) e = cudaStreamCreateWithFlags(&c->snap_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess && !c->snap_after) e = cudaEventCreateWithFlags(&c->snap_after, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = sl.dev.alloc(bytes);
+    if (e == cudaSuccess && !sl.host) e = cudaMallocHost(&sl.host, bytes);
+    if (e == cudaSuccess && !sl.ready) e = cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming);
+    if (e != cudaSuccess) return release(e, "gs_snapshot_vtk: allocation");
+    // device copy on the compute stream (the next step may overwrite u), then the side
+    // stream brings it to pinned host memory while the next steps run
+    e = cudaMemcpyAsync(sl.dev.p, c->u.p, bytes, cudaMemcpyDeviceToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(c->snap_after, c->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->snap_stream, c->snap_after, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sl.host, sl.dev.p, bytes, cudaMemcpyDeviceToHost, c->snap_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(sl.ready, c->snap_stream);
+    if (e != cudaSuccess) return release(e, "gs_snapshot_vtk: copy");
+
+    SnapJob job;
+    job.slot = slot;
+    job.f = f;
+    job.path = path;
+    std::copy(origin, origin + 3, job.origin);
+    if (labels) job.labels.assign(labels, labels + c->n);
+    {
+        std::lock_guard<std::mutex> lk(c->snap_mu);
+        c->snap_q.push_back(std::move(job));
+        if (!c->snap_thread.joinable()) {
+            c->snap_thread = std::thread([c] {
+                cudaSetDevice(c->device);
+                for (;;) {
+                    SnapJob j;
+                    {
+                        std::unique_lock<std::mutex> lk(c->snap_mu);
+                        c->snap_cv.wait(lk, [&] { return c->snap_stop || !c->snap_q.empty(); });
+                        if (c->snap_q.empty()) return;  // stop requested and nothing left
+                        j = std::move(c->snap_q.front());
+                        c->snap_q.pop_front();
+                    }
+                    SnapSlot& s = c->snap[j.slot];
+                    gsio::Error err;
+                    const cudaError_t ce = cudaEventSynchronize(s.ready);
+                    bool ok = ce == cudaSuccess;
+                    if (!ok) err = {GS_ECUDA, std::string("gs_snapshot_vtk: ") + cudaGetErrorString(ce)};
+                    ok = ok && gsio::write_vtk_stream(j.f, j.path, s.host, c->nx, c->ny, c->nz, c->h, j.origin,
+                                                      j.labels.empty() ? nullptr : j.labels.data(), 0, err);
+                    if (std::fclose(j.f) != 0 && ok) {
+                        ok = false;
+                        err = {GS_EDATA, "write failed: " + j.path};
+                    }
+                    {
+                        std::lock_guard<std::mutex> lk(c->snap_mu);
+                        s.busy = false;
+                        if (!ok && c->snap_code == GS_OK) {
+                            c->snap_code = static_cast<gs_status>(err.code);
+                            c->snap_err = err.msg;
+                        }
+                    }
+                    c->snap_cv.notify_all();
+                }
+            });
+        }
+    }
+    c->snap_cv.notify_all();
+    return GS_OK;
+}
+
+gs_status gs_snapshot_flush(gs_ctx* c) {
+    if (!c) return fail(c, GS_EINVAL, "gs_snapshot_flush: null argument");
+    std::unique_lock<std::mutex> lk(c->snap_mu);
+    c->snap_cv.wait(lk, [&] {
+        if (!c->snap_q.empty()) return false;
+        for (const SnapSlot& s : c->snap)
+            if (s.busy) return false;
+        return true;
+    });
+    if (c->snap_code != GS_OK) {
+        const gs_status code = c->snap_code;
+        c->snap_code = GS_OK;
+        c->err = c->snap_err;
+        return code;
+    }
+    return GS_OK;
+}
+
+gs_status gs_matter_fractions(gs_ctx* c, double* white, double* gray) {
+    if (!c || !white || !gray) return fail(c, GS_EINVAL, "gs_matter_fractions: null argument");
+    if (!c->has_labels) return fail(c, GS_EINVAL, "gs_matter_fractions: operator was not built from material labels");
+    cudaSetDevice(c->device);
+    DevBuf cnt;
+    GS_CUDA(c, cnt.alloc(4 * sizeof(unsigned long long)));
+    GS_CUDA(c, cudaMemsetAsync(cnt.p, 0, 4 * sizeof(unsigned long long), c->stream));
+    const int blocks = std::max(1, static_cast<int>(std::min<int64_t>((c->n / 16 + 255) / 256, c->num_sms * 8)));
+    gs::label_count_kernel<<<blocks, 256, 0, c->stream>>>(c->pal.as<uint8_t>(), c->n,
+                                                          cnt.as<unsigned long long>());
+    GS_CUDA(c, cudaGetLastError());
+    unsigned long long h[4];
+    GS_CUDA(c, cudaMemcpyAsync(h, cnt.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    GS_CUDA(c, cudaStreamSynchronize(c->stream));
+    cnt.release();
+    const int64_t w = static_cast<int64_t>(h[1]), g = static_cast<int64_t>(h[2]);
+    const int64_t tissue = w + g;
+    if (tissue == 0) return fail(c, GS_EDATA, "matter_fractions: volume contains no tissue voxels");
+    *white = static_cast<double>(w) / tissue;  // imaging.cpp:163
+    *gray = static_cast<double>(g) / tissue;
     return GS_OK;
 }
 

@@ -58,6 +58,39 @@ __global__ void expand_palette_kernel(const uint8_t* __restrict__ pal, const dou
         d[v] = dtab[pal[v]];
 }
 
+// matter_fractions (imaging.cpp:155-164): per-label voxel counts.  16 B loads, per-thread
+// register counters, a warp shuffle reduction and one atomic per warp and label.
+__global__ void label_count_kernel(const uint8_t* __restrict__ labels, int64_t n,
+                                   unsigned long long* __restrict__ counts) {
+    unsigned long long c[4] = {0, 0, 0, 0};
+    const int64_t n16 = n / 16;
+    const uint4* v16 = reinterpret_cast<const uint4*>(labels);
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n16;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint4 w = __ldg(v16 + q);
+        const uint32_t word[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t lab = (word[k] >> (8 * b)) & 0xffu;
+                if (lab < 4) ++c[lab];
+            }
+    }
+    for (int64_t v = n16 * 16 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint8_t lab = labels[v];
+        if (lab < 4) ++c[lab];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        unsigned long long x = c[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) == 0 && x) atomicAdd(counts + k, x);
+    }
+}
+
 // ----------------------------------------------------------------------------------
 // K3 exact 1-norm: column c sums |a_rc| over rows r = c-sz, c-sy, c-1, c, c+1, c+sy, c+sz
 // in ascending r -- the CSR storage order the reference's constructor walks

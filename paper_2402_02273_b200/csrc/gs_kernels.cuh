@@ -115,6 +115,7 @@ __global__ void csc_norm_kernel(int64_t n, const int64_t* csc_offs, const double
                                 unsigned long long* out_bits);
 // Per-voxel D(x) reconstruction (for gs_get_diffusion in palette mode)
 __global__ void expand_palette_kernel(const uint8_t* pal, const double* dtab, int64_t n, double* d);
+__global__ void label_count_kernel(const uint8_t* labels, int64_t n, unsigned long long* counts);
 // The exponential-Euler step as a launch sequence (gs_solve.cu):
 //   [metrics_kernel] -> per step: prep_kernel -> border_kernel -> taylor_kernel (cooperative) -> update_kernel
 __global__ void metrics_kernel(const __grid_constant__ SolveParams p);

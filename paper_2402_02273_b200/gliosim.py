@@ -23,6 +23,7 @@ on the CPU beyond argument checks and the libm-parity seed (done in the library)
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -195,7 +196,7 @@ class StencilOperator:
         h = C.c_void_p()
         rc = self.lib.gs_create(C.byref(h), grid.nx, grid.ny, grid.nz, float(grid.h), device)
         if rc != N.GS_OK:
-            _raise(rc, self.lib.gs_last_error(None).decode())
+            _raise(rc, self.lib.gs_last_error(None).decode("utf-8", "surrogateescape"))
         self.ctx = h
 
     # -- lifetime ----------------------------------------------------------------------
@@ -218,7 +219,7 @@ class StencilOperator:
 
     def _check(self, rc):
         if rc != N.GS_OK:
-            _raise(rc, self.lib.gs_last_error(self.ctx).decode())
+            _raise(rc, self.lib.gs_last_error(self.ctx).decode("utf-8", "surrogateescape"))
 
     # -- construction -------------------------------------------------------------------
     @classmethod
@@ -311,6 +312,19 @@ class StencilOperator:
         self._check(self.lib.gs_get_kernel_times(self.ctx, ms, n))
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(["prep", "border", "taylor", "update"])}
 
+    def snapshot_vtk(self, path, labels=None):
+        """Queue the resident state as a VTK snapshot (gs_snapshot_vtk): device copy now,
+        host copy on a side stream, formatting on a writer thread.  Errors of earlier
+        snapshots surface here or in flush_snapshots()."""
+        lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.uint8).ravel()
+        if lab is not None and lab.size != self.dim():
+            raise ValueError("write_vtk: material volume does not match the field grid")
+        self._check(self.lib.gs_snapshot_vtk(self.ctx, os.fsencode(path), N.d3(self.grid.origin),
+                                             lab.ctypes.data if lab is not None else None))
+
+    def flush_snapshots(self):
+        self._check(self.lib.gs_snapshot_flush(self.ctx))
+
     def step_resident(self, rho, tau, tol, info=True):
         inf = N.GsStepInfo() if info else None
         self._check(self.lib.gs_step(self.ctx, rho, tau, tol, C.byref(inf) if inf is not None else None))
@@ -341,7 +355,7 @@ class CsrOperator(StencilOperator):
         h = C.c_void_p()
         rc = self.lib.gs_create_csr(C.byref(h), n, offs, cols, vals, device)
         if rc != N.GS_OK:
-            _raise(rc, self.lib.gs_last_error(None).decode())
+            _raise(rc, self.lib.gs_last_error(None).decode("utf-8", "surrogateescape"))
         self.ctx = h
 
 
@@ -386,7 +400,7 @@ def select_params(norm_tA: float, tol: float):
     s, m = C.c_int(), C.c_int()
     rc = lib.gs_select_params(norm_tA, tol, C.byref(s), C.byref(m))
     if rc != N.GS_OK:
-        _raise(rc, lib.gs_last_error(None).decode())
+        _raise(rc, lib.gs_last_error(None).decode("utf-8", "surrogateescape"))
     return s.value, m.value
 
 
@@ -423,18 +437,22 @@ def step(a: StencilOperator, u, rho: float, tau: float, tol: float, info: bool =
 
 
 def seed_initial(a: StencilOperator, cfg: SimConfig, mask: bool = True) -> np.ndarray:
-    """integrator.cpp:32-50 (host libm, bit-identical to the reference)."""
+    """integrator.cpp:32-50 (host libm, bit-identical to the reference); lattice points are
+    placed by the operator's grid (grid.point, grid.hpp:35-37), as seed_initial(d, cfg) does."""
     u = np.empty(a.dim(), dtype=np.float64)
-    a._check(a.lib.gs_seed_initial(a.ctx, N.d3(cfg.origin), cfg.seed_amplitude, cfg.seed_width,
+    a._check(a.lib.gs_seed_initial(a.ctx, N.d3(a.grid.origin), cfg.seed_amplitude, cfg.seed_width,
                                    N.d3(cfg.seed_center), 1 if mask else 0, u))
     return u
 
 
 def run(cfg: SimConfig, a: StencilOperator, u0, snapshot=None, on_range=None, on_step=None,
-        with_infos: bool = False) -> RunResult:
+        with_infos: bool = False, _vtk=None) -> RunResult:
     """integrator.cpp:91-138: the time loop runs on the GPU as one launch per segment
     between snapshots; metrics are computed on the device at every node, then the
-    hooks fire in order with the reference's arguments."""
+    hooks fire in order with the reference's arguments.
+
+    _vtk = (out_dir, labels or None) is run_to_directory's sink (pipeline.cpp:39-45):
+    snapshot_NNNN.vtk files written asynchronously by the native library."""
     cfg.validate()
     grid = a.grid
     u0 = np.ascontiguousarray(u0, dtype=np.float64)
@@ -444,10 +462,19 @@ def run(cfg: SimConfig, a: StencilOperator, u0, snapshot=None, on_range=None, on
     a.set_state(u0)
     tau = cfg.tau()
     # snapshot nodes: 0, every snapshot_every, and the last (integrator.cpp:112, :135-136)
+    sinks = snapshot is not None or _vtk is not None
     cuts = [n for n in range(1, cfg.num_steps + 1) if n % cfg.snapshot_every == 0 or n == cfg.num_steps] \
-        if snapshot else [cfg.num_steps]
-    if snapshot:
-        snapshot(0, time_at(cfg, 0), u0.copy())
+        if sinks else [cfg.num_steps]
+
+    def emit(n):
+        tic = time.perf_counter()
+        if snapshot:
+            snapshot(n, time_at(cfg, n), a.get_state())
+        if _vtk is not None:
+            a.snapshot_vtk(os.path.join(_vtk[0], "snapshot_%04d.vtk" % n), _vtk[1])
+        res.timings.io_seconds += time.perf_counter() - tic
+
+    emit(0)
     done = 0
     all_metrics = []
     for cut in cuts:
@@ -472,8 +499,19 @@ def run(cfg: SimConfig, a: StencilOperator, u0, snapshot=None, on_range=None, on
         if with_infos:
             res.infos.extend(inf[q].as_dict() for q in range(k))
         done = cut
-        if snapshot:
-            snapshot(cut, time_at(cfg, cut), a.get_state())
+        if sinks:
+            emit(cut)
+    if _vtk is not None:
+        tic = time.perf_counter()
+        a._check(a.lib.gs_snapshot_flush(a.ctx))
+        res.timings.io_seconds += time.perf_counter() - tic
     res.metrics = all_metrics
     res.u = a.get_state()
     return res
+
+
+# file formats and run_to_directory (vtk.cpp, imaging.cpp, pipeline.cpp)
+from .fileio import (DiffusionField, ImageStack, MaterialVolume, ScalarField, load_raw_volume,  # noqa: E402,F401
+                     load_stack, matter_fractions, read_label_volume, read_vtk, run_to_directory,
+                     stencil_from_stack, uniform_diffusion, uniform_labels, write_label_volume,
+                     write_metrics_csv, write_vtk)

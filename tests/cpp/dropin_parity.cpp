@@ -8,13 +8,19 @@
 // order-free metrics (max, min, radius) to 1e-12; step() / phi1v() / expmv() / apply() too.
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <sstream>
+#include <string>
 #include <vector>
 
 #include "gliosim/config.hpp"
 #include "gliosim/expact.hpp"
 #include "gliosim/fields.hpp"
 #include "gliosim/integrator.hpp"
+#include "gliosim/pipeline.hpp"
 #include "gliosim/stencil.hpp"
+#include "gliosim/vtk.hpp"
 #include "gliosim_b200.hpp"
 
 static double rel_l2(const std::vector<double>& a, const std::vector<double>& b) {
@@ -24,6 +30,13 @@ static double rel_l2(const std::vector<double>& a, const std::vector<double>& b)
         den += b[i] * b[i];
     }
     return std::sqrt(num / (den > 0 ? den : 1.0));
+}
+
+static std::string slurp(const std::string& p) {
+    std::ifstream in(p, std::ios::binary);
+    std::ostringstream ss;
+    ss << in.rdbuf();
+    return ss.str();
 }
 
 int main() {
@@ -96,6 +109,52 @@ int main() {
         threw = true;
     }
     gate(threw, "phi1v length mismatch -> std::invalid_argument", 0.0);
+
+    // run_to_directory (pipeline.hpp:18-24) with labels: the same files, read back by the
+    // reference's own reader; the GPU's files re-written by the reference's writer are
+    // byte-identical (formatting parity), and the states agree with the reference run.
+    gliosim::MaterialVolume mv(cfg.grid());
+    for (size_t v = 0; v < mv.labels.size(); ++v)
+        mv.labels[v] = d.d[v] == cfg.d_white ? gliosim::Material::WhiteMatter
+                       : d.d[v] == cfg.d_gray ? gliosim::Material::GrayMatter : gliosim::Material::Air;
+    const std::string tmp = std::filesystem::temp_directory_path().string();
+    const std::string dir_ref = tmp + "/gs_dropin_ref", dir_gpu = tmp + "/gs_dropin_gpu";
+    std::filesystem::remove_all(dir_ref);
+    std::filesystem::remove_all(dir_gpu);
+    const gliosim::RunResult rr = gliosim::run_to_directory(cfg, d, &mv, dir_ref);
+    int gpu_steps = 0;
+    const gliosim_b200::RunResult rg =
+        gliosim_b200::run_to_directory(cfg, d, &mv, dir_gpu, 1, [&](const gliosim_b200::StepMetrics&) { ++gpu_steps; });
+    gate(gpu_steps == cfg.num_steps, "run_to_directory: step watcher calls", gpu_steps);
+    bool files_ok = true, bytes_ok = true;
+    double worst_snap = 0.0;
+    for (int k = 0; k <= cfg.num_steps; ++k) {
+        char name[32];
+        std::snprintf(name, sizeof name, "/snapshot_%04d.vtk", k);
+        const bool want = k % cfg.snapshot_every == 0 || k == cfg.num_steps;
+        const bool a_has = std::filesystem::exists(dir_ref + name), b_has = std::filesystem::exists(dir_gpu + name);
+        files_ok = files_ok && a_has == want && b_has == want;
+        if (!want || !a_has || !b_has) continue;
+        const gliosim::ScalarField fa = gliosim::read_vtk(dir_ref + name);
+        const gliosim::ScalarField fb = gliosim::read_vtk(dir_gpu + name);
+        worst_snap = std::fmax(worst_snap, rel_l2(fb.values, fa.values));
+        gliosim::write_vtk(fb, dir_gpu + "/rewrite.vtk", &mv);
+        bytes_ok = bytes_ok && slurp(dir_gpu + "/rewrite.vtk") == slurp(dir_gpu + name);
+        const auto fc = gliosim_b200::read_vtk<gliosim::ScalarField>(dir_gpu + name);
+        bytes_ok = bytes_ok && fc.values == fb.values && fc.grid.h == fb.grid.h;
+    }
+    gate(files_ok, "run_to_directory: snapshot files at the reference's nodes", 0.0);
+    gate(bytes_ok, "run_to_directory: snapshot bytes == reference write_vtk of the same state", 0.0);
+    gate(worst_snap <= 1e-8, "run_to_directory: snapshots vs reference rel L2", worst_snap);
+    gate(rg.u == gliosim::read_vtk(dir_gpu + "/snapshot_0012.vtk").values, "run_to_directory: last file == u", 0.0);
+    std::vector<gliosim::StepMetrics> gm;
+    for (const auto& m : rg.metrics) gm.push_back({m.step, m.time, m.total_mass, m.max_density, m.min_density, m.radius});
+    gliosim::write_metrics_csv(gm, dir_gpu + "/metrics_ref.csv");
+    gate(slurp(dir_gpu + "/metrics_ref.csv") == slurp(dir_gpu + "/metrics.csv"), "metrics.csv bytes", 0.0);
+    gate(rr.metrics.size() == rg.metrics.size(), "run_to_directory: metrics rows", 0.0);
+    std::filesystem::remove_all(dir_ref);
+    std::filesystem::remove_all(dir_gpu);
+
     std::printf("%s\n", fails ? "dropin parity: FAILED" : "dropin parity: all passed");
     return fails ? 1 : 0;
 }
