@@ -69,11 +69,15 @@ def main():
         t = time.perf_counter()
         G.write_vtk(G.ScalarField(grid, state), os.path.join(tmp, "one.vtk"), labels)
         native = time.perf_counter() - t
+        t = time.perf_counter()
+        G.write_vtk(G.ScalarField(grid, state), "/dev/null", labels)  # formatting alone, no file system
+        fmt_only = time.perf_counter() - t
         line = {"bench": "snapshot_io", "workload": "C4 256^3, 4 steps, snapshot_every 2 (3 snapshots + csv)",
                 "run_s": round(plain, 4), "run_to_directory_s": round(with_io, 4),
                 "exposed_s_per_snapshot": round((with_io - plain) / 3, 4),
                 "snapshot_bytes": size, "native_write_vtk_s": round(native, 4),
-                "native_values_per_s": round(w.n / native, 1), "host_threads": os.cpu_count()}
+                "native_values_per_s": round(w.n / native, 1), "format_only_s": round(fmt_only, 4),
+                "host_threads": os.cpu_count()}
         if ref is not None:
             t = time.perf_counter()
             ref.write_vtk(os.path.join(tmp, "ref.vtk"), state, (w.nx, w.ny, w.nz), w.h, (0.0, 0.0, 0.0), labels)
