@@ -54,6 +54,9 @@ struct DevBuf {
 // pinned host copy landed by the side stream, and one writer thread per context.
 constexpr int kSnapSlots = 3;
 
+// Taylor terms per fused TMA sweep (2 or 3); GS_FUSE overrides it per launch.
+constexpr int kDefaultFuse = 2;
+
 struct SnapSlot {
     DevBuf dev;
     double* host = nullptr;      // pinned
@@ -108,7 +111,9 @@ struct gs_ctx {
     CUtensorMap xmap[gs::kNumBufs];
     CUtensorMap omap[gs::kNumBufs];
     CUtensorMap x2map[gs::kNumBufs];
-    CUtensorMap lmap, l2map;
+    CUtensorMap x3map[gs::kNumBufs];
+    CUtensorMap b3map;
+    CUtensorMap lmap, l2map, l3map;
     int trace_cap = 0;
     bool ktime = false;
     double kms[4] = {0, 0, 0, 0};
@@ -202,6 +207,9 @@ gs_status build_tensor_maps(gs_ctx* c) {
     const cuuint32_t own[3] = {gs::kTmaTX, gs::kTmaTY, 1};
     const cuuint32_t halo2[3] = {gs::kXPitch, gs::k2XRows, 1};
     const cuuint32_t lhalo[3] = {gs::kLPitch, gs::kTmaTY + 2, 1};
+    const cuuint32_t halo3[3] = {gs::k3XPitch, gs::k3XRows, 1};
+    const cuuint32_t bhalo3[3] = {gs::k3XPitch, gs::k3BRows, 1};
+    const cuuint32_t lhalo3[3] = {gs::kLPitch, gs::k3LRows, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     DevBuf* bufs[gs::kNumBufs] = {&c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out};
     for (int b = 0; b < gs::kNumBufs; ++b) {
@@ -217,7 +225,19 @@ gs_status build_tensor_maps(gs_ctx* c) {
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(halo2) failed: " + std::to_string(r));
+        r = encode(&c->x3map[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, bufs[b]->p, dims, st8, halo3, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(halo3) failed: " + std::to_string(r));
     }
+    CUresult rb = encode(&c->b3map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->g.p, dims, st8, bhalo3, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rb != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(b halo3) failed: " + std::to_string(rb));
+    rb = encode(&c->l3map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, c->pal.p, dims, st1, lhalo3, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rb != CUDA_SUCCESS) return fail(c, GS_ECUDA, "cuTensorMapEncodeTiled(labels halo3) failed: " + std::to_string(rb));
     CUresult r = encode(&c->lmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, c->pal.p, dims, st1, own, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -318,10 +338,10 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     GS_CUDA(c, c->part_b.alloc(sizeof(double) * pb));
     GS_CUDA(c, c->part_c.alloc(sizeof(double) * pb));
     GS_CUDA(c, c->part_u.alloc(sizeof(double) * pb));
-    GS_CUDA(c, c->slots.alloc(sizeof(unsigned long long) * 12));
+    GS_CUDA(c, c->slots.alloc(sizeof(unsigned long long) * 24));
     GS_CUDA(c, c->mslots.alloc(sizeof(unsigned long long) * 4));
     GS_CUDA(c, c->ctrl.alloc(sizeof(gs::Ctrl)));
-    GS_CUDA(c, cudaMemsetAsync(c->slots.p, 0, sizeof(unsigned long long) * 12, c->stream));
+    GS_CUDA(c, cudaMemsetAsync(c->slots.p, 0, sizeof(unsigned long long) * 24, c->stream));
     const unsigned long long ms_init[4] = {0ull, ~0ull, 0ull, 0ull};
     GS_CUDA(c, cudaMemcpyAsync(c->mslots.p, ms_init, sizeof ms_init, cudaMemcpyHostToDevice, c->stream));
     GS_CUDA(c, cudaMemsetAsync(c->ctrl.p, 0, sizeof(gs::Ctrl), c->stream));
@@ -339,10 +359,16 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             p.xmap[b] = c->xmap[b];
             p.omap[b] = c->omap[b];
             p.x2map[b] = c->x2map[b];
+            p.x3map[b] = c->x3map[b];
         }
+        p.b3map = c->b3map;
         p.lmap = c->lmap;
         p.l2map = c->l2map;
+        p.l3map = c->l3map;
     }
+    // Taylor terms per fused sweep (GS_FUSE=2|3 overrides the default for A/B measurements)
+    p.fuse = kDefaultFuse;
+    if (const char* f = std::getenv("GS_FUSE")) p.fuse = std::atoi(f) == 3 ? 3 : 2;
     p.metrics = metrics ? c->metrics.as<double>() : nullptr;
     p.want_metrics = metrics ? 1 : 0;
     p.infos = infos ? c->infos.as<gs_step_info>() : nullptr;
@@ -405,7 +431,9 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             int border_blocks = sb;
             void* args[] = {&p, &border_blocks, &step};
             GS_CUDA(c, ev(2));
-            GS_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gs::taylor_kernel), dim3(gb), blk, args, dyn,
+            GS_CUDA(c, cudaLaunchCooperativeKernel(p.fuse == 3 ? reinterpret_cast<void*>(gs::taylor_kernel<3>)
+                                                                 : reinterpret_cast<void*>(gs::taylor_kernel<2>),
+                                                   dim3(gb), blk, args, dyn,
                                                    c->stream));
             GS_CUDA(c, ev_end());
             GS_CUDA(c, ev(3));
@@ -492,13 +520,19 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
         return GS_ECUDA;
     }
     c->num_sms = prop.multiProcessorCount;
-    for (const void* fn : {reinterpret_cast<const void*>(gs::taylor_kernel), reinterpret_cast<const void*>(gs::prep_kernel)})
+    for (const void* fn : {reinterpret_cast<const void*>(gs::taylor_kernel<2>), reinterpret_cast<const void*>(gs::taylor_kernel<3>),
+                           reinterpret_cast<const void*>(gs::prep_kernel)})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kDynSmemBytes)) != cudaSuccess)
             return bail(e, "cudaFuncSetAttribute(smem)");
     int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::taylor_kernel, gs::kSolveThreads,
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::taylor_kernel<2>, gs::kSolveThreads,
                                                            gs::kDynSmemBytes)) != cudaSuccess)
         return bail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    int per_sm3 = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, gs::taylor_kernel<3>, gs::kSolveThreads,
+                                                           gs::kDynSmemBytes)) != cudaSuccess)
+        return bail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    per_sm = std::min(per_sm, per_sm3);
     if (per_sm < 1) {
         g_create_error = "gs_create: solve kernel does not fit on an SM";
         gs_destroy(c);

@@ -55,7 +55,35 @@ constexpr int kT1Rows = kTmaTY + 2;
 constexpr int kT1Bytes = kT1Rows * kT1Pitch * 8;
 constexpr int kT1Planes = 3;  // T1(z+1) is written while T1(z-1) is read; T1(z) is kept for the next iteration
 constexpr int k2RingBytes = k2Stages * k2SlotBytes + kT1Planes * kT1Bytes + 128;
-constexpr int kDynSmemBytes = kRingBytes > k2RingBytes ? kRingBytes : k2RingBytes;
+
+// Three-term fused sweep: T_{j+1} on the tile plus a two-voxel ring (4-plane shared ring),
+// T_{j+2} on the tile plus a one-voxel ring (3-plane shared ring), T_{j+3} on the tile; the
+// input needs a three-voxel halo.  X slots (input + labels) and F/b slots are separate rings:
+// F is consumed two planes behind X, b/gamma at X's pace, and never both in one sweep.
+constexpr int k3XHaloX = 4;                                             // x0-4: 16-byte aligned start
+constexpr int k3XPitch = kTmaTX + 2 * k3XHaloX;                         // 72
+constexpr int k3XRows = kTmaTY + 6;                                     // y halo 3
+constexpr int k3XBytes = (k3XRows * k3XPitch * 8 + 127) / 128 * 128;    // 22 x 72 doubles
+constexpr int k3LRows = kTmaTY + 4;                                     // labels, y halo 2
+constexpr int k3LBytes = (k3LRows * kLPitch + 127) / 128 * 128;         // 20 x 96 labels
+constexpr int k3XSlotBytes = k3XBytes + k3LBytes;
+constexpr int k3XStages = 7;
+constexpr int k3BRows = kTmaTY + 4;                                     // b/gamma, y halo 2
+constexpr int k3BBytes = (k3BRows * k3XPitch * 8 + 127) / 128 * 128;    // 20 x 72 doubles
+constexpr int k3FBBytes = kOBytes > k3BBytes ? kOBytes : k3BBytes;
+constexpr int k3FBStages = 3;
+constexpr int k3T1Pitch = kTmaTX + 4;
+constexpr int k3T1Rows = kTmaTY + 4;
+constexpr int k3T1Bytes = k3T1Rows * k3T1Pitch * 8;
+constexpr int k3T1Planes = 4;
+constexpr int k3T2Pitch = kTmaTX + 2;
+constexpr int k3T2Rows = kTmaTY + 2;
+constexpr int k3T2Bytes = k3T2Rows * k3T2Pitch * 8;
+constexpr int k3T2Planes = 3;
+constexpr int k3RingBytes = k3XStages * k3XSlotBytes + k3FBStages * k3FBBytes + k3T1Planes * k3T1Bytes +
+                            k3T2Planes * k3T2Bytes + 128;
+constexpr int kMaxRing = kRingBytes > k2RingBytes ? kRingBytes : k2RingBytes;
+constexpr int kDynSmemBytes = kMaxRing > k3RingBytes ? kMaxRing : k3RingBytes;
 
 // Device-resident control block shared by the kernels of one launch sequence.
 struct Ctrl {
@@ -72,10 +100,14 @@ struct SolveParams {
     CUtensorMap xmap[kNumBufs];
     CUtensorMap omap[kNumBufs];
     CUtensorMap x2map[kNumBufs];   // halo-2 boxes (fused two-term sweep)
+    CUtensorMap x3map[kNumBufs];   // halo-3 boxes (fused three-term sweep)
+    CUtensorMap b3map;             // b/gamma (buffer G) with a two-voxel halo
     CUtensorMap lmap;
     CUtensorMap l2map;             // labels with a one-voxel halo
+    CUtensorMap l3map;             // labels with a two-voxel halo
     StencilOp op;
     int use_tma;
+    int fuse;               // Taylor terms per fused TMA sweep: 2 or 3
     int mode;
     int n_steps;
     int want_metrics;
@@ -92,7 +124,7 @@ struct SolveParams {
     double* part_b;         // [grid] block partial sums of |b|
     double* part_c;         // [grid] block partial sums of |b/gamma|
     double* part_u;         // [grid] block partial sums of u (metrics)
-    unsigned long long* slots;   // [3][4] rotating max slots for per-term reductions
+    unsigned long long* slots;   // [3][8] rotating max slots for per-term reductions
     unsigned long long* mslots;  // [2][4] metric max/min/r2 slots (step parity)
     Ctrl* ctrl;
     unsigned long long* trace;  // optional phase trace: (tag, globaltimer ns) pairs
@@ -121,6 +153,7 @@ __global__ void label_count_kernel(const uint8_t* labels, int64_t n, unsigned lo
 __global__ void metrics_kernel(const __grid_constant__ SolveParams p);
 __global__ void prep_kernel(const __grid_constant__ SolveParams p, int step);
 __global__ void border_kernel(const __grid_constant__ SolveParams p, int prep_blocks, int step);
+template <int FUSE>
 __global__ void taylor_kernel(const __grid_constant__ SolveParams p, int border_blocks, int step);
 __global__ void update_kernel(const __grid_constant__ SolveParams p, int step);
 

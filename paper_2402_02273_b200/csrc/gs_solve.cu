@@ -35,10 +35,12 @@ namespace {
 
 struct Smem {
     double wtab[256];
-    double red[kSolveThreads / 32][4];
+    double red[kSolveThreads / 32][6];
     double bcast[4];
-    uint64_t bar1[kTmaStages];  // single-term ring
-    uint64_t bar2[k2Stages];    // fused two-term ring
+    uint64_t bar1[kTmaStages];   // single-term ring
+    uint64_t bar2[k2Stages];     // fused two-term ring
+    uint64_t bar3x[k3XStages];   // fused three-term ring: input + labels
+    uint64_t bar3f[k3FBStages];  // fused three-term ring: F or b/gamma
 };
 
 struct Ring {
@@ -582,6 +584,362 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
     fence_proxy_async_global();
 }
 
+// ------------------------------------------------------------------------------------------
+// Three-term fused TMA sweep (deeper temporal blocking)
+// ------------------------------------------------------------------------------------------
+// One pass over HBM computes three consecutive Taylor terms (expact.cpp:81-95 three times):
+//   A: T1 = c1 * (A~ X)   on the tile plus a two-voxel ring   (4-plane shared ring)
+//   B: T2 = c2 * (A T1)   on the tile plus a one-voxel ring   (3-plane shared ring)
+//   C: T3 = c3 * (A T2)   on the tile;  F1 = Fprev + T1, F2 = F1 + T2, F3 = F2 + T3
+// and writes T3 and F2 (F3 = F2 + T3 stays implicit; F1 is recomputed by a single-term
+// sweep in the rare case a stage stops right after T1).  Iteration z runs A on plane z+1,
+// B on plane z-1 and C on plane z-2: each reads only shared planes completed in earlier
+// iterations (z-neighbours of its own points come from registers), so there is one barrier
+// per plane.  Points outside the grid hold 0.0 in every ring (the missing neighbours).
+struct Ring3 {
+    unsigned char* base;
+    uint64_t* barx;  // [k3XStages]
+    uint64_t* barf;  // [k3FBStages]
+    __device__ double* x(int s) const { return reinterpret_cast<double*>(base + s * k3XSlotBytes); }
+    __device__ uint8_t* l(int s) const { return base + s * k3XSlotBytes + k3XBytes; }
+    __device__ double* fb(int s) const {
+        return reinterpret_cast<double*>(base + k3XStages * k3XSlotBytes + s * k3FBBytes);
+    }
+    __device__ double* t1(int q) const {
+        return reinterpret_cast<double*>(base + k3XStages * k3XSlotBytes + k3FBStages * k3FBBytes + q * k3T1Bytes);
+    }
+    __device__ double* t2(int q) const {
+        return reinterpret_cast<double*>(base + k3XStages * k3XSlotBytes + k3FBStages * k3FBBytes +
+                                         k3T1Planes * k3T1Bytes + q * k3T2Bytes);
+    }
+};
+
+template <int KIND>
+__device__ __forceinline__ void sweep3_tma(const SolveParams& p, const Ring3& ring, int xbuf, int fbuf, double c1,
+                                           double c2, double c3, double* outT, double* outF, double (&mx)[6],
+                                           uint32_t& seqx, uint32_t& seqf, uint32_t& pmx, uint32_t& pmf,
+                                           const double* s_wtab) {
+    constexpr bool needX = KIND != k2FirstZero;
+    constexpr bool needF = KIND == k2Next;
+    constexpr bool needB = KIND == k2FirstZero || KIND == k2FirstBorder;
+    constexpr uint32_t kXTx = k3XRows * k3XPitch * 8;
+    constexpr uint32_t kLTx = k3LRows * kLPitch;
+    constexpr uint32_t kBTx = k3BRows * k3XPitch * 8;
+    constexpr int kARing = 2 * (kTmaTX + 4) * 2 + 4 * kTmaTY;  // 336 points of T1's two-voxel ring
+    constexpr int kBRing = 2 * (kTmaTX + 2) + 2 * kTmaTY;      // 164 points of T2's one-voxel ring
+    static_assert(kARing + kBRing <= kSolveThreads, "ring points need one thread each");
+    const StencilOp& op = p.op;
+    const int tid = threadIdx.x;
+    const int xl = tid & (kTmaTX - 1);
+    const int ry0 = 2 * (tid / kTmaTX);
+    const int oX = (ry0 + 3) * k3XPitch + xl + k3XHaloX;
+    const int oL = (ry0 + 2) * kLPitch + xl + kLHaloX;
+    const int oB = (ry0 + 2) * k3XPitch + xl + k3XHaloX;
+    const int oT1 = (ry0 + 2) * k3T1Pitch + xl + 2;
+    const int oT2 = (ry0 + 1) * k3T2Pitch + xl + 1;
+    const int oF = ry0 * kTmaTX + xl;
+    // ring point of this thread: T1's ring for tid < 336, T2's ring for 336 <= tid < 500
+    const bool aring = tid < kARing;
+    const bool bring = !aring && tid < kARing + kBRing;
+    int rr = 0, rc = 0;
+    if (aring) {
+        if (tid < 4 * (kTmaTX + 4)) {  // rows -2, -1, 16, 17 over columns -2 .. 65
+            const int rowi = tid / (kTmaTX + 4);
+            rr = rowi < 2 ? rowi - 2 : kTmaTY + rowi - 2;
+            rc = tid % (kTmaTX + 4) - 2;
+        } else {  // columns -2, -1, 64, 65 over rows 0 .. 15
+            const int e = tid - 4 * (kTmaTX + 4);
+            rr = e >> 2;
+            const int k = e & 3;
+            rc = k < 2 ? k - 2 : kTmaTX + k - 2;
+        }
+    } else if (bring) {
+        const int b = tid - kARing;
+        if (b < 2 * (kTmaTX + 2)) {  // rows -1 and 16 over columns -1 .. 64
+            rr = b < kTmaTX + 2 ? -1 : kTmaTY;
+            rc = b % (kTmaTX + 2) - 1;
+        } else {  // columns -1 and 64 over rows 0 .. 15
+            const int e = b - 2 * (kTmaTX + 2);
+            rr = e >> 1;
+            rc = (e & 1) ? kTmaTX : -1;
+        }
+    }
+    const int aX = (rr + 3) * k3XPitch + rc + k3XHaloX;
+    const int aL = (rr + 2) * kLPitch + rc + kLHaloX;
+    const int aB = (rr + 2) * k3XPitch + rc + k3XHaloX;
+    const int aT1 = (rr + 2) * k3T1Pitch + rc + 2;
+    const int aT2 = (rr + 1) * k3T2Pitch + rc + 1;
+
+    const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
+    const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
+    const int64_t Q = static_cast<int64_t>(tiles_x) * tiles_y * op.nz;
+    const int64_t q_begin = static_cast<int64_t>(blockIdx.x) * Q / gridDim.x;
+    const int64_t q_end = static_cast<int64_t>(blockIdx.x + 1) * Q / gridDim.x;
+    if (tid == 0) fence_proxy_async_global();
+
+    for (int64_t q = q_begin; q < q_end;) {
+        const int64_t tile = q / op.nz;
+        const int z0 = static_cast<int>(q % op.nz);
+        const int z1 = static_cast<int>(min(static_cast<int64_t>(op.nz), static_cast<int64_t>(z0) + (q_end - q)));
+        q += z1 - z0;
+        const int x0 = static_cast<int>(tile % tiles_x) * kTmaTX;
+        const int y0 = static_cast<int>(tile / tiles_x) * kTmaTY;
+        const uint32_t basex = seqx, basef = seqf;
+        const int pfirst = z0 - 3, plast = z1 + 2;  // X planes loaded
+        const int fbfirst = needF ? z0 : z0 - 2;    // first F / b plane
+        const int fblast = needF ? z1 - 1 : z1 + 1;
+        const int nfb = (needF || needB) ? fblast - fbfirst + 1 : 0;
+
+        auto issue_x = [&](int pl) {  // thread 0 only
+            const int slot = static_cast<int>((basex + static_cast<uint32_t>(pl - pfirst)) % k3XStages);
+            uint64_t* bar = ring.barx + slot;
+            mbar_arrive_expect_tx(bar, (needX ? kXTx : 0) + kLTx);
+            if (needX) tma_load_3d(ring.x(slot), &p.x3map[xbuf], x0 - k3XHaloX, y0 - 3, pl, bar);
+            tma_load_3d(ring.l(slot), &p.l3map, x0 - kLHaloX, y0 - 2, pl, bar);
+        };
+        auto issue_fb = [&](int pl) {  // thread 0 only
+            const int slot = static_cast<int>((basef + static_cast<uint32_t>(pl - fbfirst)) % k3FBStages);
+            uint64_t* bar = ring.barf + slot;
+            if (needF) {
+                mbar_arrive_expect_tx(bar, kOBytes);
+                tma_load_3d(ring.fb(slot), &p.omap[fbuf], x0, y0, pl, bar);
+            } else {
+                mbar_arrive_expect_tx(bar, kBTx);
+                tma_load_3d(ring.fb(slot), &p.b3map, x0 - k3XHaloX, y0 - 2, pl, bar);
+            }
+        };
+        auto xslot = [&](int pl) { return static_cast<int>((basex + static_cast<uint32_t>(pl - pfirst)) % k3XStages); };
+        auto fbslot = [&](int pl) {
+            return static_cast<int>((basef + static_cast<uint32_t>(pl - fbfirst)) % k3FBStages);
+        };
+        auto wait_x = [&](int pl) {
+            const int slot = xslot(pl);
+            mbar_wait(ring.barx + slot, (pmx >> slot) & 1u);
+            pmx ^= 1u << slot;
+        };
+        auto wait_fb = [&](int pl) {
+            const int slot = fbslot(pl);
+            mbar_wait(ring.barf + slot, (pmf >> slot) & 1u);
+            pmf ^= 1u << slot;
+        };
+
+        if (tid == 0) {
+            for (int k = 0; k < k3XStages && pfirst + k <= plast; ++k) issue_x(pfirst + k);
+            for (int k = 0; k < k3FBStages && k < nfb; ++k) issue_fb(fbfirst + k);
+        }
+
+        // per-segment geometry (own points: column gx, rows gy0, gy0 + 1)
+        const int gx = x0 + xl, gy0 = y0 + ry0;
+        const bool inx = gx < op.nx;
+        const bool in0 = inx && gy0 < op.ny, in1 = inx && gy0 + 1 < op.ny;
+        const int cxy = (gx > 0) + (gx < op.nx - 1);
+        const double ncxy0 = -static_cast<double>(cxy + (gy0 > 0) + (gy0 < op.ny - 1));
+        const double ncxy1 = -static_cast<double>(cxy + (gy0 + 1 > 0) + (gy0 + 1 < op.ny - 1));
+        const int rgx = x0 + rc, rgy = y0 + rr;
+        const bool rin = (aring || bring) && rgx >= 0 && rgx < op.nx && rgy >= 0 && rgy < op.ny;
+        const double rncxy = -static_cast<double>((rgx > 0) + (rgx < op.nx - 1) + (rgy > 0) + (rgy < op.ny - 1));
+        const int64_t v0 = gx + static_cast<int64_t>(gy0) * op.sy;
+        auto dhz = [&](int pl) { return static_cast<double>((pl > 0) + (pl < op.nz - 1)); };
+        auto zin = [&](int pl) { return pl >= 0 && pl < op.nz; };
+
+        // register rings (index = (plane - zb) & 3) of own values: X(z+1..z+2), T1(z-1..z+1),
+        // T2(z-2..z-1); the oldest plane each phase needs is re-read from shared memory
+        const int zb = z0 - 3;
+        double Xr[4][2], T1r[4][2], T2r[4][2];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            Xr[k][0] = Xr[k][1] = 0.0;
+            T1r[k][0] = T1r[k][1] = 0.0;
+            T2r[k][0] = T2r[k][1] = 0.0;
+        }
+        wait_x(zb);
+        wait_x(zb + 1);
+        if (needX) {
+            const double* X0 = ring.x(xslot(zb));
+            const double* X1 = ring.x(xslot(zb + 1));
+            Xr[0][0] = X0[oX];
+            Xr[0][1] = X0[oX + k3XPitch];
+            Xr[1][0] = X1[oX];
+            Xr[1][1] = X1[oX + k3XPitch];
+        }
+        double* pT = outT + v0 + static_cast<int64_t>(z0) * op.sz;
+        double* pF = outF + v0 + static_cast<int64_t>(z0) * op.sz;
+
+        auto iter = [&](int z, auto rconst) {
+            constexpr int r = decltype(rconst)::value;
+            constexpr int r1 = (r + 1) & 3, r2 = (r + 2) & 3, r3 = (r + 3) & 3;
+            // ---- A: T1 of plane pa = z + 1 (X of z, z+1, z+2 in Xr[r], Xr[r1], Xr[r2]) ----
+            if (z <= z1) {
+                const int pa = z + 1;
+                wait_x(z + 2);
+                const int sm_ = xslot(z), sc_ = xslot(pa), sp_ = xslot(z + 2);
+                const double* Xc = ring.x(sc_);
+                double xz0 = 0.0, xz1 = 0.0;  // own X(z): the ring's oldest plane, from shared memory
+                if (needX) {
+                    const double* Xp = ring.x(sp_);
+                    Xr[r2][0] = Xp[oX];
+                    Xr[r2][1] = Xp[oX + k3XPitch];
+                    const double* Xm = ring.x(sm_);
+                    xz0 = Xm[oX];
+                    xz1 = Xm[oX + k3XPitch];
+                }
+                const double* B = nullptr;
+                if (needB) {
+                    wait_fb(pa);
+                    B = ring.fb(fbslot(pa));
+                }
+                const uint8_t* L = ring.l(sc_);
+                const bool za = zin(pa);
+                const double dz = dhz(pa);
+                const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
+                double s0, s1;
+                if (KIND == k2FirstZero) {
+                    s0 = __dadd_rn(0.0, B[oB]);
+                    s1 = __dadd_rn(0.0, B[oB + k3XPitch]);
+                } else {
+                    s0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dz), xz0, Xc[oX - k3XPitch], Xc[oX - 1],
+                                      Xr[r1][0], Xc[oX + 1], Xr[r1][1], Xr[r2][0]);
+                    s1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dz), xz1, Xr[r1][0],
+                                      Xc[oX + k3XPitch - 1], Xr[r1][1], Xc[oX + k3XPitch + 1], Xc[oX + 2 * k3XPitch],
+                                      Xr[r2][1]);
+                    if (KIND == k2FirstBorder) {
+                        s0 = __dadd_rn(s0, B[oB]);
+                        s1 = __dadd_rn(s1, B[oB + k3XPitch]);
+                    }
+                }
+                const double t0v = (za && in0) ? __dmul_rn(c1, s0) : 0.0;
+                const double t1v = (za && in1) ? __dmul_rn(c1, s1) : 0.0;
+                T1r[r1][0] = t0v;
+                T1r[r1][1] = t1v;
+                double* T1 = ring.t1(pa & 3);
+                T1[oT1] = t0v;
+                T1[oT1 + k3T1Pitch] = t1v;
+                if (aring) {
+                    const double w = s_wtab[L[aL]];
+                    double sc;
+                    if (KIND == k2FirstZero) {
+                        sc = __dadd_rn(0.0, B[aB]);
+                    } else {
+                        const double* Xm = ring.x(sm_);
+                        const double* Xp = ring.x(sp_);
+                        sc = row_apply_nc(w, w != 0.0, __dsub_rn(rncxy, dz), Xm[aX], Xc[aX - k3XPitch], Xc[aX - 1],
+                                          Xc[aX], Xc[aX + 1], Xc[aX + k3XPitch], Xp[aX]);
+                        if (KIND == k2FirstBorder) sc = __dadd_rn(sc, B[aB]);
+                    }
+                    T1[aT1] = (za && rin) ? __dmul_rn(c1, sc) : 0.0;
+                }
+            }
+            // ---- B: T2 of plane pb = z - 1 (own T1 of z-2, z-1, z in T1r[r2], T1r[r3], T1r[r]) ----
+            if (z >= z0) {
+                const int pb = z - 1;
+                const double* T1m = ring.t1((pb + 3) & 3);
+                const double* T1c = ring.t1(pb & 3);
+                const double* T1p = ring.t1((pb + 1) & 3);
+                const uint8_t* L = ring.l(xslot(pb));
+                const bool zb_ = zin(pb);
+                const double dz = dhz(pb);
+                const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
+                const double a0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dz), T1m[oT1], T1c[oT1 - k3T1Pitch],
+                                               T1c[oT1 - 1], T1r[r3][0], T1c[oT1 + 1], T1r[r3][1], T1r[r][0]);
+                const double a1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dz), T1m[oT1 + k3T1Pitch], T1r[r3][0],
+                                               T1c[oT1 + k3T1Pitch - 1], T1r[r3][1], T1c[oT1 + k3T1Pitch + 1],
+                                               T1c[oT1 + 2 * k3T1Pitch], T1r[r][1]);
+                const double u0 = (zb_ && in0) ? __dmul_rn(c2, a0) : 0.0;
+                const double u1 = (zb_ && in1) ? __dmul_rn(c2, a1) : 0.0;
+                T2r[r3][0] = u0;
+                T2r[r3][1] = u1;
+                double* T2 = ring.t2((pb + 3) % 3);
+                T2[oT2] = u0;
+                T2[oT2 + k3T2Pitch] = u1;
+                if (bring) {
+                    const double w = s_wtab[L[aL]];
+                    const double sc = row_apply_nc(w, w != 0.0, __dsub_rn(rncxy, dz), T1m[aT1], T1c[aT1 - k3T1Pitch],
+                                                   T1c[aT1 - 1], T1c[aT1], T1c[aT1 + 1], T1c[aT1 + k3T1Pitch], T1p[aT1]);
+                    T2[aT2] = (zb_ && rin) ? __dmul_rn(c2, sc) : 0.0;
+                }
+            }
+            // ---- C: T3 of plane pc = z - 2 (own T2 of pc-1, pc, pc+1 in T2r[r1], T2r[r2], T2r[r3]) ----
+            const bool runC = z >= z0 + 2;
+            if (runC) {
+                // reads T2's shared plane z-2 (written last iteration) and own T2 / T1 registers
+                // only, so no barrier separates it from A and B
+                const int pc = z - 2;
+                const double* T2c = ring.t2((pc + 3) % 3);
+                const double* T2m = ring.t2((pc + 2) % 3);
+                const double* T1o = ring.t1(pc & 3);
+                const uint8_t* L = ring.l(xslot(pc));
+                const double dz = dhz(pc);
+                const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
+                const double b0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dz), T2m[oT2], T2c[oT2 - k3T2Pitch],
+                                               T2c[oT2 - 1], T2r[r2][0], T2c[oT2 + 1], T2r[r2][1], T2r[r3][0]);
+                const double b1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dz), T2m[oT2 + k3T2Pitch], T2r[r2][0],
+                                               T2c[oT2 + k3T2Pitch - 1], T2r[r2][1], T2c[oT2 + k3T2Pitch + 1],
+                                               T2c[oT2 + 2 * k3T2Pitch], T2r[r3][1]);
+                const double t30 = __dmul_rn(c3, b0), t31 = __dmul_rn(c3, b1);
+                double fp0, fp1;
+                if (KIND == k2FirstZero) {
+                    fp0 = 0.0;
+                    fp1 = 0.0;
+                } else {
+                    const double* XC = ring.x(xslot(pc));
+                    const double xo0 = XC[oX], xo1 = XC[oX + k3XPitch];
+                    if (KIND == k2Next) {
+                        wait_fb(pc);
+                        const double* Fo = ring.fb(fbslot(pc));
+                        fp0 = __dadd_rn(Fo[oF], xo0);
+                        fp1 = __dadd_rn(Fo[oF + kTmaTX], xo1);
+                    } else {
+                        fp0 = xo0;
+                        fp1 = xo1;
+                    }
+                }
+                const double t10 = T1o[oT1], t11 = T1o[oT1 + k3T1Pitch];
+                const double f10 = __dadd_rn(fp0, t10), f11 = __dadd_rn(fp1, t11);
+                const double f20 = __dadd_rn(f10, T2r[r2][0]), f21 = __dadd_rn(f11, T2r[r2][1]);
+                const double f30 = __dadd_rn(f20, t30), f31 = __dadd_rn(f21, t31);
+                if (in0) {
+                    pT[0] = t30;
+                    pF[0] = f20;
+                    mx[0] = nan_dropping_max(mx[0], fabs(t10));
+                    mx[1] = nan_dropping_max(mx[1], fabs(f10));
+                    mx[2] = nan_dropping_max(mx[2], fabs(T2r[r2][0]));
+                    mx[3] = nan_dropping_max(mx[3], fabs(f20));
+                    mx[4] = nan_dropping_max(mx[4], fabs(t30));
+                    mx[5] = nan_dropping_max(mx[5], fabs(f30));
+                }
+                if (in1) {
+                    pT[op.sy] = t31;
+                    pF[op.sy] = f21;
+                    mx[0] = nan_dropping_max(mx[0], fabs(t11));
+                    mx[1] = nan_dropping_max(mx[1], fabs(f11));
+                    mx[2] = nan_dropping_max(mx[2], fabs(T2r[r2][1]));
+                    mx[3] = nan_dropping_max(mx[3], fabs(f21));
+                    mx[4] = nan_dropping_max(mx[4], fabs(t31));
+                    mx[5] = nan_dropping_max(mx[5], fabs(f31));
+                }
+                pT += op.sz;
+                pF += op.sz;
+            }
+            __syncthreads();  // slots of plane z-2, T1(z-2)'s and T2(z-3)'s shared planes are free
+            if (tid == 0) {
+                const int freed = z - 2;  // X plane no longer read by any later iteration
+                if (freed >= pfirst && freed + k3XStages <= plast) issue_x(freed + k3XStages);
+                if (needF && runC && z - 2 + k3FBStages <= fblast) issue_fb(z - 2 + k3FBStages);
+                if (needB && z <= z1 && z + 1 + k3FBStages <= fblast) issue_fb(z + 1 + k3FBStages);
+            }
+        };
+        for (int zz = zb; zz <= z1 + 1; zz += 4) {
+            iter(zz, std::integral_constant<int, 0>{});
+            if (zz + 1 <= z1 + 1) iter(zz + 1, std::integral_constant<int, 1>{});
+            if (zz + 2 <= z1 + 1) iter(zz + 2, std::integral_constant<int, 2>{});
+            if (zz + 3 <= z1 + 1) iter(zz + 3, std::integral_constant<int, 3>{});
+        }
+        seqx = basex + static_cast<uint32_t>(plast - pfirst + 1);
+        seqf = basef + static_cast<uint32_t>(nfb);
+    }
+    fence_proxy_async_global();
+}
+
 enum TermKind { kFirstZero, kFirstBorder, kFirstPlain, kNext };
 
 // Per-block setup shared by the kernels: w table in shared memory, mbarriers for TMA.
@@ -591,6 +949,8 @@ __device__ __forceinline__ void block_setup(const SolveParams& p, Smem& sm, bool
     if (with_tma && threadIdx.x == 0) {
         for (int s = 0; s < kTmaStages; ++s) mbar_init(sm.bar1 + s, 1);
         for (int s = 0; s < k2Stages; ++s) mbar_init(sm.bar2 + s, 1);
+        for (int s = 0; s < k3XStages; ++s) mbar_init(sm.bar3x + s, 1);
+        for (int s = 0; s < k3FBStages; ++s) mbar_init(sm.bar3f + s, 1);
         mbar_fence_init();
         for (int b = 0; b < kNumBufs; ++b) tma_prefetch_desc(&p.xmap[b]);
     }
@@ -841,6 +1201,7 @@ __global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_cons
 // two-term sweeps (TMA) or single-term sweeps (fallback) with the in-kernel termination
 // test; grid barriers between terms.  The small-norm branch's stencil pass lives here too.
 // ------------------------------------------------------------------------------------------
+template <int FUSE>
 __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_constant__ SolveParams p,
                                                                   int border_blocks, int step) {
     cg::grid_group grid = cg::this_grid();
@@ -853,7 +1214,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
     block_setup(p, sm, p.use_tma);
     Ring ring{dyn, sm.bar1};
     Ring2 ring2{dyn, sm.bar2};
-    uint32_t seq = 0, seq2 = 0, pmask2 = 0;
+    Ring3 ring3{dyn, sm.bar3x, sm.bar3f};
+    uint32_t seq = 0, seq2 = 0, pmask2 = 0, seq3x = 0, seq3f = 0, pm3x = 0, pm3f = 0;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     gs_step_info* info = (p.infos && leader) ? p.infos + step : nullptr;
     // Grid barrier; with TMA, first order this thread's generic global writes before any
@@ -867,8 +1229,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
     auto sync_round = [&](int tag) {
         gsync(tag);
         if (leader) {
-            unsigned long long* z = p.slots + ((round + 2) % 3) * 4;
-            z[0] = z[1] = z[2] = z[3] = 0ull;
+            unsigned long long* z = p.slots + ((round + 2) % 3) * 8;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) z[q] = 0ull;
         }
         ++round;
     };
@@ -933,46 +1296,157 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
         }
         return true;
     };
+    // A stage starts from f: the previous stage's F[fres], materialising an implicit
+    // F + T first (vectorised: two double2 loads per input in flight per thread).
+    auto stage_start = [&](int stage) -> int {
+        if (stage == 0) return bordered ? -1 : kBufG;
+        if (tres < 0) return fres;
+        const double* Fa = p.buf[fres];
+        const double* Tb = p.buf[tres];
+        const int fo = (fres == kBufF0) ? kBufF1 : kBufF0;
+        double* Fw = p.buf[fo];
+        const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+        const int64_t n2 = op.n >> 1;
+        const double2* A2 = reinterpret_cast<const double2*>(Fa);
+        const double2* B2 = reinterpret_cast<const double2*>(Tb);
+        double2* W2 = reinterpret_cast<double2*>(Fw);
+        for (int64_t i = tid; i < n2; i += 2 * stride) {
+            const bool second = i + stride < n2;
+            const double2 a0 = A2[i], b0 = B2[i];
+            double2 a1 = make_double2(0.0, 0.0), b1 = a1;
+            if (second) {
+                a1 = A2[i + stride];
+                b1 = B2[i + stride];
+            }
+            W2[i] = make_double2(__dadd_rn(a0.x, b0.x), __dadd_rn(a0.y, b0.y));
+            if (second) W2[i + stride] = make_double2(__dadd_rn(a1.x, b1.x), __dadd_rn(a1.y, b1.y));
+        }
+        if ((op.n & 1) && tid == 0) Fw[op.n - 1] = __dadd_rn(Fa[op.n - 1], Tb[op.n - 1]);
+        gsync(kTrFixup);
+        return fo;
+    };
+    auto publish_max = [&](double* mx, int k, int tag) {
+        if (threadIdx.x == 0) {
+            unsigned long long* sl = p.slots + (round % 3) * 8;
+            for (int q = 0; q < k; ++q)
+                if (mx[q] > 0.0) atomicMax(sl + q, static_cast<unsigned long long>(__double_as_longlong(mx[q])));
+        }
+        sync_round(tag);
+    };
     if (p.use_tma) {
+      if constexpr (FUSE == 3) {
+        // Fused three-term sweeps; decisions term by term as the reference's loop
+        // (expact.cpp:81-95) on the six maxima of each sweep.  State between sweeps:
+        // (T_j in T[tsel^1], F_{j-1} in F[fsel^1]) with F_j = F_{j-1} + T_j implicit.
+        int fsel = 0, tsel = 0;
+        for (int stage = 0; stage < s_st; ++stage) {
+            const int fstart = stage_start(stage);
+            if (fstart == kBufF0) fsel = 1;
+            else if (fstart == kBufF1) fsel = 0;
+            int used = 0;
+            int kind = fstart < 0 ? k2FirstZero : (bordered ? k2FirstBorder : k2FirstPlain);
+            int xb = fstart, fb = -1;
+            while (true) {
+                const double c1 = __ddiv_rn(tau_s, static_cast<double>(used + 1));  // expact.cpp:83
+                const double c2 = __ddiv_rn(tau_s, static_cast<double>(used + 2));
+                const double c3 = __ddiv_rn(tau_s, static_cast<double>(used + 3));
+                const int fout = kBufF0 + fsel, tout = kBufT0 + tsel;
+                double mx[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                {
+                    const int xb_ = xb < 0 ? 0 : xb, fb_ = fb < 0 ? 0 : fb;
+                    double* oT = p.buf[tout];
+                    double* oF = p.buf[fout];
+                    if (kind == k2Next)
+                        sweep3_tma<k2Next>(p, ring3, xb_, fb_, c1, c2, c3, oT, oF, mx, seq3x, seq3f, pm3x, pm3f,
+                                           sm.wtab);
+                    else if (kind == k2FirstBorder)
+                        sweep3_tma<k2FirstBorder>(p, ring3, xb_, fb_, c1, c2, c3, oT, oF, mx, seq3x, seq3f, pm3x,
+                                                  pm3f, sm.wtab);
+                    else if (kind == k2FirstZero)
+                        sweep3_tma<k2FirstZero>(p, ring3, xb_, fb_, c1, c2, c3, oT, oF, mx, seq3x, seq3f, pm3x,
+                                                pm3f, sm.wtab);
+                    else
+                        sweep3_tma<k2FirstPlain>(p, ring3, xb_, fb_, c1, c2, c3, oT, oF, mx, seq3x, seq3f, pm3x,
+                                                 pm3f, sm.wtab);
+                }
+                block_reduce<6, true>(mx, sm);
+                publish_max(mx, 6, kind == k2Next ? kTrFusedNext : kTrFusedFirst);
+                const unsigned long long* sl = p.slots + ((round - 1) % 3) * 8;
+                double cur[3], fn[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    cur[k] = slot_read(sl + 2 * k);
+                    fn[k] = slot_read(sl + 2 * k + 1);
+                    if (bordered) fn[k] = nan_dropping_max(fn[k], 1.0);  // f_n == 1 (expact.cpp:89)
+                }
+                // term used+1: F1 = Fprev + T1 was not stored -- recompute it if the stage ends here
+                ++used;
+                if (!finite_or_fail(cur[0], fn[0])) return;
+                if (__dadd_rn(prev, cur[0]) <= __dmul_rn(p.tol, fn[0]) || used == m_deg) {
+                    double* Fo = p.buf[fout];
+                    if (kind == k2FirstZero) {
+                        sweep_points(op, [&](int64_t v) {
+                            Fo[v] = __dadd_rn(0.0, __dmul_rn(c1, __dadd_rn(0.0, G[v])));
+                        });
+                    } else if (kind == k2FirstBorder) {
+                        stencil_sweep(p, sm, ring, seq, xb, -1, kBufG, [&](int64_t v, double acc, double x, double,
+                                                                           double bg) {
+                            Fo[v] = __dadd_rn(x, __dmul_rn(c1, __dadd_rn(acc, bg)));
+                        });
+                    } else if (kind == k2FirstPlain) {
+                        stencil_sweep(p, sm, ring, seq, xb, -1, -1, [&](int64_t v, double acc, double x, double,
+                                                                        double) {
+                            Fo[v] = __dadd_rn(x, __dmul_rn(c1, acc));
+                        });
+                    } else {
+                        stencil_sweep(p, sm, ring, seq, xb, fb, -1, [&](int64_t v, double acc, double x, double f,
+                                                                        double) {
+                            Fo[v] = __dadd_rn(__dadd_rn(f, x), __dmul_rn(c1, acc));
+                        });
+                    }
+                    gsync(kTrTerm);
+                    prev = fn[0];
+                    fres = fout;
+                    tres = -1;
+                    break;
+                }
+                prev = cur[0];
+                // term used+1: F2, stored
+                ++used;
+                if (!finite_or_fail(cur[1], fn[1])) return;
+                if (__dadd_rn(prev, cur[1]) <= __dmul_rn(p.tol, fn[1]) || used == m_deg) {
+                    prev = fn[1];
+                    fres = fout;
+                    tres = -1;
+                    break;
+                }
+                prev = cur[1];
+                // term used+1: F3 = F2 + T3, implicit
+                ++used;
+                if (!finite_or_fail(cur[2], fn[2])) return;
+                if (__dadd_rn(prev, cur[2]) <= __dmul_rn(p.tol, fn[2]) || used == m_deg) {
+                    prev = fn[2];
+                    fres = fout;
+                    tres = tout;
+                    break;
+                }
+                prev = cur[2];
+                kind = k2Next;
+                xb = tout;
+                fb = fout;
+                fsel ^= 1;
+                tsel ^= 1;
+            }
+            total_terms += used;
+            if (info && stage < kMaxLoggedStages) info->terms[stage] = used;
+        }
+      } else {
         // Fused two-term sweeps; the decisions are taken term by term exactly as the
         // reference's loop (expact.cpp:81-95), on the four maxima of each sweep.
         int fsel = 0, tsel = 0;
         for (int stage = 0; stage < s_st; ++stage) {
-            int fstart;  // buffer holding this stage's starting f (the stencil input)
-            if (stage == 0) {
-                fstart = bordered ? -1 : kBufG;
-            } else if (tres >= 0) {
-                // previous stage ended on its implicit F2: materialise f = F1 + T2
-                const double* Fa = p.buf[fres];
-                const double* Tb = p.buf[tres];
-                const int fo = (fres == kBufF0) ? kBufF1 : kBufF0;
-                double* Fw = p.buf[fo];
-                {
-                    // vectorised: two double2 loads per input in flight per thread
-                    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-                    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-                    const int64_t n2 = op.n >> 1;
-                    const double2* A2 = reinterpret_cast<const double2*>(Fa);
-                    const double2* B2 = reinterpret_cast<const double2*>(Tb);
-                    double2* W2 = reinterpret_cast<double2*>(Fw);
-                    for (int64_t i = tid; i < n2; i += 2 * stride) {
-                        const bool second = i + stride < n2;
-                        const double2 a0 = A2[i], b0 = B2[i];
-                        double2 a1 = make_double2(0.0, 0.0), b1 = a1;
-                        if (second) {
-                            a1 = A2[i + stride];
-                            b1 = B2[i + stride];
-                        }
-                        W2[i] = make_double2(__dadd_rn(a0.x, b0.x), __dadd_rn(a0.y, b0.y));
-                        if (second) W2[i + stride] = make_double2(__dadd_rn(a1.x, b1.x), __dadd_rn(a1.y, b1.y));
-                    }
-                    if ((op.n & 1) && tid == 0) Fw[op.n - 1] = __dadd_rn(Fa[op.n - 1], Tb[op.n - 1]);
-                }
-                gsync(kTrFixup);
-                fstart = fo;
-            } else {
-                fstart = fres;
-            }
+            const int fstart = stage_start(stage);
             if (fstart == kBufF0) fsel = 1;
             else if (fstart == kBufF1) fsel = 0;
             int used = 0;
@@ -998,13 +1472,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                 }
                 block_reduce<4, true>(mx, sm);
                 if (threadIdx.x == 0) {
-                    unsigned long long* sl = p.slots + (round % 3) * 4;
+                    unsigned long long* sl = p.slots + (round % 3) * 8;
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
                         if (mx[q] > 0.0) atomicMax(sl + q, static_cast<unsigned long long>(__double_as_longlong(mx[q])));
                 }
                 sync_round(kind == k2Next ? kTrFusedNext : kTrFusedFirst);
-                const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
+                const unsigned long long* sl = p.slots + ((round - 1) % 3) * 8;
                 double cur[2] = {slot_read(sl + 0), slot_read(sl + 2)};
                 double fn[2] = {slot_read(sl + 1), slot_read(sl + 3)};
                 if (bordered) {
@@ -1040,6 +1514,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
             total_terms += used;
             if (info && stage < kMaxLoggedStages) info->terms[stage] = used;
         }
+      }
     } else {
         // Single-term sweeps (shapes the TMA path cannot describe)
         int fcur = bordered ? -1 : kBufG;  // -1: f = e_{n+1} (all zero) for the bordered action
@@ -1083,7 +1558,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                 double v2[2] = {mt, mf};
                 block_reduce<2, true>(v2, sm);
                 if (threadIdx.x == 0) {
-                    unsigned long long* sl = p.slots + (round % 3) * 4;
+                    unsigned long long* sl = p.slots + (round % 3) * 8;
                     if (v2[0] > 0.0) atomicMax(sl + 0, static_cast<unsigned long long>(__double_as_longlong(v2[0])));
                     if (v2[1] > 0.0) atomicMax(sl + 1, static_cast<unsigned long long>(__double_as_longlong(v2[1])));
                 }
@@ -1093,7 +1568,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                 tprev = tout;
                 fsel ^= 1;
                 tsel ^= 1;
-                const unsigned long long* sl = p.slots + ((round - 1) % 3) * 4;
+                const unsigned long long* sl = p.slots + ((round - 1) % 3) * 8;
                 const double cur = slot_read(sl + 0);
                 double fnorm = slot_read(sl + 1);
                 if (bordered) fnorm = nan_dropping_max(fnorm, 1.0);  // f_n == 1 (expact.cpp:89)
@@ -1120,6 +1595,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
 // ------------------------------------------------------------------------------------------
 // K5 update: u <- u + tau * (gamma/tau) * y (run, + compute_metrics) or out = scale * y
 // ------------------------------------------------------------------------------------------
+template __global__ void taylor_kernel<2>(const __grid_constant__ SolveParams, int, int);
+template __global__ void taylor_kernel<3>(const __grid_constant__ SolveParams, int, int);
+
 __global__ void __launch_bounds__(kSolveThreads) update_kernel(const __grid_constant__ SolveParams p, int step) {
     __shared__ Smem sm;
     const Ctrl* ctrl = p.ctrl;

@@ -258,8 +258,10 @@ def test_constants_preserved_by_expmv(G):
     assert np.allclose(y, 1.0, rtol=1e-12, atol=0)
 
 
-def test_mid_size_step_vs_oracle(G, port):
+@pytest.mark.parametrize("fuse", ["2", "3"])
+def test_mid_size_step_vs_oracle(G, port, fuse, monkeypatch):
     """64^3 phantom, several steps: bitwise against the oracle given the device sums."""
+    monkeypatch.setenv("GS_FUSE", fuse)
     from paper_2402_02273_b200 import phantom
     n = 64
     inten = phantom.shell_phantom(n, n, n, seed=31)
@@ -288,10 +290,14 @@ TMA_SHAPES = [(48, 32, 20), (80, 40, 12), (64, 48, 1), (32, 32, 32), (16, 16, 16
 
 
 @pytest.mark.parametrize("shape", TMA_SHAPES)
-@pytest.mark.parametrize("tma", [True, False])
-def test_sweep_paths_vs_oracle(G, port, shape, tma, monkeypatch):
-    if not tma:
+@pytest.mark.parametrize("path", ["tma2", "tma3", "l1"])
+def test_sweep_paths_vs_oracle(G, port, shape, path, monkeypatch):
+    """Every sweep implementation: fused two-term TMA (default), fused three-term TMA
+    (GS_FUSE=3) and the L1 single-term fallback -- bitwise against the oracle."""
+    if path == "l1":
         monkeypatch.setenv("GS_DISABLE_TMA", "1")
+    if path == "tma3":
+        monkeypatch.setenv("GS_FUSE", "3")
     rng = np.random.default_rng(sum(shape))
     n = int(np.prod(shape))
     table = np.array([0.0, 0.13, 0.013, 0.05])
