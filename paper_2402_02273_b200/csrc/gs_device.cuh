@@ -107,6 +107,13 @@ __device__ __forceinline__ double row_apply_nc(double w, bool live, double negcn
 // (expact.cpp:15-19), so the result equals the reference's serial max bit for bit.
 __device__ __forceinline__ double nan_dropping_max(double m, double x) { return (m < x) ? x : m; }
 
+// |x| by clearing the sign bit in the integer pipe (fabs would cost an fp64 DADD with an
+// |.| modifier); identical to fabs for every input, NaN included.
+__device__ __forceinline__ double abs_bits(double x) {
+    return __hiloint2double(__double2hiint(x) & 0x7fffffff, __double2loint(x));
+}
+__device__ __forceinline__ double max_abs(double m, double x) { return nan_dropping_max(m, abs_bits(x)); }
+
 // Signed doubles mapped to an unsigned order-preserving key (for min/max of u).
 __device__ __forceinline__ unsigned long long ordered_key(double x) {
     unsigned long long b = __double_as_longlong(x);

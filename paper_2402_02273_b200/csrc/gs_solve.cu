@@ -406,9 +406,11 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
 
         // Phase A: T1 of plane pl.  sm/sc/sp: ring slots of planes pl-1, pl, pl+1.
         // xm/xc/xp: own rows' X at pl-1, pl, pl+1.  Writes T1's shared plane (pl & 1).
-        auto phaseA = [&](int pl, int sm_, int sc_, int sp_, const double (&xm)[2], const double (&xc)[2],
+        // T1 shared planes rotate per segment: plane pl lives in slot (pl - z0 + 1) % 3, a
+        // compile-time index inside the unrolled loop
+        auto phaseA = [&](int pl, int tslot, int sm_, int sc_, int sp_, const double (&xm)[2], const double (&xc)[2],
                           const double (&xp)[2], double (&t1)[2], double (&lw)[2]) {
-            double* T1 = ring.t1((pl + 3) % kT1Planes);
+            double* T1 = ring.t1(tslot);
             const bool zin = pl >= 0 && pl < op.nz;
             const double dhz = static_cast<double>((pl > 0) + (pl < op.nz - 1));
             const double* Xc = ring.x(sc_);
@@ -473,14 +475,14 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
         }
         // own T1 of planes z-2, z-1, z (relative to the loop's z); w unused here
         double tm2[2] = {0.0, 0.0}, tm1[2], t0[2], lwd[2];
-        phaseA(z0 - 1, s0, s1, s2, xz, xa, xb, tm1, lwd);
+        phaseA(z0 - 1, 0, s0, s1, s2, xz, xa, xb, tm1, lwd);
         wait_slot(s3);
         if (needX) {
             const double* X3 = ring.x(s3);
             xn[0] = X3[oX];
             xn[1] = X3[oX + kXPitch];
         }
-        phaseA(z0, s1, s2, s3, xa, xb, xn, t0, lwd);
+        phaseA(z0, 1, s1, s2, s3, xa, xb, xn, t0, lwd);
         xa[0] = xb[0];
         xa[1] = xb[1];
         xb[0] = xn[0];
@@ -506,7 +508,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             if (z > z0) {
                 // Phase B: own voxels of plane zo = z-1 (T1 of zo-1, zo, zo+1 in T3[r2], T3[r], T3[r1])
                 const int zo = z - 1;
-                const double* T1s = ring.t1((zo + 3) % kT1Planes);
+                const double* T1s = ring.t1(r);  // plane zo = z - 1: slot (z - z0) % 3
                 const uint8_t* L = ring.l(sM);
                 const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
                 const double dhz = static_cast<double>((zo > 0) + (zo < op.nz - 1));
@@ -538,18 +540,18 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 if (in0) {
                     pT[0] = t20;
                     pF[0] = f10;
-                    mx[0] = nan_dropping_max(mx[0], fabs(T3[r][0]));
-                    mx[1] = nan_dropping_max(mx[1], fabs(f10));
-                    mx[2] = nan_dropping_max(mx[2], fabs(t20));
-                    mx[3] = nan_dropping_max(mx[3], fabs(f20));
+                    mx[0] = max_abs(mx[0], T3[r][0]);
+                    mx[1] = max_abs(mx[1], f10);
+                    mx[2] = max_abs(mx[2], t20);
+                    mx[3] = max_abs(mx[3], f20);
                 }
                 if (in1) {
                     pT[op.sy] = t21;
                     pF[op.sy] = f11;
-                    mx[0] = nan_dropping_max(mx[0], fabs(T3[r][1]));
-                    mx[1] = nan_dropping_max(mx[1], fabs(f11));
-                    mx[2] = nan_dropping_max(mx[2], fabs(t21));
-                    mx[3] = nan_dropping_max(mx[3], fabs(f21));
+                    mx[0] = max_abs(mx[0], T3[r][1]);
+                    mx[1] = max_abs(mx[1], f11);
+                    mx[2] = max_abs(mx[2], t21);
+                    mx[3] = max_abs(mx[3], f21);
                 }
                 pT += op.sz;
                 pF += op.sz;
@@ -562,7 +564,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                     X3[r2][1] = XC[oX + kXPitch];
                 }
                 double lwN[2];
-                phaseA(z + 1, sA, sB, sC, X3[r], X3[r1], X3[r2], T3[r2], lwN);
+                phaseA(z + 1, r2, sA, sB, sC, X3[r], X3[r1], X3[r2], T3[r2], lwN);
             }
             sM = sA;
             sA = sB;
@@ -900,22 +902,22 @@ __device__ __forceinline__ void sweep3_tma(const SolveParams& p, const Ring3& ri
                 if (in0) {
                     pT[0] = t30;
                     pF[0] = f20;
-                    mx[0] = nan_dropping_max(mx[0], fabs(t10));
-                    mx[1] = nan_dropping_max(mx[1], fabs(f10));
-                    mx[2] = nan_dropping_max(mx[2], fabs(T2r[r2][0]));
-                    mx[3] = nan_dropping_max(mx[3], fabs(f20));
-                    mx[4] = nan_dropping_max(mx[4], fabs(t30));
-                    mx[5] = nan_dropping_max(mx[5], fabs(f30));
+                    mx[0] = max_abs(mx[0], t10);
+                    mx[1] = max_abs(mx[1], f10);
+                    mx[2] = max_abs(mx[2], T2r[r2][0]);
+                    mx[3] = max_abs(mx[3], f20);
+                    mx[4] = max_abs(mx[4], t30);
+                    mx[5] = max_abs(mx[5], f30);
                 }
                 if (in1) {
                     pT[op.sy] = t31;
                     pF[op.sy] = f21;
-                    mx[0] = nan_dropping_max(mx[0], fabs(t11));
-                    mx[1] = nan_dropping_max(mx[1], fabs(f11));
-                    mx[2] = nan_dropping_max(mx[2], fabs(T2r[r2][1]));
-                    mx[3] = nan_dropping_max(mx[3], fabs(f21));
-                    mx[4] = nan_dropping_max(mx[4], fabs(t31));
-                    mx[5] = nan_dropping_max(mx[5], fabs(f31));
+                    mx[0] = max_abs(mx[0], t11);
+                    mx[1] = max_abs(mx[1], f11);
+                    mx[2] = max_abs(mx[2], T2r[r2][1]);
+                    mx[3] = max_abs(mx[3], f21);
+                    mx[4] = max_abs(mx[4], t31);
+                    mx[5] = max_abs(mx[5], f31);
                 }
                 pT += op.sz;
                 pF += op.sz;
