@@ -14,6 +14,8 @@
 //   RunResult run(cfg, d, u0, workers, sink, warn, watch)      run(cfg, d, u0, sink, warn, watch)
 //                                                               (integrator.hpp:75-77)
 //   write_vtk / read_vtk / write_metrics_csv (vtk.hpp:40-48)   same names (byte-identical files)
+//   load_stack / load_raw_volume / resample / matter_fractions  same names (imaging.hpp:28-54); resample and
+//     / write_label_volume / read_label_volume               matter_fractions run on the GPU
 //   RunResult run_to_directory(cfg, d, materials, dir, ...)    run_to_directory(...) (pipeline.hpp:18-24),
 //                                                               snapshots written while the GPU steps on
 //   std::invalid_argument / numeric_error / data_error         same std::invalid_argument /
@@ -33,6 +35,7 @@
 #include <functional>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -351,6 +354,85 @@ void write_metrics_csv(const SeriesT& series, const std::string& path) {
     }
     detail::check_free(gs_write_metrics_csv(path.c_str(), static_cast<int>(step.size()), step.data(), time.data(),
                                             m.data()));
+}
+
+// ---- imaging (imaging.hpp:28-54): loaders on the host, the material map on the GPU -----
+// load_stack / load_raw_volume for any ImageStack-like type (width, height, num_slices,
+// intensities), e.g. gliosim_b200::load_stack<gliosim::ImageStack>(paths).
+template <class ImageStackT>
+ImageStackT load_stack(const std::vector<std::string>& paths) {
+    std::vector<const char*> cp;
+    for (const auto& s : paths) cp.push_back(s.c_str());
+    int w = 0, h = 0, n = 0;
+    detail::check_free(gs_load_stack(cp.data(), static_cast<int>(cp.size()), &w, &h, &n, nullptr, 0));
+    ImageStackT st;
+    st.width = w;
+    st.height = h;
+    st.num_slices = n;
+    st.intensities.resize(static_cast<size_t>(w) * h * n);
+    detail::check_free(gs_load_stack(cp.data(), static_cast<int>(cp.size()), &w, &h, &n, st.intensities.data(),
+                                     static_cast<int64_t>(st.intensities.size())));
+    return st;
+}
+
+template <class ImageStackT>
+ImageStackT load_raw_volume(const std::string& path) {
+    int w = 0, h = 0, n = 0;
+    detail::check_free(gs_load_raw_volume(path.c_str(), &w, &h, &n, nullptr, 0));
+    ImageStackT st;
+    st.width = w;
+    st.height = h;
+    st.num_slices = n;
+    st.intensities.resize(static_cast<size_t>(w) * h * n);
+    detail::check_free(gs_load_raw_volume(path.c_str(), &w, &h, &n, st.intensities.data(),
+                                          static_cast<int64_t>(st.intensities.size())));
+    return st;
+}
+
+// resample (imaging.cpp:118-141: nearest source + classify) on the GPU (K1), returning the
+// caller's MaterialVolume type, e.g. resample<gliosim::MaterialVolume>(stack, grid, cfg).
+template <class MaterialVolumeT, class ImageStackT, class GridT, class SimConfigT>
+MaterialVolumeT resample(const ImageStackT& stack, const GridT& grid, const SimConfigT& cfg, int device = 0) {
+    if (stack.num_slices < 1 || stack.width < 1 || stack.height < 1) throw data_error("resample: degenerate stack");
+    StencilOperator op(grid.nx, grid.ny, grid.nz, grid.h, device);
+    check(gs_set_intensity(op.ctx(), stack.intensities.data(), stack.width, stack.height, stack.num_slices,
+                           cfg.threshold_air, cfg.threshold_white, cfg.threshold_gray, cfg.d_white, cfg.d_gray),
+          op.ctx());
+    std::vector<uint8_t> lab(static_cast<size_t>(op.dim()));
+    check(gs_get_labels(op.ctx(), lab.data()), op.ctx());
+    MaterialVolumeT mv(grid);
+    using M = typename std::decay<decltype(mv.labels[0])>::type;
+    for (size_t v = 0; v < lab.size(); ++v) mv.labels[v] = static_cast<M>(lab[v]);
+    return mv;
+}
+
+// matter_fractions (imaging.cpp:155-164), counted on the GPU.
+struct MatterFractions {
+    double white = 0.0, gray = 0.0;
+};
+template <class MaterialVolumeT>
+MatterFractions matter_fractions(const MaterialVolumeT& mv, int device = 0) {
+    StencilOperator op(mv.grid.nx, mv.grid.ny, mv.grid.nz, mv.grid.h, device);
+    op.set_labels(detail::label_bytes(mv), 0.13, 0.013);
+    MatterFractions f;
+    check(gs_matter_fractions(op.ctx(), &f.white, &f.gray), op.ctx());
+    return f;
+}
+
+template <class MaterialVolumeT>
+void write_label_volume(const MaterialVolumeT& mv, const std::string& path) {
+    const std::vector<uint8_t> lab = detail::label_bytes(mv);
+    detail::check_free(gs_write_label_volume(path.c_str(), lab.data(), mv.grid.nx, mv.grid.ny, mv.grid.nz));
+}
+
+template <class MaterialVolumeT, class GridT>
+MaterialVolumeT read_label_volume(const std::string& path, const GridT& grid) {
+    std::vector<uint8_t> lab(static_cast<size_t>(grid.nx) * grid.ny * grid.nz);
+    detail::check_free(gs_read_label_volume(path.c_str(), grid.nx, grid.ny, grid.nz, lab.data()));
+    MaterialVolumeT mv(grid);
+    using M = typename std::decay<decltype(mv.labels[0])>::type;
+    for (size_t v = 0; v < lab.size(); ++v) mv.labels[v] = static_cast<M>(lab[v]);
+    return mv;
 }
 
 // run_to_directory (pipeline.cpp:30-53): seed from cfg (integrator.cpp:32-50, D-masked), run on

@@ -17,6 +17,7 @@
 #include "gliosim/config.hpp"
 #include "gliosim/expact.hpp"
 #include "gliosim/fields.hpp"
+#include "gliosim/imaging.hpp"
 #include "gliosim/integrator.hpp"
 #include "gliosim/pipeline.hpp"
 #include "gliosim/stencil.hpp"
@@ -154,6 +155,47 @@ int main() {
     gate(rr.metrics.size() == rg.metrics.size(), "run_to_directory: metrics rows", 0.0);
     std::filesystem::remove_all(dir_ref);
     std::filesystem::remove_all(dir_gpu);
+
+    // imaging: PGM stack -> resample on the GPU, label files, matter fractions
+    {
+        const int W = 53, H = 41, S = 7;
+        gliosim::ImageStack st;
+        st.width = W;
+        st.height = H;
+        st.num_slices = S;
+        st.intensities.resize(static_cast<size_t>(W) * H * S);
+        uint64_t x = 0x9e3779b97f4a7c15ull;
+        for (auto& b : st.intensities) {
+            x ^= x << 13;
+            x ^= x >> 7;
+            x ^= x << 17;
+            const int r = static_cast<int>(x % 100);
+            b = static_cast<uint8_t>(r < 10 ? 0 : r < 60 ? 150 + r : r < 90 ? 232 + r % 8 : 250);
+        }
+        std::vector<std::string> paths;
+        for (int z = 0; z < S; ++z) {
+            const std::string p = tmp + "/gs_dropin_slice_" + std::to_string(z) + ".pgm";
+            std::ofstream o(p, std::ios::binary);
+            o << "P5\n# dropin\n" << W << ' ' << H << "\n255\n";
+            o.write(reinterpret_cast<const char*>(st.intensities.data()) + static_cast<size_t>(z) * W * H, W * H);
+            paths.push_back(p);
+        }
+        const gliosim::ImageStack a = gliosim::load_stack(paths);
+        const auto b = gliosim_b200::load_stack<gliosim::ImageStack>(paths);
+        gate(a.intensities == b.intensities && a.width == b.width && a.num_slices == b.num_slices,
+             "load_stack bytes", 0.0);
+        const gliosim::Grid g(40, 36, 20, 2.0);
+        const gliosim::MaterialVolume mr = gliosim::resample(a, g, cfg);
+        const auto mg = gliosim_b200::resample<gliosim::MaterialVolume>(b, g, cfg);
+        gate(mr.labels == mg.labels, "resample (GPU) labels exact", 0.0);
+        const auto fr = gliosim::matter_fractions(mr);
+        const auto fg = gliosim_b200::matter_fractions(mg);
+        gate(fr.white == fg.white && fr.gray == fg.gray, "matter_fractions exact", fg.white);
+        gliosim_b200::write_label_volume(mg, tmp + "/gs_dropin_labels.raw");
+        gate(gliosim::read_label_volume(tmp + "/gs_dropin_labels.raw", g).labels == mr.labels, "label volume", 0.0);
+        for (const auto& p : paths) std::filesystem::remove(p);
+        std::filesystem::remove(tmp + "/gs_dropin_labels.raw");
+    }
 
     std::printf("%s\n", fails ? "dropin parity: FAILED" : "dropin parity: all passed");
     return fails ? 1 : 0;
