@@ -174,7 +174,7 @@ def slab_of(w, labels, u0, depth):
     return labels[sl].copy(), u0[sl].copy()
 
 
-def cpu_reference_sample(w, labels, u0, target_s, steps=None, warmup=0, gpu_terms_of=None, rho=None):
+def cpu_reference_sample(w, labels, u0, target_s, steps=None, warmup=0, gpu_terms_of=None, rho=None, cores=None):
     """Time the reference's own run() loop (RunTimings::step_seconds, integrator.cpp:123-125)
     on a slab with workers = all host cores; the C port stands in only if oracle/_ref is
     absent.  `steps` fixed -> exactly that many timed steps after `warmup` untimed ones;
@@ -189,7 +189,7 @@ def cpu_reference_sample(w, labels, u0, target_s, steps=None, warmup=0, gpu_term
         ref = None
         kind = "port"
     from paper_2402_02273_b200 import workloads as W
-    cores = os.cpu_count() or 1
+    cores = cores or os.cpu_count() or 1
     depth = w.nz if w.n <= 128 ** 3 else 16
     lab_s, u_s = slab_of(w, labels, u0, depth)
     shape = (w.nx, w.ny, depth)
@@ -342,6 +342,13 @@ def run_ours(args, w, rank, world, local):
                               f"extrapolated by voxel count to {full_s:.1f} s per {w.nx}x{w.ny}x{w.nz} step; slab Taylor "
                               f"terms/step {np.mean(sample['terms_slab']) if sample['terms_slab'] else float('nan'):.1f} "
                               f"vs full grid {np.mean(terms):.1f}")}
+            # the reference with workers = 1 as well (one timed step of the slab)
+            if sample["kind"] == "reference" and sample["cores"] > 1:
+                one = cpu_reference_sample(w, labels, u0, args.cpu_seconds, steps=1, cores=1)
+                v1, full1 = extrapolate(one, w.n)
+                cpu.update({"value_1core": v1,
+                            "sample_1core": (f"1 gliosim::step (workers=1) on the same slab, {one['step_times'][0]:.2f} s, "
+                                             f"extrapolated to {full1:.1f} s per full step")})
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "unavailable",
                    "sample": f"failed: {e}"}
@@ -369,6 +376,7 @@ def run_ours(args, w, rank, world, local):
         "taylor_terms_per_s": world * sum(terms) / (ms / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "frac_of_spec_8000GBs": achieved / 8000.0,
                      "kernel": "gs::taylor_kernel (cooperative; one launch per step, fused two-term sweeps)",
                      "launches": taylor_n, "avg_launch_ms": taylor_ms / max(taylor_n, 1),
                      "share_of_step": taylor_ms / ms,
