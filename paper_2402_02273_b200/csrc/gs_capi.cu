@@ -431,9 +431,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             int border_blocks = sb;
             void* args[] = {&p, &border_blocks, &step};
             GS_CUDA(c, ev(2));
-            GS_CUDA(c, cudaLaunchCooperativeKernel(p.fuse == 3 ? reinterpret_cast<void*>(gs::taylor_kernel<3>)
-                                                                 : reinterpret_cast<void*>(gs::taylor_kernel<2>),
-                                                   dim3(gb), blk, args, dyn,
+            GS_CUDA(c, cudaLaunchCooperativeKernel(gs::taylor_kernel_fn(p.fuse), dim3(gb), blk, args, dyn,
                                                    c->stream));
             GS_CUDA(c, ev_end());
             GS_CUDA(c, ev(3));
@@ -520,16 +518,15 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
         return GS_ECUDA;
     }
     c->num_sms = prop.multiProcessorCount;
-    for (const void* fn : {reinterpret_cast<const void*>(gs::taylor_kernel<2>), reinterpret_cast<const void*>(gs::taylor_kernel<3>),
-                           reinterpret_cast<const void*>(gs::prep_kernel)})
+    for (const void* fn : {gs::taylor_kernel_fn(2), gs::taylor_kernel_fn(3), reinterpret_cast<const void*>(gs::prep_kernel)})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kDynSmemBytes)) != cudaSuccess)
             return bail(e, "cudaFuncSetAttribute(smem)");
     int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::taylor_kernel<2>, gs::kSolveThreads,
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::taylor_kernel_fn(2), gs::kSolveThreads,
                                                            gs::kDynSmemBytes)) != cudaSuccess)
         return bail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     int per_sm3 = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, gs::taylor_kernel<3>, gs::kSolveThreads,
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, gs::taylor_kernel_fn(3), gs::kSolveThreads,
                                                            gs::kDynSmemBytes)) != cudaSuccess)
         return bail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     per_sm = std::min(per_sm, per_sm3);
@@ -701,6 +698,7 @@ gs_status gs_set_diffusion(gs_ctx* c, const double* d) {
     std::vector<uint64_t> keys(static_cast<size_t>(c->n));
     std::memcpy(keys.data(), d, sizeof(double) * keys.size());
     std::vector<uint64_t> uniq(keys);
+    uniq.push_back(0);  // palette index 0 is always D = +0.0: TMA zero-fill outside the grid reads it
     std::sort(uniq.begin(), uniq.end());
     uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
     c->has_labels = false;

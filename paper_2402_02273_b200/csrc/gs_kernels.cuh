@@ -153,8 +153,8 @@ __global__ void label_count_kernel(const uint8_t* labels, int64_t n, unsigned lo
 __global__ void metrics_kernel(const __grid_constant__ SolveParams p);
 __global__ void prep_kernel(const __grid_constant__ SolveParams p, int step);
 __global__ void border_kernel(const __grid_constant__ SolveParams p, int prep_blocks, int step);
-template <int FUSE>
-__global__ void taylor_kernel(const __grid_constant__ SolveParams p, int border_blocks, int step);
+// Taylor kernel for FUSE terms per TMA pass (2 or 3), as a launchable handle.
+const void* taylor_kernel_fn(int fuse);
 __global__ void update_kernel(const __grid_constant__ SolveParams p, int step);
 
 }  // namespace gs

@@ -400,7 +400,6 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
         const double ncxy0 = -static_cast<double>(cxy + (gy0 > 0) + (gy0 < op.ny - 1));
         const double ncxy1 = -static_cast<double>(cxy + (gy0 + 1 > 0) + (gy0 + 1 < op.ny - 1));
         const int rgx = x0 - 1 + rc, rgy = y0 - 1 + rr;
-        const bool rin = ringer && rgx >= 0 && rgx < op.nx && rgy >= 0 && rgy < op.ny;
         const double rncxy = -static_cast<double>((rgx > 0) + (rgx < op.nx - 1) + (rgy > 0) + (rgy < op.ny - 1));
         const int64_t v0 = gx + static_cast<int64_t>(gy0) * op.sy;
 
@@ -411,7 +410,6 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
         auto phaseA = [&](int pl, int tslot, int sm_, int sc_, int sp_, const double (&xm)[2], const double (&xc)[2],
                           const double (&xp)[2], double (&t1)[2], double (&lw)[2]) {
             double* T1 = ring.t1(tslot);
-            const bool zin = pl >= 0 && pl < op.nz;
             const double dhz = static_cast<double>((pl > 0) + (pl < op.nz - 1));
             const double* Xc = ring.x(sc_);
             const uint8_t* L = ring.l(sc_);
@@ -433,8 +431,11 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                     s1 = __dadd_rn(s1, B[oB + kXPitch]);
                 }
             }
-            const double v0_ = (zin && in0) ? __dmul_rn(c1, s0) : 0.0;
-            const double v1_ = (zin && in1) ? __dmul_rn(c1, s1) : 0.0;
+            // Outside the grid (planes -1 / nz, rows or columns past the edge) TMA zero-fills
+            // the labels, and palette index 0 is always D = 0: the row is dead, s = 0 and T1 is
+            // a signed zero, which as a neighbour adds nothing (accumulators start at +0.0).
+            const double v0_ = __dmul_rn(c1, s0);
+            const double v1_ = __dmul_rn(c1, s1);
             t1[0] = v0_;
             t1[1] = v1_;
             T1[oT] = v0_;
@@ -451,7 +452,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                                       Xc[rX + 1], Xc[rX + kXPitch], Xp[rX]);
                     if (KIND == k2FirstBorder) sc = __dadd_rn(sc, B[rB]);
                 }
-                T1[rT] = (zin && rin) ? __dmul_rn(c1, sc) : 0.0;
+                T1[rT] = __dmul_rn(c1, sc);
             }
         };
 
@@ -474,7 +475,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             xb[1] = X2[oX + kXPitch];
         }
         // own T1 of planes z-2, z-1, z (relative to the loop's z); w unused here
-        double tm2[2] = {0.0, 0.0}, tm1[2], t0[2], lwd[2];
+        double tm1[2], t0[2], lwd[2];
         phaseA(z0 - 1, 0, s0, s1, s2, xz, xa, xb, tm1, lwd);
         wait_slot(s3);
         if (needX) {
@@ -1599,6 +1600,11 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
 // ------------------------------------------------------------------------------------------
 template __global__ void taylor_kernel<2>(const __grid_constant__ SolveParams, int, int);
 template __global__ void taylor_kernel<3>(const __grid_constant__ SolveParams, int, int);
+
+// Host-side handles of the instantiations (kept in this translation unit).
+const void* taylor_kernel_fn(int fuse) {
+    return fuse == 3 ? reinterpret_cast<const void*>(taylor_kernel<3>) : reinterpret_cast<const void*>(taylor_kernel<2>);
+}
 
 __global__ void __launch_bounds__(kSolveThreads) update_kernel(const __grid_constant__ SolveParams p, int step) {
     __shared__ Smem sm;
