@@ -537,22 +537,20 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 }
                 const double f10 = __dadd_rn(fp0, T3[r][0]), f11 = __dadd_rn(fp1, T3[r][1]);
                 const double f20 = __dadd_rn(f10, t20), f21 = __dadd_rn(f11, t21);
-                // fmax drops NaN like std::max(m, |x|) (m is never NaN): expact.cpp:15-19
+                // The maxima drop NaN like std::max(m, |x|) (m is never NaN): expact.cpp:15-19.
+                // They need no domain test: past the grid edge every input is zero-filled and the
+                // row is dead (palette index 0), so T1, T2, F1 and F2 are signed zeros there.
+                mx[0] = max_abs(max_abs(mx[0], T3[r][0]), T3[r][1]);
+                mx[1] = max_abs(max_abs(mx[1], f10), f11);
+                mx[2] = max_abs(max_abs(mx[2], t20), t21);
+                mx[3] = max_abs(max_abs(mx[3], f20), f21);
                 if (in0) {
                     pT[0] = t20;
                     pF[0] = f10;
-                    mx[0] = max_abs(mx[0], T3[r][0]);
-                    mx[1] = max_abs(mx[1], f10);
-                    mx[2] = max_abs(mx[2], t20);
-                    mx[3] = max_abs(mx[3], f20);
                 }
                 if (in1) {
                     pT[op.sy] = t21;
                     pF[op.sy] = f11;
-                    mx[0] = max_abs(mx[0], T3[r][1]);
-                    mx[1] = max_abs(mx[1], f11);
-                    mx[2] = max_abs(mx[2], t21);
-                    mx[3] = max_abs(mx[3], f21);
                 }
                 pT += op.sz;
                 pF += op.sz;
