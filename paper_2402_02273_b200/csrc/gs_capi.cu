@@ -329,7 +329,12 @@ void fill_rtab(double tol, double* rtab) {
 
 // Grid sizes of the launch sequence.  prep/taylor: one CTA per SM (the TMA rings take most
 // of shared memory); border/update/metrics: streaming kernels, two CTAs per SM.
-int stream_blocks(const gs_ctx* c) { return 2 * c->num_sms; }
+// Small grids get fewer streaming CTAs (>= 8 voxels per thread): their per-block reductions,
+// tickets and partial-sum trees cost more than the sweep itself at 32^3.
+int stream_blocks(const gs_ctx* c) {
+    const int64_t want = (c->n + 8 * gs::kSolveThreads - 1) / (8 * gs::kSolveThreads);
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 2 * c->num_sms)));
+}
 
 gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* metrics, gs_step_info* infos) {
     const int gb = c->grid_blocks;        // prep / taylor (co-resident)
