@@ -424,7 +424,39 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             gs::metrics_kernel<<<sb, blk, 0, c->stream>>>(p);
             GS_CUDA(c, cudaGetLastError());
         }
-        for (int step = 0; step < steps; ++step) {
+        // Runs of several steps replay one captured step as a CUDA graph: the four kernels'
+        // ~4 KB parameter blocks are uploaded once, and the step index lives on the device
+        // (advance_kernel).  Timing/trace modes and a failed capture use direct launches.
+        bool graphed = false;
+        if (p.mode == gs::kModeRun && steps >= 2 && !c->ktime && c->trace_cap == 0 &&
+            std::getenv("GS_NO_GRAPH") == nullptr) {
+            cudaGraph_t graph = nullptr;
+            cudaGraphExec_t exec = nullptr;
+            int border_blocks = sb, neg = -1;
+            void* args[] = {&p, &border_blocks, &neg};
+            bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                gs::prep_kernel<<<gb, blk, dyn, c->stream>>>(p, -1);
+                gs::border_kernel<<<sb, blk, 0, c->stream>>>(p, gb, -1);
+                cudaLaunchCooperativeKernel(gs::taylor_kernel_fn(p.fuse), dim3(gb), blk, args, dyn, c->stream);
+                gs::update_kernel<<<sb, blk, 0, c->stream>>>(p, -1);
+                gs::advance_kernel<<<1, 1, 0, c->stream>>>(p.ctrl);
+                ok = cudaStreamEndCapture(c->stream, &graph) == cudaSuccess && graph != nullptr;
+                ok = ok && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+            }
+            cudaError_t le = cudaSuccess;
+            if (ok) {
+                for (int step = 0; step < steps && le == cudaSuccess; ++step) le = cudaGraphLaunch(exec, c->stream);
+                graphed = true;
+            } else {
+                cudaGetLastError();  // nothing ran during the capture: fall back to direct launches
+            }
+            if (graphed && le == cudaSuccess) le = cudaStreamSynchronize(c->stream);  // before destroying
+            if (exec) cudaGraphExecDestroy(exec);
+            if (graph) cudaGraphDestroy(graph);
+            GS_CUDA(c, le);
+        }
+        for (int step = 0; step < steps && !graphed; ++step) {
             GS_CUDA(c, ev(0));
             gs::prep_kernel<<<gb, blk, dyn, c->stream>>>(p, step);
             GS_CUDA(c, cudaGetLastError());

@@ -93,6 +93,7 @@ struct Ctrl {
     int fres, tres;       // Taylor result: F[fres] (+ T[tres] when implicit)
     unsigned int ticket;  // last-block-done counter (metrics)
     int ntrace;
+    int step;             // current step of a graph-replayed run (kernels launched with step < 0)
 };
 
 struct SolveParams {
@@ -153,6 +154,8 @@ __global__ void label_count_kernel(const uint8_t* labels, int64_t n, unsigned lo
 __global__ void metrics_kernel(const __grid_constant__ SolveParams p);
 __global__ void prep_kernel(const __grid_constant__ SolveParams p, int step);
 __global__ void border_kernel(const __grid_constant__ SolveParams p, int prep_blocks, int step);
+// ctrl->step += 1: closes one step of a CUDA-graph replayed run.
+__global__ void advance_kernel(Ctrl* ctrl);
 // Taylor kernel for FUSE terms per TMA pass (2 or 3), as a launchable handle.
 const void* taylor_kernel_fn(int fuse);
 __global__ void update_kernel(const __grid_constant__ SolveParams p, int step);

@@ -1116,6 +1116,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) prep_kernel(const __grid_con
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_constant__ SolveParams p, int prep_blocks,
                                                                int step) {
+    if (step < 0) step = __ldcg(&p.ctrl->step);  // graph replay: the step lives on the device
     __shared__ Smem sm;
     Ctrl* ctrl = p.ctrl;
     if (ctrl->status) return;
@@ -1205,6 +1206,7 @@ __global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_cons
 template <int FUSE>
 __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_constant__ SolveParams p,
                                                                   int border_blocks, int step) {
+    if (step < 0) step = __ldcg(&p.ctrl->step);  // graph replay: the step lives on the device
     cg::grid_group grid = cg::this_grid();
     __shared__ Smem sm;
     extern __shared__ __align__(128) unsigned char dyn[];
@@ -1593,18 +1595,22 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
     if (p.use_tma) fence_proxy_async_global();
 }
 
-// ------------------------------------------------------------------------------------------
-// K5 update: u <- u + tau * (gamma/tau) * y (run, + compute_metrics) or out = scale * y
-// ------------------------------------------------------------------------------------------
 template __global__ void taylor_kernel<2>(const __grid_constant__ SolveParams, int, int);
 template __global__ void taylor_kernel<3>(const __grid_constant__ SolveParams, int, int);
+
+__global__ void advance_kernel(Ctrl* ctrl) { ctrl->step += 1; }
 
 // Host-side handles of the instantiations (kept in this translation unit).
 const void* taylor_kernel_fn(int fuse) {
     return fuse == 3 ? reinterpret_cast<const void*>(taylor_kernel<3>) : reinterpret_cast<const void*>(taylor_kernel<2>);
 }
 
+// ------------------------------------------------------------------------------------------
+// K5 update: u <- u + tau * (gamma/tau) * y (run, + compute_metrics) or out = scale * y
+// ------------------------------------------------------------------------------------------
+
 __global__ void __launch_bounds__(kSolveThreads) update_kernel(const __grid_constant__ SolveParams p, int step) {
+    if (step < 0) step = __ldcg(&p.ctrl->step);  // graph replay: the step lives on the device
     __shared__ Smem sm;
     const Ctrl* ctrl = p.ctrl;
     if (__ldcg(&ctrl->status)) return;
