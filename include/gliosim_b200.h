@@ -145,6 +145,10 @@ gs_status gs_get_trace(gs_ctx* ctx, uint64_t* pairs, int capacity, int* count);
  * [0] prep (RHS), [1] border, [2] taylor (the Taylor-term kernel), [3] update. */
 gs_status gs_set_kernel_timing(gs_ctx* ctx, int enable);
 gs_status gs_get_kernel_times(gs_ctx* ctx, double ms[4], int launches[4]);
+/* 1 when gs_run on this context takes the small-grid path: one thread-block cluster runs
+ * every step with the state in distributed shared memory (grids up to 40 K voxels;
+ * GS_NO_CLUSTER=1 disables it).  The kernel times then report it as the Taylor kernel. */
+int gs_uses_cluster(const gs_ctx* ctx);
 
 /* ---- snapshot and metrics files (vtk.hpp:15-45, src/vtk.cpp:59-157) ------------------- */
 /* write_vtk (vtk.cpp:59-91): legacy ASCII VTK, header + one "%.17g" value per line, then,

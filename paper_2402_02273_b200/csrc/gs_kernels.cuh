@@ -154,6 +154,27 @@ __global__ void label_count_kernel(const uint8_t* labels, int64_t n, unsigned lo
 __global__ void metrics_kernel(const __grid_constant__ SolveParams p);
 __global__ void prep_kernel(const __grid_constant__ SolveParams p, int step);
 __global__ void border_kernel(const __grid_constant__ SolveParams p, int prep_blocks, int step);
+// Small grids: whole runs in one thread-block cluster (gs_cluster.cu).
+constexpr int kClusterCTAs = 16;  // non-portable cluster size (opt-in attribute)
+struct ClusterParams {
+    StencilOp op;            // palette mode: pal + wtab
+    int n_steps, want_metrics;
+    int64_t slice, halo;     // voxels per CTA, halo width (one plane, or one row in 2-D)
+    double rho, tau, tol, anorm;
+    double rtab[kMaxDegree + 1];
+    double* u;               // resident state: read at the start, written at the end
+    double* metrics;         // [(n_steps+1)*4] or nullptr
+    gs_step_info* infos;     // [n_steps] or nullptr
+    Ctrl* ctrl;
+    double origin[3], center[3], h, front_threshold;
+};
+// Dynamic shared memory of cluster_run_kernel per CTA (5 haloed vectors, b/gamma, labels,
+// neighbour masks).
+inline size_t cluster_smem_bytes(int64_t slice, int64_t halo) {
+    return static_cast<size_t>(5 * (slice + 2 * halo) + slice) * 8 + 2 * ((static_cast<size_t>(slice) + 15) / 16) * 16;
+}
+__global__ void cluster_run_kernel(const __grid_constant__ ClusterParams p);
+
 // ctrl->step += 1: closes one step of a CUDA-graph replayed run.
 __global__ void advance_kernel(Ctrl* ctrl);
 // Taylor kernel for FUSE terms per TMA pass (2 or 3), as a launchable handle.

@@ -301,6 +301,10 @@ class StencilOperator:
         self._check(self.lib.gs_get_trace(self.ctx, buf, cap, C.byref(n)))
         return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(n.value)]
 
+    def uses_cluster(self) -> bool:
+        """True when gs_run takes the small-grid single-cluster path."""
+        return bool(self.lib.gs_uses_cluster(self.ctx))
+
     def set_kernel_timing(self, enable: bool):
         """CUDA-event timing of every kernel launch of later calls (on the context's stream)."""
         self._check(self.lib.gs_set_kernel_timing(self.ctx, 1 if enable else 0))

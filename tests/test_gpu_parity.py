@@ -119,8 +119,13 @@ def test_phi1v_expmv_stencil_kats(G, kat, port):
 
 # ---- exponential-Euler step and run ---------------------------------------------------------
 
+@pytest.mark.parametrize("path", ["auto", "multikernel"])
 @pytest.mark.parametrize("name", RUN_NAMES)
-def test_step_parity_per_step(G, port, runs_kat, name):
+def test_step_parity_per_step(G, port, runs_kat, name, path, monkeypatch):
+    """Every step of the reference's trajectories; "auto" takes the single-cluster path on
+    grids it fits, "multikernel" forces the launch sequence of the large-grid path."""
+    if path == "multikernel":
+        monkeypatch.setenv("GS_NO_CLUSTER", "1")
     c = case(runs_kat, name)
     grid = G.Grid(*c["shape"], h=c["h"])
     d_oracle = port.diffusion_from_labels(c["labels"])
@@ -139,8 +144,11 @@ def test_step_parity_per_step(G, port, runs_kat, name):
             assert info.stage_terms() == log.stage_terms()
 
 
+@pytest.mark.parametrize("path", ["auto", "multikernel"])
 @pytest.mark.parametrize("name", RUN_NAMES)
-def test_run_parity_full(G, runs_kat, name):
+def test_run_parity_full(G, runs_kat, name, path, monkeypatch):
+    if path == "multikernel":
+        monkeypatch.setenv("GS_NO_CLUSTER", "1")
     c = case(runs_kat, name)
     steps = len(c["states"]) - 1
     grid = G.Grid(*c["shape"], h=c["h"])
@@ -290,10 +298,13 @@ TMA_SHAPES = [(48, 32, 20), (80, 40, 12), (64, 48, 1), (32, 32, 32), (16, 16, 16
 
 
 @pytest.mark.parametrize("shape", TMA_SHAPES)
-@pytest.mark.parametrize("path", ["tma2", "tma3", "l1"])
+@pytest.mark.parametrize("path", ["cluster", "tma2", "tma3", "l1"])
 def test_sweep_paths_vs_oracle(G, port, shape, path, monkeypatch):
-    """Every sweep implementation: fused two-term TMA (default), fused three-term TMA
-    (GS_FUSE=3) and the L1 single-term fallback -- bitwise against the oracle."""
+    """Every sweep implementation: the single-cluster small-grid path, fused two-term TMA,
+    fused three-term TMA (GS_FUSE=3) and the L1 single-term fallback -- bitwise against the
+    oracle."""
+    if path != "cluster":
+        monkeypatch.setenv("GS_NO_CLUSTER", "1")
     if path == "l1":
         monkeypatch.setenv("GS_DISABLE_TMA", "1")
     if path == "tma3":
@@ -307,6 +318,8 @@ def test_sweep_paths_vs_oracle(G, port, shape, path, monkeypatch):
     x = rng.uniform(-1, 1, n)
     u = rng.uniform(0, 1, n)
     with G.assemble_diffusion(G.Grid(*shape, h=h), d) as op:
+        if path == "cluster" and not op.uses_cluster():
+            pytest.skip("grid too large (or too thin) for the single-cluster path")
         assert np.array_equal(op.apply(x), port.apply(op_o, x))
         got, info = G.step(op, u, 0.1, 33.5, 1e-9, info=True)
         want, log = port.step(op_o, u, 0.1, 33.5, 1e-9, bnorm=info.bnorm, coln=info.coln)
