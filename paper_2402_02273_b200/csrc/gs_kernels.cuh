@@ -50,7 +50,7 @@ constexpr int k2LBytes = ((kTmaTY + 2) * kLPitch + 127) / 128 * 128;   // 18 x 9
 // F (own, next-kind) and b/gamma (halo, first-kind) are never needed by the same sweep: one region.
 constexpr int k2FBBytes = kOBytes > k2BBytes ? kOBytes : k2BBytes;
 constexpr int k2SlotBytes = k2XBytes + k2FBBytes + k2LBytes;
-constexpr int kT1Pitch = kTmaTX + 2;
+constexpr int kT1Pitch = kXPitch;  // same pitch as the X tile: T1, b/gamma and X offsets differ by constants
 constexpr int kT1Rows = kTmaTY + 2;
 constexpr int kT1Bytes = kT1Rows * kT1Pitch * 8;
 constexpr int kT1Planes = 3;  // T1(z+1) is written while T1(z-1) is read; T1(z) is kept for the next iteration

@@ -330,9 +330,9 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
     const int xl = tid & (kTmaTX - 1);
     const int ry0 = 2 * (tid / kTmaTX);
     const int oX = (ry0 + 2) * kXPitch + xl + kXHalo;   // own row 0 in the X halo-2 tile
-    const int oT = (ry0 + 1) * kT1Pitch + xl + 1;       // own row 0 in a T1 plane
+    const int oT = oX - kXPitch - 1;                    // own row 0 in a T1 plane (same pitch)
     const int oL = (ry0 + 1) * kLPitch + xl + kLHaloX;  // own row 0 in the label tile
-    const int oB = (ry0 + 1) * kXPitch + xl + kXHalo;   // own row 0 in the b/gamma tile
+    const int oB = oX - kXPitch;                        // own row 0 in the b/gamma tile
     const int oF = ry0 * kTmaTX + xl;                   // own row 0 in the F tile
     // this thread's ring point (rows -1 and 16, then columns -1 and 64)
     const bool ringer = tid < kRing;
@@ -347,8 +347,8 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             rc = (e & 1) ? kTmaTX + 1 : 0;
         }
     }
-    const int rX = (rr + 1) * kXPitch + rc + 1, rT = rr * kT1Pitch + rc, rL = rr * kLPitch + rc + kLHaloX - 1,
-              rB = rr * kXPitch + rc + 1;
+    const int rX = (rr + 1) * kXPitch + rc + 1, rT = rX - kXPitch - 1, rL = rr * kLPitch + rc + kLHaloX - 1,
+              rB = rX - kXPitch;
 
     const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
     const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
