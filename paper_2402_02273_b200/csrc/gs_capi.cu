@@ -388,6 +388,8 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     // Taylor terms per fused sweep (GS_FUSE=2|3 overrides the default for A/B measurements)
     p.fuse = kDefaultFuse;
     if (const char* f = std::getenv("GS_FUSE")) p.fuse = std::atoi(f) == 3 ? 3 : 2;
+    // thin grids (2-D and a few planes): the two-term sweep that skips the planes past the grid
+    if (p.fuse == 2 && c->nz < 8) p.fuse = 4;
     p.metrics = metrics ? c->metrics.as<double>() : nullptr;
     p.want_metrics = metrics ? 1 : 0;
     p.infos = infos ? c->infos.as<gs_step_info>() : nullptr;
@@ -608,7 +610,8 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
         return GS_ECUDA;
     }
     c->num_sms = prop.multiProcessorCount;
-    for (const void* fn : {gs::taylor_kernel_fn(2), gs::taylor_kernel_fn(3), reinterpret_cast<const void*>(gs::prep_kernel)})
+    for (const void* fn : {gs::taylor_kernel_fn(2), gs::taylor_kernel_fn(3), gs::taylor_kernel_fn(4),
+                           reinterpret_cast<const void*>(gs::prep_kernel)})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kDynSmemBytes)) != cudaSuccess)
             return bail(e, "cudaFuncSetAttribute(smem)");
     int per_sm = 0;

@@ -177,7 +177,8 @@ __global__ void cluster_run_kernel(const __grid_constant__ ClusterParams p);
 
 // ctrl->step += 1: closes one step of a CUDA-graph replayed run.
 __global__ void advance_kernel(Ctrl* ctrl);
-// Taylor kernel for FUSE terms per TMA pass (2 or 3), as a launchable handle.
+// Taylor kernel as a launchable handle: FUSE = 2 or 3 Taylor terms per TMA pass, 4 = two
+// terms with the past-the-grid planes skipped (thin grids).
 const void* taylor_kernel_fn(int fuse);
 __global__ void update_kernel(const __grid_constant__ SolveParams p, int step);
 

@@ -308,7 +308,10 @@ struct Ring2 {
     }
 };
 
-template <int KIND>
+// kSkipOut: planes past the grid skip their (all-zero) T1 stencil work -- worth it on thin
+// grids (2-D: two of every three T1 planes), a separate instantiation so the deep-grid
+// kernel's code is unchanged.
+template <int KIND, bool kSkipOut = false>
 __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ring, int xbuf, int fbuf, int bbuf,
                                            double c1, double c2, double* outT, double* outF, double (&mx)[4],
                                            uint32_t& seq, uint32_t& phase_mask, const double* s_wtab) {
@@ -410,6 +413,15 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
         auto phaseA = [&](int pl, int tslot, int sm_, int sc_, int sp_, const double (&xm)[2], const double (&xc)[2],
                           const double (&xp)[2], double (&t1)[2], double (&lw)[2]) {
             double* T1 = ring.t1(tslot);
+            if (kSkipOut && static_cast<unsigned>(pl) >= static_cast<unsigned>(op.nz)) {
+                // a plane past the grid (z = -1 or nz): T1 is all zero there -- no stencil work
+                // (2-D grids would otherwise compute three planes per useful one)
+                t1[0] = t1[1] = 0.0;
+                T1[oT] = 0.0;
+                T1[oT + kT1Pitch] = 0.0;
+                if (ringer) T1[rT] = 0.0;
+                return;
+            }
             const double dhz = static_cast<double>((pl > 0) + (pl < op.nz - 1));
             const double* Xc = ring.x(sc_);
             const uint8_t* L = ring.l(sc_);
@@ -1464,14 +1476,18 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                     const int xb_ = xb < 0 ? 0 : xb, fb_ = fb < 0 ? 0 : fb;
                     double* oT = p.buf[tout];
                     double* oF = p.buf[fout];
+                    constexpr bool kSkip = FUSE == 4;
                     if (kind == k2Next)
-                        sweep2_tma<k2Next>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                        sweep2_tma<k2Next, kSkip>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
                     else if (kind == k2FirstBorder)
-                        sweep2_tma<k2FirstBorder>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                        sweep2_tma<k2FirstBorder, kSkip>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2,
+                                                         sm.wtab);
                     else if (kind == k2FirstZero)
-                        sweep2_tma<k2FirstZero>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                        sweep2_tma<k2FirstZero, kSkip>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2,
+                                                       sm.wtab);
                     else
-                        sweep2_tma<k2FirstPlain>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
+                        sweep2_tma<k2FirstPlain, kSkip>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2,
+                                                        sm.wtab);
                 }
                 block_reduce<4, true>(mx, sm);
                 if (threadIdx.x == 0) {
@@ -1597,12 +1613,15 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
 
 template __global__ void taylor_kernel<2>(const __grid_constant__ SolveParams, int, int);
 template __global__ void taylor_kernel<3>(const __grid_constant__ SolveParams, int, int);
+template __global__ void taylor_kernel<4>(const __grid_constant__ SolveParams, int, int);
 
 __global__ void advance_kernel(Ctrl* ctrl) { ctrl->step += 1; }
 
 // Host-side handles of the instantiations (kept in this translation unit).
 const void* taylor_kernel_fn(int fuse) {
-    return fuse == 3 ? reinterpret_cast<const void*>(taylor_kernel<3>) : reinterpret_cast<const void*>(taylor_kernel<2>);
+    return fuse == 3   ? reinterpret_cast<const void*>(taylor_kernel<3>)
+           : fuse == 4 ? reinterpret_cast<const void*>(taylor_kernel<4>)
+                       : reinterpret_cast<const void*>(taylor_kernel<2>);
 }
 
 // ------------------------------------------------------------------------------------------
