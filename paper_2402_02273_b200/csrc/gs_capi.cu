@@ -110,6 +110,9 @@ struct gs_ctx {
 
     gs::StencilOp op{};
     int grid_blocks = 0;
+    // gs_step_host: the state's H2D / D2H ride in the launch sequence (one synchronisation)
+    const double* stage_in = nullptr;
+    double* stage_out = nullptr;
     // small-grid path (gs_cluster.cu): one 16-CTA cluster runs whole gs_run calls
     int64_t cl_slice = 0, cl_halo = 0;
     size_t cl_smem = 0;
@@ -364,6 +367,9 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     const unsigned long long ms_init[4] = {0ull, ~0ull, 0ull, 0ull};
     GS_CUDA(c, cudaMemcpyAsync(c->mslots.p, ms_init, sizeof ms_init, cudaMemcpyHostToDevice, c->stream));
     GS_CUDA(c, cudaMemsetAsync(c->ctrl.p, 0, sizeof(gs::Ctrl), c->stream));
+    if (c->stage_in)
+        GS_CUDA(c, cudaMemcpyAsync(c->u.p, c->stage_in, sizeof(double) * static_cast<size_t>(c->n),
+                                   cudaMemcpyHostToDevice, c->stream));
     if (metrics) GS_CUDA(c, c->metrics.alloc(sizeof(double) * 4 * (n_steps + 1)));
     if (infos) {
         GS_CUDA(c, c->infos.alloc(sizeof(gs_step_info) * std::max(1, n_steps)));
@@ -532,6 +538,9 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             GS_CUDA(c, ev_end());
         }
     }
+    if (c->stage_out)
+        GS_CUDA(c, cudaMemcpyAsync(c->stage_out, c->u.p, sizeof(double) * static_cast<size_t>(c->n),
+                                   cudaMemcpyDeviceToHost, c->stream));
     gs::Ctrl ctrl{};
     GS_CUDA(c, cudaMemcpyAsync(&ctrl, c->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, c->stream));
     if (metrics)
@@ -1032,11 +1041,14 @@ gs_status gs_step(gs_ctx* c, double rho, double tau, double tol, gs_step_info* i
 
 gs_status gs_step_host(gs_ctx* c, const double* u, double rho, double tau, double tol, double* out,
                        gs_step_info* info) {
-    gs_status st = gs_set_state(c, u);
-    if (st != GS_OK) return st;
-    st = gs_step(c, rho, tau, tol, info);
-    if (st != GS_OK) return st;
-    return gs_get_state(c, out);
+    if (!c || !u || !out) return fail(c, GS_EINVAL, "gs_step_host: null argument");
+    // u in, one step, u' out on the context's stream with a single synchronisation
+    c->stage_in = u;
+    c->stage_out = out;
+    const gs_status st = gs_step(c, rho, tau, tol, info);
+    c->stage_in = nullptr;
+    c->stage_out = nullptr;
+    return st;
 }
 
 gs_status gs_seed_initial(gs_ctx* c, const double origin[3], double amplitude, double width, const double center[3],
