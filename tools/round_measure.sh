@@ -1,15 +1,14 @@
 # Round-end measurement batch (run on the GPU box from the repo root):
 #   bash tools/round_measure.sh
-# GPU tests, the C4 bench line (both arms), the ncu launch list of the same command, and one
-# ncu --set full capture of the Taylor kernel (each ncu pass only after its command exited 0).
+# GPU tests, the C4 bench line (both arms), the ncu launch list of the same default bench command,
+# and one ncu --set full capture of the Taylor kernel (each ncu pass only after its command exited 0).
 set -u
 mkdir -p gpurun_out
 timeout 1800 python -m pytest tests -m gpu -q -x > gpurun_out/m_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/m_tests.log
 timeout 900 python bench.py > gpurun_out/m_bench.json 2> gpurun_out/m_bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference > gpurun_out/m_bench_ref.json 2> gpurun_out/m_bench_ref.err; echo "ref rc=$?"
-timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/m_small.json 2>/dev/null && \
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/m_launches.csv \
-    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/m_ncu_launch.log 2>&1; echo "launches rc=$?"
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/m_launches.csv \
+    python bench.py > gpurun_out/m_ncu_launch.log 2>&1; echo "launches rc=$?"
 timeout 900 python tools/prof_step.py --config C4 --steps 1 --repeat 2 > gpurun_out/m_prof_plain.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:taylor_kernel -s 1 -c 1 \
     -o gpurun_out/m_taylor python tools/prof_step.py --config C4 --steps 1 --repeat 2 > gpurun_out/m_ncu_full.log 2>&1; echo "full rc=$?"
