@@ -335,13 +335,19 @@ def test_sweep_paths_vs_oracle(G, port, shape, path, monkeypatch):
 
 # ---- the C++ drop-in against the reference, called like a reference user calls it --------
 
-def test_cpp_dropin_parity():
+@pytest.mark.parametrize("path", ["auto", "multikernel"])
+def test_cpp_dropin_parity(path):
+    """The C++ drop-in against the linked reference; its 24x20x16 grid takes the single-cluster
+    path by default, and the multi-kernel launch sequence with GS_NO_CLUSTER=1."""
     import os
     import subprocess
     exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "dropin_parity")
     if not os.path.exists(exe):
         pytest.skip("oracle/_ref/dropin_parity not built (needs the reference headers at build time)")
-    res = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    env = dict(os.environ)
+    if path == "multikernel":
+        env["GS_NO_CLUSTER"] = "1"
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=300, env=env)
     print(res.stdout)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "all passed" in res.stdout
