@@ -307,7 +307,7 @@ bool write_values(std::FILE* f, const double* u, int64_t n, int threads) {
         }
         return true;
     }
-    const int T = static_cast<int>(std::min<int64_t>(threads, nb));
+    const int T = static_cast<int>(std::min<int64_t>(std::min(threads, 32), nb));  // ring: 2T x 0.85 MB
     const int R = 2 * T;
     std::vector<std::vector<char>> ring(R, std::vector<char>(static_cast<size_t>(kBlock) * kMaxLen));
     std::vector<size_t> len(R, 0);
@@ -378,25 +378,20 @@ bool write_vtk_stream(std::FILE* f, const std::string& path, const double* u, in
     if (ok && labels) {
         static const char kHead[] = "SCALARS material int 1\nLOOKUP_TABLE default\n";
         ok = std::fwrite(kHead, 1, sizeof kHead - 1, f) == sizeof kHead - 1;
-        std::vector<char> buf(2 * static_cast<size_t>(std::min<int64_t>(n, 1 << 20)));
-        for (int64_t lo = 0; ok && lo < n; lo += 1 << 20) {
-            const int64_t cnt = std::min<int64_t>(n - lo, 1 << 20);
+        constexpr int64_t kChunk = 1 << 20;
+        std::vector<char> buf(4 * static_cast<size_t>(std::min<int64_t>(n, kChunk)));  // "255\n" at most
+        for (int64_t lo = 0; ok && lo < n; lo += kChunk) {
+            const int64_t cnt = std::min<int64_t>(n - lo, kChunk);
             size_t l = 0;
             for (int64_t i = 0; i < cnt; ++i) {
-                // Material codes are printed as int (vtk.cpp:85); every byte value is legal here
+                // Material codes are printed as int (vtk.cpp:85)
                 const int code = labels[lo + i];
-                if (code >= 10) {
-                    const std::string s = std::to_string(code);
-                    if (std::fwrite(buf.data(), 1, l, f) != l || std::fwrite(s.data(), 1, s.size(), f) != s.size())
-                        ok = false;
-                    l = 0;
-                    buf[l++] = '\n';
-                    continue;
-                }
-                buf[l++] = static_cast<char>('0' + code);
+                if (code >= 100) buf[l++] = static_cast<char>('0' + code / 100);
+                if (code >= 10) buf[l++] = static_cast<char>('0' + (code / 10) % 10);
+                buf[l++] = static_cast<char>('0' + code % 10);
                 buf[l++] = '\n';
             }
-            if (ok && std::fwrite(buf.data(), 1, l, f) != l) ok = false;
+            if (std::fwrite(buf.data(), 1, l, f) != l) ok = false;
         }
     }
     if (ok && std::fflush(f) != 0) ok = false;
