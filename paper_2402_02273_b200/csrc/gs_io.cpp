@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <memory>
 #include <mutex>
 #include <sstream>
 #include <thread>
@@ -294,8 +295,11 @@ size_t format_block(const double* u, int64_t n, char* out) {
     return static_cast<size_t>(o - out);
 }
 
-// Values in order, formatted by `threads` workers into a ring of blocks and written by the
-// calling thread as each next block completes.
+// Values in order: T workers format waves of T consecutive blocks (worker i takes block
+// w*T + i of wave w) into one of two buffer sets, while the calling thread writes the
+// previous wave in order.  Hand-offs are two atomics per wave (no locks): a worker may start
+// wave w once wave w-2 has been written, and the writer takes wave w once all T blocks of
+// it are in.
 bool write_values(std::FILE* f, const double* u, int64_t n, int threads) {
     const int64_t nb = (n + kBlock - 1) / kBlock;
     if (threads <= 1 || nb <= 1) {
@@ -307,54 +311,47 @@ bool write_values(std::FILE* f, const double* u, int64_t n, int threads) {
         }
         return true;
     }
-    const int T = static_cast<int>(std::min<int64_t>(std::min(threads, 32), nb));  // ring: 2T x 0.85 MB
-    const int R = 2 * T;
-    std::vector<std::vector<char>> ring(R, std::vector<char>(static_cast<size_t>(kBlock) * kMaxLen));
-    std::vector<size_t> len(R, 0);
-    std::vector<int64_t> ready(R, -1);
-    std::atomic<int64_t> next{0};
-    std::mutex mu;
-    std::condition_variable cv;
-    int64_t written = 0;
-    bool abort = false;
-    auto worker = [&] {
-        for (;;) {
-            const int64_t b = next.fetch_add(1);
-            if (b >= nb) return;
-            {
-                std::unique_lock<std::mutex> lk(mu);
-                cv.wait(lk, [&] { return abort || b < written + R; });
-                if (abort) return;
+    const int T = static_cast<int>(std::min<int64_t>(std::min(threads, 32), nb));
+    const int64_t nwaves = (nb + T - 1) / T;
+    std::unique_ptr<char[]> store(new char[2 * static_cast<size_t>(T) * kBlock * kMaxLen]);  // not zeroed
+    auto buf = [&](int set, int i) { return store.get() + (static_cast<size_t>(set) * T + i) * kBlock * kMaxLen; };
+    std::vector<size_t> len(2 * static_cast<size_t>(T), 0);
+    std::atomic<int> ready[2];
+    ready[0].store(0);
+    ready[1].store(0);
+    std::atomic<int64_t> free_upto{2};  // waves < free_upto may be formatted
+    std::atomic<bool> abort{false};
+    auto worker = [&](int i) {
+        for (int64_t w = 0; w < nwaves; ++w) {
+            while (w >= free_upto.load(std::memory_order_acquire)) {
+                if (abort.load(std::memory_order_relaxed)) return;
+                std::this_thread::yield();
             }
-            const int s = static_cast<int>(b % R);
-            const int64_t lo = b * kBlock, cnt = std::min(kBlock, n - lo);
-            const size_t l = format_block(u + lo, cnt, ring[s].data());
-            {
-                std::lock_guard<std::mutex> lk(mu);
-                len[s] = l;
-                ready[s] = b;
+            const int set = static_cast<int>(w & 1);
+            const int64_t b = w * T + i;
+            size_t l = 0;
+            if (b < nb) {
+                const int64_t lo = b * kBlock, cnt = std::min(kBlock, n - lo);
+                l = format_block(u + lo, cnt, buf(set, i));
             }
-            cv.notify_all();
+            len[static_cast<size_t>(set) * T + i] = l;
+            ready[set].fetch_add(1, std::memory_order_release);
         }
     };
     std::vector<std::thread> pool;
-    for (int i = 0; i < T; ++i) pool.emplace_back(worker);
+    for (int i = 0; i < T; ++i) pool.emplace_back(worker, i);
     bool ok = true;
-    for (int64_t b = 0; b < nb && ok; ++b) {
-        const int s = static_cast<int>(b % R);
-        {
-            std::unique_lock<std::mutex> lk(mu);
-            cv.wait(lk, [&] { return ready[s] == b; });
+    for (int64_t w = 0; w < nwaves && ok; ++w) {
+        const int set = static_cast<int>(w & 1);
+        while (ready[set].load(std::memory_order_acquire) < T) std::this_thread::yield();
+        for (int i = 0; i < T && ok; ++i) {
+            const size_t l = len[static_cast<size_t>(set) * T + i];
+            if (l && std::fwrite(buf(set, i), 1, l, f) != l) ok = false;
         }
-        if (std::fwrite(ring[s].data(), 1, len[s], f) != len[s]) ok = false;
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            written = b + 1;
-            ready[s] = -1;
-            if (!ok) abort = true;
-        }
-        cv.notify_all();
+        ready[set].store(0, std::memory_order_relaxed);
+        free_upto.store(w + 3, std::memory_order_release);  // wave w's set is free for wave w+2
     }
+    if (!ok) abort.store(true);
     for (auto& th : pool) th.join();
     return ok;
 }
