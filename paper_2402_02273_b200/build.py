@@ -15,8 +15,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libgliosim_b200.so")
-SOURCES = ["gs_kernels.cu", "gs_solve.cu", "gs_cluster.cu", "gs_capi.cu", "gs_io.cpp"]
-HEADERS = ["gs_device.cuh", "gs_kernels.cuh", "gs_tma.cuh", "gs_io.hpp"]
+SOURCES = ["gs_kernels.cu", "gs_solve.cu", "gs_cluster.cu", "gs_vtkfmt.cu", "gs_capi.cu", "gs_io.cpp"]
+HEADERS = ["gs_device.cuh", "gs_kernels.cuh", "gs_tma.cuh", "gs_io.hpp", "gs_vtkfmt.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

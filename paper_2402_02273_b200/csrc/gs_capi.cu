@@ -24,6 +24,7 @@
 #include "gliosim_b200.h"
 #include "gs_io.hpp"
 #include "gs_kernels.cuh"
+#include "gs_vtkfmt.cuh"
 
 namespace {
 
@@ -61,9 +62,8 @@ constexpr int64_t kClusterMaxVoxels = 40000;
 constexpr int kDefaultFuse = 2;
 
 struct SnapSlot {
-    DevBuf dev;
-    double* host = nullptr;      // pinned
-    cudaEvent_t ready = nullptr; // host copy complete
+    DevBuf dev;                  // device copy of the state at the snapshot
+    cudaEvent_t ready = nullptr; // the device copy is complete (recorded on the compute stream)
     bool busy = false;
 };
 
@@ -135,8 +135,12 @@ struct gs_ctx {
 
     // snapshot pipeline
     SnapSlot snap[kSnapSlots];
-    cudaStream_t snap_stream = nullptr;
-    cudaEvent_t snap_after = nullptr;
+    cudaStream_t snap_stream = nullptr;  // the writer thread's stream (formatting + D2H)
+    // writer-thread scratch (the writer handles one snapshot at a time)
+    DevBuf fmt_lens, fmt_offs, fmt_text, fmt_tmp, fmt_tie, fmt_lab, fmt_ltext;
+    char* host_text = nullptr;           // pinned: the formatted value lines, then the label lines
+    double* host_u = nullptr;            // pinned: raw values for the host formatter fallback
+    unsigned long long* host_small = nullptr;  // pinned: tie flag, last offset, last length
     std::thread snap_thread;
     std::mutex snap_mu;
     std::condition_variable snap_cv;
@@ -580,6 +584,133 @@ bool tol_ok(double tol) { return tol > 0.0 && tol < 1.0; }
 
 }  // namespace
 
+namespace {
+
+// One snapshot job on the writer thread: the value column formatted on the GPU (gs_vtkfmt.cu),
+// the material column too when every code is < 10, the text copied back and written.  A value
+// the GPU formatter flags (near a rounding tie), or a grid too large for it, goes through the
+// host formatter instead; either way the bytes are write_vtk's (vtk.cpp:59-91).
+bool snapshot_write_job(gs_ctx* c, SnapJob& j, gsio::Error& err) {
+    SnapSlot& s = c->snap[j.slot];
+    const int64_t n = c->n;
+    const bool with_labels = !j.labels.empty();
+    auto cuda_err = [&](cudaError_t e) {
+        err = {GS_ECUDA, std::string("gs_snapshot_vtk: ") + cudaGetErrorString(e)};
+        return false;
+    };
+    cudaError_t e = cudaSuccess;
+    if (!c->snap_stream) e = cudaStreamCreateWithFlags(&c->snap_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess && !c->host_small) e = cudaMallocHost(&c->host_small, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->snap_stream, s.ready, 0);
+    if (e != cudaSuccess) return cuda_err(e);
+    bool labels_on_gpu = with_labels;
+    for (size_t v = 0; labels_on_gpu && v < j.labels.size(); ++v) labels_on_gpu = j.labels[v] < 10;
+    bool gpu = n < (int64_t{1} << 31) && std::getenv("GS_HOST_VTK") == nullptr;
+    if (gpu) {
+        gs::VtkfmtScratch sc;
+        const size_t scan = gs::vtkfmt_scratch_bytes(n);
+        e = gs::vtkfmt_init();
+        if (e == cudaSuccess) e = c->fmt_lens.alloc(8 * static_cast<size_t>(n));
+        if (e == cudaSuccess) e = c->fmt_offs.alloc(8 * static_cast<size_t>(n));
+        if (e == cudaSuccess) e = c->fmt_text.alloc(static_cast<size_t>(gs::kVtkMaxLine) * n);
+        if (e == cudaSuccess) e = c->fmt_tmp.alloc(std::max<size_t>(scan, 16));
+        if (e == cudaSuccess) e = c->fmt_tie.alloc(sizeof(int));
+        if (e == cudaSuccess && labels_on_gpu) e = c->fmt_lab.alloc(static_cast<size_t>(n));
+        if (e == cudaSuccess && labels_on_gpu) e = c->fmt_ltext.alloc(2 * static_cast<size_t>(n));
+        if (e == cudaSuccess && !c->host_text)
+            e = cudaMallocHost(&c->host_text, static_cast<size_t>(gs::kVtkMaxLine + 2) * n);
+        if (e != cudaSuccess) return cuda_err(e);
+        sc.lens = c->fmt_lens.as<unsigned long long>();
+        sc.offs = c->fmt_offs.as<unsigned long long>();
+        sc.text = c->fmt_text.as<char>();
+        sc.scan_tmp = c->fmt_tmp.p;
+        sc.scan_bytes = std::max<size_t>(scan, 16);
+        sc.tie = c->fmt_tie.as<int>();
+        e = gs::vtkfmt_values(s.dev.as<double>(), n, sc, c->snap_stream);
+        if (e == cudaSuccess && labels_on_gpu) {
+            e = cudaMemcpyAsync(c->fmt_lab.p, j.labels.data(), static_cast<size_t>(n), cudaMemcpyHostToDevice,
+                                c->snap_stream);
+            if (e == cudaSuccess) e = gs::vtkfmt_labels(c->fmt_lab.as<uint8_t>(), n, c->fmt_ltext.as<char>(), c->snap_stream);
+        }
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(c->host_small, sc.tie, sizeof(int), cudaMemcpyDeviceToHost, c->snap_stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(c->host_small + 1, sc.offs + (n - 1), 8, cudaMemcpyDeviceToHost, c->snap_stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(c->host_small + 2, sc.lens + (n - 1), 8, cudaMemcpyDeviceToHost, c->snap_stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->snap_stream);
+        if (e != cudaSuccess) return cuda_err(e);
+        gpu = *reinterpret_cast<const int*>(c->host_small) == 0;  // no near-tie value
+        if (gpu) {
+            const size_t total = static_cast<size_t>(c->host_small[1] + c->host_small[2]);
+            e = cudaMemcpyAsync(c->host_text, sc.text, total, cudaMemcpyDeviceToHost, c->snap_stream);
+            if (e == cudaSuccess && labels_on_gpu)
+                e = cudaMemcpyAsync(c->host_text + total, c->fmt_ltext.p, 2 * static_cast<size_t>(n),
+                                    cudaMemcpyDeviceToHost, c->snap_stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(c->snap_stream);
+            if (e != cudaSuccess) return cuda_err(e);
+            const std::string head = gsio::vtk_header(c->nx, c->ny, c->nz, c->h, j.origin);
+            bool ok = std::fwrite(head.data(), 1, head.size(), j.f) == head.size();
+            ok = ok && std::fwrite(c->host_text, 1, total, j.f) == total;
+            if (ok && with_labels) {
+                const size_t lh = std::strlen(gsio::kVtkMaterialHead);
+                ok = std::fwrite(gsio::kVtkMaterialHead, 1, lh, j.f) == lh;
+                if (ok && labels_on_gpu) {
+                    ok = std::fwrite(c->host_text + total, 1, 2 * static_cast<size_t>(n), j.f) ==
+                         2 * static_cast<size_t>(n);
+                } else if (ok) {  // codes >= 10: the host formats the material column
+                    std::string t;
+                    for (uint8_t code : j.labels) t += std::to_string(code) + '\n';
+                    ok = std::fwrite(t.data(), 1, t.size(), j.f) == t.size();
+                }
+            }
+            ok = ok && std::fflush(j.f) == 0;
+            if (!ok) err = {GS_EDATA, "write failed: " + j.path};
+            return ok;
+        }
+    }
+    // host formatter: raw values back, then the parallel exact %.17g writer
+    if (!c->host_u) e = cudaMallocHost(&c->host_u, sizeof(double) * static_cast<size_t>(n));
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c->host_u, s.dev.p, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost,
+                            c->snap_stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->snap_stream);
+    if (e != cudaSuccess) return cuda_err(e);
+    return gsio::write_vtk_stream(j.f, j.path, c->host_u, c->nx, c->ny, c->nz, c->h, j.origin,
+                                  with_labels ? j.labels.data() : nullptr, 0, err);
+}
+
+void snapshot_writer(gs_ctx* c) {
+    cudaSetDevice(c->device);
+    for (;;) {
+        SnapJob j;
+        {
+            std::unique_lock<std::mutex> lk(c->snap_mu);
+            c->snap_cv.wait(lk, [&] { return c->snap_stop || !c->snap_q.empty(); });
+            if (c->snap_q.empty()) return;  // stop requested and nothing left
+            j = std::move(c->snap_q.front());
+            c->snap_q.pop_front();
+        }
+        gsio::Error err;
+        bool ok = snapshot_write_job(c, j, err);
+        if (std::fclose(j.f) != 0 && ok) {
+            ok = false;
+            err = {GS_EDATA, "write failed: " + j.path};
+        }
+        {
+            std::lock_guard<std::mutex> lk(c->snap_mu);
+            c->snap[j.slot].busy = false;
+            if (!ok && c->snap_code == GS_OK) {
+                c->snap_code = static_cast<gs_status>(err.code);
+                c->snap_err = err.msg;
+            }
+        }
+        c->snap_cv.notify_all();
+    }
+}
+
+}  // namespace
+
 extern "C" {
 
 gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) {
@@ -766,10 +897,13 @@ void gs_destroy(gs_ctx* c) {
     }
     for (SnapSlot& s : c->snap) {
         s.dev.release();
-        if (s.host) cudaFreeHost(s.host);
         if (s.ready) cudaEventDestroy(s.ready);
     }
-    if (c->snap_after) cudaEventDestroy(c->snap_after);
+    for (DevBuf* b : {&c->fmt_lens, &c->fmt_offs, &c->fmt_text, &c->fmt_tmp, &c->fmt_tie, &c->fmt_lab, &c->fmt_ltext})
+        b->release();
+    if (c->host_text) cudaFreeHost(c->host_text);
+    if (c->host_u) cudaFreeHost(c->host_u);
+    if (c->host_small) cudaFreeHost(c->host_small);
     if (c->snap_stream) cudaStreamDestroy(c->snap_stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->csr_offs, &c->csr_cols, &c->csr_vals, &c->csc_offs, &c->csc_abs})
@@ -1062,26 +1196,53 @@ gs_status gs_seed_initial(gs_ctx* c, const double origin[3], double amplitude, d
         if (center[a] < lo || center[a] > hi)
             return fail(c, GS_EDATA, "seed center lies outside the computational domain");
     }
+    // the D == 0 mask (seed_initial(d, cfg), integrator.cpp:44-48): palette indices + table
+    // (1 byte per voxel back from the device), or the fp64 field
+    std::vector<uint8_t> pal;
     std::vector<double> d;
     if (mask) {
         gs_status st = ensure_operator(c);
         if (st != GS_OK) return st;
-        d.resize(static_cast<size_t>(c->n));
-        st = gs_get_diffusion(c, d.data());
-        if (st != GS_OK) return st;
+        if (c->palette_mode && !c->is_csr) {
+            pal.resize(static_cast<size_t>(c->n));
+            GS_CUDA(c, cudaMemcpyAsync(pal.data(), c->pal.p, pal.size(), cudaMemcpyDeviceToHost, c->stream));
+            GS_CUDA(c, cudaStreamSynchronize(c->stream));
+        } else {
+            d.resize(static_cast<size_t>(c->n));
+            st = gs_get_diffusion(c, d.data());
+            if (st != GS_OK) return st;
+        }
     }
+    auto dead = [&](int64_t v) {
+        return pal.empty() ? d[static_cast<size_t>(v)] == 0.0 : c->dtab_host[pal[static_cast<size_t>(v)]] == 0.0;
+    };
     // integrator.cpp:32-50; sq_dist integrator.cpp:23-29 (this file is built with
-    // -ffp-contract=off on the host side too)
-    int64_t v = 0;
-    for (int k = 1; k <= c->nz; ++k)
-        for (int j = 1; j <= c->ny; ++j)
-            for (int i = 1; i <= c->nx; ++i, ++v) {
-                const double px = o[0] + (i - 1) * c->h, py = o[1] + (j - 1) * c->h, pz = o[2] + (k - 1) * c->h;
-                const double dx = px - center[0], dy = py - center[1], dz = pz - center[2];
-                const double sq = dx * dx + dy * dy + dz * dz;
-                u[v] = amplitude * std::exp(-width * sq);
-                if (mask && d[static_cast<size_t>(v)] == 0.0) u[v] = 0.0;
-            }
+    // -ffp-contract=off on the host side too).  Planes are split over host threads: every
+    // voxel is computed independently with the same glibc exp, so the result does not
+    // depend on the split.
+    const int nthreads = static_cast<int>(std::min<int64_t>(std::max(1, gsio::default_threads()), c->nz));
+    auto planes = [&](int k0, int k1) {
+        for (int k = k0 + 1; k <= k1; ++k) {
+            int64_t v = static_cast<int64_t>(k - 1) * c->nx * c->ny;
+            for (int j = 1; j <= c->ny; ++j)
+                for (int i = 1; i <= c->nx; ++i, ++v) {
+                    const double px = o[0] + (i - 1) * c->h, py = o[1] + (j - 1) * c->h, pz = o[2] + (k - 1) * c->h;
+                    const double dx = px - center[0], dy = py - center[1], dz = pz - center[2];
+                    const double sq = dx * dx + dy * dy + dz * dz;
+                    u[v] = amplitude * std::exp(-width * sq);
+                    if (mask && dead(v)) u[v] = 0.0;
+                }
+        }
+    };
+    if (nthreads <= 1 || c->n < (1 << 16)) {
+        planes(0, c->nz);
+    } else {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < nthreads; ++t)
+            pool.emplace_back(planes, static_cast<int>(static_cast<int64_t>(c->nz) * t / nthreads),
+                              static_cast<int>(static_cast<int64_t>(c->nz) * (t + 1) / nthreads));
+        for (auto& th : pool) th.join();
+    }
     return GS_OK;
 }
 
@@ -1154,20 +1315,13 @@ gs_status gs_snapshot_vtk(gs_ctx* c, const char* path, const double origin[3], c
         }
         return cuda_fail(c, e, where);
     };
-    cudaError_t e = cudaSuccess;
-    if (!c->snap_stream) e = cudaStreamCreateWithFlags(&c->snap_stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess && !c->snap_after) e = cudaEventCreateWithFlags(&c->snap_after, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = sl.dev.alloc(bytes);
-    if (e == cudaSuccess && !sl.host) e = cudaMallocHost(&sl.host, bytes);
+    cudaError_t e = sl.dev.alloc(bytes);
     if (e == cudaSuccess && !sl.ready) e = cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming);
     if (e != cudaSuccess) return release(e, "gs_snapshot_vtk: allocation");
-    // device copy on the compute stream (the next step may overwrite u), then the side
-    // stream brings it to pinned host memory while the next steps run
+    // device copy on the compute stream (the next step overwrites u); the writer thread
+    // formats it on the GPU and brings the text back on its own stream
     e = cudaMemcpyAsync(sl.dev.p, c->u.p, bytes, cudaMemcpyDeviceToDevice, c->stream);
-    if (e == cudaSuccess) e = cudaEventRecord(c->snap_after, c->stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->snap_stream, c->snap_after, 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(sl.host, sl.dev.p, bytes, cudaMemcpyDeviceToHost, c->snap_stream);
-    if (e == cudaSuccess) e = cudaEventRecord(sl.ready, c->snap_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(sl.ready, c->stream);
     if (e != cudaSuccess) return release(e, "gs_snapshot_vtk: copy");
 
     SnapJob job;
@@ -1179,41 +1333,7 @@ gs_status gs_snapshot_vtk(gs_ctx* c, const char* path, const double origin[3], c
     {
         std::lock_guard<std::mutex> lk(c->snap_mu);
         c->snap_q.push_back(std::move(job));
-        if (!c->snap_thread.joinable()) {
-            c->snap_thread = std::thread([c] {
-                cudaSetDevice(c->device);
-                for (;;) {
-                    SnapJob j;
-                    {
-                        std::unique_lock<std::mutex> lk(c->snap_mu);
-                        c->snap_cv.wait(lk, [&] { return c->snap_stop || !c->snap_q.empty(); });
-                        if (c->snap_q.empty()) return;  // stop requested and nothing left
-                        j = std::move(c->snap_q.front());
-                        c->snap_q.pop_front();
-                    }
-                    SnapSlot& s = c->snap[j.slot];
-                    gsio::Error err;
-                    const cudaError_t ce = cudaEventSynchronize(s.ready);
-                    bool ok = ce == cudaSuccess;
-                    if (!ok) err = {GS_ECUDA, std::string("gs_snapshot_vtk: ") + cudaGetErrorString(ce)};
-                    ok = ok && gsio::write_vtk_stream(j.f, j.path, s.host, c->nx, c->ny, c->nz, c->h, j.origin,
-                                                      j.labels.empty() ? nullptr : j.labels.data(), 0, err);
-                    if (std::fclose(j.f) != 0 && ok) {
-                        ok = false;
-                        err = {GS_EDATA, "write failed: " + j.path};
-                    }
-                    {
-                        std::lock_guard<std::mutex> lk(c->snap_mu);
-                        s.busy = false;
-                        if (!ok && c->snap_code == GS_OK) {
-                            c->snap_code = static_cast<gs_status>(err.code);
-                            c->snap_err = err.msg;
-                        }
-                    }
-                    c->snap_cv.notify_all();
-                }
-            });
-        }
+        if (!c->snap_thread.joinable()) c->snap_thread = std::thread([c] { snapshot_writer(c); });
     }
     c->snap_cv.notify_all();
     return GS_OK;

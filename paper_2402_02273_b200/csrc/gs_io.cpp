@@ -276,6 +276,17 @@ int fmt17(double v, char* out) {
     return static_cast<int>(o - out);
 }
 
+void pow10_table_export(uint64_t* hi, uint64_t* lo, int* b, int* qmin, int* count) {
+    const Pow10Table& t = table();
+    *qmin = kQMin;
+    *count = kQMax - kQMin + 1;
+    for (int k = 0; k < *count; ++k) {
+        hi[k] = static_cast<uint64_t>(t.f[k] >> 64);
+        lo[k] = static_cast<uint64_t>(t.f[k]);
+        b[k] = t.b[k];
+    }
+}
+
 int default_threads() {
     const unsigned hc = std::thread::hardware_concurrency();
     return static_cast<int>(std::clamp(hc ? hc : 1u, 1u, 64u));
@@ -358,8 +369,7 @@ bool write_values(std::FILE* f, const double* u, int64_t n, int threads) {
 
 }  // namespace
 
-bool write_vtk_stream(std::FILE* f, const std::string& path, const double* u, int nx, int ny, int nz, double h,
-                      const double origin[3], const uint8_t* labels, int threads, Error& err) {
+std::string vtk_header(int nx, int ny, int nz, double h, const double origin[3]) {
     const int64_t n = static_cast<int64_t>(nx) * ny * nz;
     char a[32], b[32], c[32];
     std::string head = "# vtk DataFile Version 3.0\ntumor density snapshot\nASCII\nDATASET STRUCTURED_POINTS\n";
@@ -370,6 +380,13 @@ bool write_vtk_stream(std::FILE* f, const std::string& path, const double* u, in
             std::string(b, static_cast<size_t>(fmt17(origin[1], b))) + ' ' +
             std::string(c, static_cast<size_t>(fmt17(origin[2], c))) + '\n';
     head += "POINT_DATA " + std::to_string(n) + "\nSCALARS tumor_density float 1\nLOOKUP_TABLE default\n";
+    return head;
+}
+
+bool write_vtk_stream(std::FILE* f, const std::string& path, const double* u, int nx, int ny, int nz, double h,
+                      const double origin[3], const uint8_t* labels, int threads, Error& err) {
+    const int64_t n = static_cast<int64_t>(nx) * ny * nz;
+    const std::string head = vtk_header(nx, ny, nz, h, origin);
     bool ok = std::fwrite(head.data(), 1, head.size(), f) == head.size();
     ok = ok && write_values(f, u, n, threads <= 0 ? default_threads() : threads);
     if (ok && labels) {

@@ -26,6 +26,16 @@ struct Error {
 bool write_vtk_stream(std::FILE* f, const std::string& path, const double* u, int nx, int ny, int nz, double h,
                       const double origin[3], const uint8_t* labels, int threads, Error& err);
 
+// The lines of write_vtk before the values (vtk.cpp:70-80); the material section's two header
+// lines are kVtkMaterialHead.
+std::string vtk_header(int nx, int ny, int nz, double h, const double origin[3]);
+constexpr const char* kVtkMaterialHead = "SCALARS material int 1\nLOOKUP_TABLE default\n";
+
 int default_threads();
+
+// The 128-bit truncated powers of ten behind fmt17 (10^q = (hi:lo) * 2^b for q = qmin ..
+// qmin + count - 1), for the device formatter.  Arrays need kPow10Count entries.
+constexpr int kPow10Count = 646;
+void pow10_table_export(uint64_t* hi, uint64_t* lo, int* b, int* qmin, int* count);
 
 }  // namespace gsio
