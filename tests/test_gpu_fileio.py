@@ -147,3 +147,28 @@ def test_pgm_stack_ingest_into_device_material_map(tmp_path, port):
     raw.write_bytes(f"{w} {hgt} {slices}\n".encode() + stack.tobytes())
     st2 = G.load_raw_volume(raw)
     assert np.array_equal(st2.intensities, st.intensities)
+
+
+def test_gpu_formatter_matches_host_formatter_on_every_value_class(tmp_path):
+    """The device %.17g (gs_vtkfmt.cu) against the host writer (exact fmt17 + glibc for the
+    special values) on random bit patterns, subnormals, huge and tiny magnitudes, integers,
+    signed zeros, infinities and NaNs of both signs: byte-identical files."""
+    n = 64 * 64 * 16
+    rng = np.random.default_rng(12)
+    bits = rng.integers(0, 2 ** 63, n, dtype=np.int64).view(np.uint64) ^ (rng.integers(0, 2, n).astype(np.uint64) << np.uint64(63))
+    v = bits.view(np.float64).copy()
+    k = n // 8
+    v[:k] = rng.uniform(0, 1, k)
+    v[k:2 * k] = rng.uniform(-1, 1, k) * 10.0 ** rng.integers(-320, 300, k)
+    v[2 * k:2 * k + 1000] = rng.integers(-10 ** 9, 10 ** 9, 1000)
+    special = [0.0, -0.0, np.inf, -np.inf, np.nan, -np.nan, 5e-324, -5e-324, 2.2250738585072014e-308,
+               1.7976931348623157e308, 1e16, 1e17, 9.999999999999999e-5, 1e-4, 0.1, 1.0 / 3]
+    v[3 * k:3 * k + len(special)] = special
+    labels = rng.integers(0, 4, n).astype(np.uint8)
+    grid = G.Grid(64, 64, 16, 0.5, (1.0, -2.0, 0.25))
+    with G.StencilOperator.from_labels(grid, labels) as op:
+        op.set_state(v)
+        op.snapshot_vtk(tmp_path / "gpu.vtk", labels)
+        op.flush_snapshots()
+    G.write_vtk(G.ScalarField(grid, v), tmp_path / "host.vtk", labels)
+    assert (tmp_path / "gpu.vtk").read_bytes() == (tmp_path / "host.vtk").read_bytes()
