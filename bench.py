@@ -309,13 +309,18 @@ def run_ours(args, w, rank, world, local):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        # device-timed on the context's stream: the events bracket the first H2D and the
+        # last D2H (gs_step_host is synchronous, so host gaps between calls are included)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         src, dst = pin_in, pin_out
         for _ in range(k_e2e):
             rc = lib.gs_step_host(op.ctx, src.numpy(), w.rho, w.tau, W.TOL, dst.numpy(), C.byref(info))
             assert rc == 0
             src, dst = dst, src
-        dt = time.perf_counter() - t0
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dt = e0.elapsed_time(e1) / 1e3
         if dist:
             t = torch.tensor([dt], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -448,12 +453,18 @@ def run_ensemble(args, w, rank, world, local):
         info = N.GsStepInfo()
         if dist:
             dist.barrier()
-        tic = time.perf_counter()
+        torch.cuda.synchronize()
+        # device-timed (events on the idle default stream bracket the synchronous calls); the
+        # loop includes staging each member's u into the pinned buffer
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         for op, u, rho in zip(runner.ops, runner.u0, runner.rhos):
             pin_in.numpy()[:] = u
             rc = op.lib.gs_step_host(op.ctx, pin_in.numpy(), rho, w.tau, W.TOL, pin_out.numpy(), C.byref(info))
             assert rc == 0
-        dt = time.perf_counter() - tic
+        e1.record()
+        torch.cuda.synchronize()
+        dt = e0.elapsed_time(e1) / 1e3
         if dist:
             t = torch.tensor([dt], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
