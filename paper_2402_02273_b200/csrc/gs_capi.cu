@@ -350,6 +350,34 @@ int stream_blocks(const gs_ctx* c) {
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 2 * c->num_sms)));
 }
 
+// Lockstep work split of the TMA sweeps (gs::cta_work): with P tiles per plane and a grid
+// of G >= P CTAs, k = G / P groups of P CTAs march z-chunks of [0, zm) one tile each, and
+// the E = G - kP others split the slab [zm, nz).  zm balances the two: a group CTA streams
+// zm/k planes, an extra CTA P(nz - zm)/E planes in about P/E + 1 segments, each segment
+// costing c0 planes more (its z-halo planes and prologue).  GS_LOCK=0 restores the even
+// split; GS_LOCK_C0 overrides c0.
+void lockstep_split(const gs_ctx* c, int gb, gs::SolveParams& p) {
+    p.lock_groups = 0;
+    p.lock_zm = 0;
+    if (!p.use_tma || p.fuse == 4) return;
+    if (const char* e = std::getenv("GS_LOCK"))
+        if (std::atoi(e) == 0) return;
+    const int64_t P = static_cast<int64_t>((c->nx + gs::kTmaTX - 1) / gs::kTmaTX) * ((c->ny + gs::kTmaTY - 1) / gs::kTmaTY);
+    const int64_t k = gb / P;
+    if (k < 1 || c->nz < 8 * k) return;
+    const int64_t E = gb - k * P;
+    double c0 = 3.0;
+    if (const char* e = std::getenv("GS_LOCK_C0")) c0 = std::atof(e);
+    int64_t zm = c->nz;
+    if (E > 0) {
+        const double z = (static_cast<double>(P) * c->nz + c0 * P) / (static_cast<double>(E) / k + P);
+        zm = std::min<int64_t>(c->nz, std::max<int64_t>(k, std::llround(z)));
+        if (P * (c->nz - zm) < E) zm = c->nz;
+    }
+    p.lock_groups = static_cast<int>(k);
+    p.lock_zm = static_cast<int>(zm);
+}
+
 gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* metrics, gs_step_info* infos) {
     int gb = c->grid_blocks;              // prep / taylor (co-resident)
     if (c->tma_ok && c->palette_mode && !c->is_csr) {
@@ -400,7 +428,8 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     if (const char* f = std::getenv("GS_FUSE")) p.fuse = std::atoi(f) == 3 ? 3 : 2;
     // thin grids (2-D and a few planes): the two-term sweep that skips the planes past the grid
     if (p.fuse == 2 && c->nz < 8) p.fuse = 4;
-    p.metrics = metrics ? c->metrics.as<double>() : nullptr;
+    lockstep_split(c, gb, p);
+    p.metrics =metrics ? c->metrics.as<double>() : nullptr;
     p.want_metrics = metrics ? 1 : 0;
     p.infos = infos ? c->infos.as<gs_step_info>() : nullptr;
     p.part_b = c->part_b.as<double>();

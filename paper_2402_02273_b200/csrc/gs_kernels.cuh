@@ -113,6 +113,8 @@ struct SolveParams {
     int n_steps;
     int want_metrics;
     int grid_blocks;
+    int lock_groups;        // TMA sweeps: CTA groups marching z in lockstep (0 = even split; cta_work)
+    int lock_zm;            // z-extent of the lockstep groups; the rest is split evenly
     double rho, tau, tol;   // tau doubles as t for phi1v / expmv
     double anorm;           // exact ||A||_1 (computed once by the norm kernel)
     double rtab[kMaxDegree + 1];  // r_m, m = 1..55, host libm (expact.cpp:47-48)

@@ -169,6 +169,49 @@ __device__ __forceinline__ void sweep_l1(const StencilOp& op, const double* X, c
     }
 }
 
+// Work of this CTA in a TMA sweep: tile-planes q in [qb, qe) of a z-range [zb, zb + len),
+// numbered q = tile * len + (z - zb), so a CTA marches z within a tile column.
+//
+// Default: the whole grid as one range, split evenly.  Lockstep (p.lock_groups = k > 0, set
+// by the host when the grid holds k full planes of tiles, SolveParams): the first k*P CTAs
+// form k groups of one CTA per tile; group j marches z-chunk j of [0, lock_zm), so every
+// tile's x- and y-neighbours are streamed at the same z at the same time and each halo
+// re-read is an L2 hit.  The remaining CTAs split the slab [lock_zm, nz) evenly.
+struct CtaWork {
+    int zb, len;
+    int64_t qb, qe;
+};
+
+__device__ __forceinline__ CtaWork cta_work(const SolveParams& p, int64_t tiles) {
+    CtaWork w;
+    const int64_t b = blockIdx.x, G = gridDim.x;
+    const int k = p.lock_groups;
+    if (k > 0 && G >= k * tiles) {
+        const int64_t kP = k * tiles;
+        if (b < kP) {
+            const int j = static_cast<int>(b / tiles);
+            w.zb = j * p.lock_zm / k;
+            w.len = (j + 1) * p.lock_zm / k - w.zb;
+            w.qb = (b % tiles) * w.len;
+            w.qe = w.qb + w.len;
+        } else {
+            w.zb = p.lock_zm;
+            w.len = p.op.nz - p.lock_zm;
+            const int64_t qs = tiles * w.len, E = G - kP, e = b - kP;
+            w.qb = e * qs / E;
+            w.qe = (e + 1) * qs / E;
+        }
+        if (w.len <= 0) w.len = 1, w.qb = w.qe = 0;
+        return w;
+    }
+    w.zb = 0;
+    w.len = p.op.nz;
+    const int64_t Q = tiles * p.op.nz;
+    w.qb = b * Q / G;
+    w.qe = (b + 1) * Q / G;
+    return w;
+}
+
 // TMA z-slab sweep.  `seq` counts plane loads issued so far in this launch (identical in
 // every thread); it fixes each ring slot's mbarrier phase parity.
 template <bool kNeedF, bool kNeedB, class Body>
@@ -179,17 +222,17 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
     const int lane = tid & 31, row = tid >> 5;
     const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
     const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
-    const int64_t Q = static_cast<int64_t>(tiles_x) * tiles_y * op.nz;
-    const int64_t q_begin = static_cast<int64_t>(blockIdx.x) * Q / gridDim.x;
-    const int64_t q_end = static_cast<int64_t>(blockIdx.x + 1) * Q / gridDim.x;
+    const CtaWork cw = cta_work(p, static_cast<int64_t>(tiles_x) * tiles_y);
+    const int64_t q_begin = cw.qb, q_end = cw.qe;
     constexpr uint32_t kOwnBytes = kLBytes + (kNeedF ? kOBytes : 0) + (kNeedB ? kOBytes : 0);
     constexpr uint32_t kHaloBytes = (kTmaTY + 2) * kXPitch * 8;
     if (tid == 0) fence_proxy_async_global();  // generic writes before this sweep -> TMA reads
+    const uint64_t pol_labels = l2_policy_evict_last();  // labels stay in L2 (see sweep2_tma)
 
     for (int64_t q = q_begin; q < q_end;) {
-        const int64_t tile = q / op.nz;
-        const int z0 = static_cast<int>(q % op.nz);
-        const int z1 = static_cast<int>(min(static_cast<int64_t>(op.nz), static_cast<int64_t>(z0) + (q_end - q)));
+        const int64_t tile = q / cw.len;
+        const int z0 = cw.zb + static_cast<int>(q % cw.len);
+        const int z1 = static_cast<int>(min(static_cast<int64_t>(cw.zb + cw.len), static_cast<int64_t>(z0) + (q_end - q)));
         q += z1 - z0;
         const int x0 = static_cast<int>(tile % tiles_x) * kTmaTX;
         const int y0 = static_cast<int>(tile / tiles_x) * kTmaTY;
@@ -206,7 +249,7 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
             if (own) {
                 if (kNeedF) tma_load_3d(ring.f(slot), &p.omap[fbuf], x0, y0, pl, bar);
                 if (kNeedB) tma_load_3d(ring.b(slot), &p.omap[bbuf], x0, y0, pl, bar);
-                tma_load_3d(ring.l(slot), &p.lmap, x0, y0, pl, bar);
+                tma_load_3d_hint(ring.l(slot), &p.lmap, x0, y0, pl, bar, pol_labels);
             }
         };
         auto slot_of = [&](int pl) { return static_cast<int>((base + static_cast<uint32_t>(pl - (z0 - 1))) % kTmaStages); };
@@ -355,15 +398,15 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
 
     const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
     const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
-    const int64_t Q = static_cast<int64_t>(tiles_x) * tiles_y * op.nz;
-    const int64_t q_begin = static_cast<int64_t>(blockIdx.x) * Q / gridDim.x;
-    const int64_t q_end = static_cast<int64_t>(blockIdx.x + 1) * Q / gridDim.x;
+    const CtaWork cw = cta_work(p, static_cast<int64_t>(tiles_x) * tiles_y);
+    const int64_t q_begin = cw.qb, q_end = cw.qe;
     if (tid == 0) fence_proxy_async_global();
+    const uint64_t pol_labels = l2_policy_evict_last();
 
     for (int64_t q = q_begin; q < q_end;) {
-        const int64_t tile = q / op.nz;
-        const int z0 = static_cast<int>(q % op.nz);
-        const int z1 = static_cast<int>(min(static_cast<int64_t>(op.nz), static_cast<int64_t>(z0) + (q_end - q)));
+        const int64_t tile = q / cw.len;
+        const int z0 = cw.zb + static_cast<int>(q % cw.len);
+        const int z1 = static_cast<int>(min(static_cast<int64_t>(cw.zb + cw.len), static_cast<int64_t>(z0) + (q_end - q)));
         q += z1 - z0;
         const int x0 = static_cast<int>(tile % tiles_x) * kTmaTX;
         const int y0 = static_cast<int>(tile / tiles_x) * kTmaTY;
@@ -382,7 +425,9 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             if (needX) tma_load_3d(ring.x(slot), &p.x2map[xbuf], x0 - kXHalo, y0 - 2, pl, bar);
             if (ownF) tma_load_3d(ring.f(slot), &p.omap[fbuf], x0, y0, pl, bar);
             if (haloB) tma_load_3d(ring.b(slot), &p.xmap[bbuf], x0 - kXHalo, y0 - 1, pl, bar);
-            if (haloL) tma_load_3d(ring.l(slot), &p.l2map, x0 - kLHaloX, y0 - 1, pl, bar);
+            // labels (1 B/voxel, 16.8 MB at 256^3) are re-read by every sweep: keep them in L2
+            // ahead of the streamed fp64 vectors
+            if (haloL) tma_load_3d_hint(ring.l(slot), &p.l2map, x0 - kLHaloX, y0 - 1, pl, bar, pol_labels);
         };
         auto wait_slot = [&](int slot) {
             mbar_wait(ring.bar + slot, (phase_mask >> slot) & 1u);
@@ -685,15 +730,15 @@ __device__ __forceinline__ void sweep3_tma(const SolveParams& p, const Ring3& ri
 
     const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
     const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
-    const int64_t Q = static_cast<int64_t>(tiles_x) * tiles_y * op.nz;
-    const int64_t q_begin = static_cast<int64_t>(blockIdx.x) * Q / gridDim.x;
-    const int64_t q_end = static_cast<int64_t>(blockIdx.x + 1) * Q / gridDim.x;
+    const CtaWork cw = cta_work(p, static_cast<int64_t>(tiles_x) * tiles_y);
+    const int64_t q_begin = cw.qb, q_end = cw.qe;
     if (tid == 0) fence_proxy_async_global();
+    const uint64_t pol_labels = l2_policy_evict_last();  // labels stay in L2 (see sweep2_tma)
 
     for (int64_t q = q_begin; q < q_end;) {
-        const int64_t tile = q / op.nz;
-        const int z0 = static_cast<int>(q % op.nz);
-        const int z1 = static_cast<int>(min(static_cast<int64_t>(op.nz), static_cast<int64_t>(z0) + (q_end - q)));
+        const int64_t tile = q / cw.len;
+        const int z0 = cw.zb + static_cast<int>(q % cw.len);
+        const int z1 = static_cast<int>(min(static_cast<int64_t>(cw.zb + cw.len), static_cast<int64_t>(z0) + (q_end - q)));
         q += z1 - z0;
         const int x0 = static_cast<int>(tile % tiles_x) * kTmaTX;
         const int y0 = static_cast<int>(tile / tiles_x) * kTmaTY;
@@ -708,7 +753,7 @@ __device__ __forceinline__ void sweep3_tma(const SolveParams& p, const Ring3& ri
             uint64_t* bar = ring.barx + slot;
             mbar_arrive_expect_tx(bar, (needX ? kXTx : 0) + kLTx);
             if (needX) tma_load_3d(ring.x(slot), &p.x3map[xbuf], x0 - k3XHaloX, y0 - 3, pl, bar);
-            tma_load_3d(ring.l(slot), &p.l3map, x0 - kLHaloX, y0 - 2, pl, bar);
+            tma_load_3d_hint(ring.l(slot), &p.l3map, x0 - kLHaloX, y0 - 2, pl, bar, pol_labels);
         };
         auto issue_fb = [&](int pl) {  // thread 0 only
             const int slot = static_cast<int>((basef + static_cast<uint32_t>(pl - fbfirst)) % k3FBStages);
