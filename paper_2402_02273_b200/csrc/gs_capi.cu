@@ -429,6 +429,9 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
     // thin grids (2-D and a few planes): the two-term sweep that skips the planes past the grid
     if (p.fuse == 2 && c->nz < 8) p.fuse = 4;
     lockstep_split(c, gb, p);
+    // GS_EXACT_MAX=1|2: test modes of the two-term sweeps' maxima (see taylor_kernel)
+    p.exact_max = 0;
+    if (const char* e = std::getenv("GS_EXACT_MAX")) p.exact_max = std::atoi(e);
     p.metrics =metrics ? c->metrics.as<double>() : nullptr;
     p.want_metrics = metrics ? 1 : 0;
     p.infos = infos ? c->infos.as<gs_step_info>() : nullptr;

@@ -114,6 +114,19 @@ __device__ __forceinline__ double abs_bits(double x) {
 }
 __device__ __forceinline__ double max_abs(double m, double x) { return nan_dropping_max(m, abs_bits(x)); }
 
+// Bounding maxima.  The high word of |x| without its sign, as an unsigned key (exponent and
+// 20 mantissa bits), orders like |x| up to the discarded low word: max over keys costs two
+// integer instructions per value instead of the DSETP/FSEL max of the exact path.  From the
+// maximum key K, key_lower(K) <= max|x| <= key_upper(key_lower(K)) for finite values; a key
+// of an inf or NaN (K >= 0xffe00000) maps to +inf, which callers treat as "bounds unknown".
+__device__ __forceinline__ unsigned max_key(double x) { return static_cast<unsigned>(__double2hiint(x)) << 1; }
+__device__ __forceinline__ double key_lower(unsigned k) {
+    return __hiloint2double(static_cast<int>(min(k, 0xffe00000u) >> 1), 0);
+}
+__device__ __forceinline__ double key_upper(double lower) {
+    return __hiloint2double(__double2hiint(lower), static_cast<int>(0xffffffffu));
+}
+
 // Signed doubles mapped to an unsigned order-preserving key (for min/max of u).
 __device__ __forceinline__ unsigned long long ordered_key(double x) {
     unsigned long long b = __double_as_longlong(x);

@@ -115,6 +115,7 @@ struct SolveParams {
     int grid_blocks;
     int lock_groups;        // TMA sweeps: CTA groups marching z in lockstep (0 = even split; cta_work)
     int lock_zm;            // z-extent of the lockstep groups; the rest is split evenly
+    int exact_max;          // two-term sweeps: 0 bounding maxima + exact fallback, 1 always exact, 2 always rerun
     double rho, tau, tol;   // tau doubles as t for phi1v / expmv
     double anorm;           // exact ||A||_1 (computed once by the norm kernel)
     double rtab[kMaxDegree + 1];  // r_m, m = 1..55, host libm (expact.cpp:47-48)

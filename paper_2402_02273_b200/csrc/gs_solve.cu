@@ -354,9 +354,9 @@ struct Ring2 {
 // kSkipOut: planes past the grid skip their (all-zero) T1 stencil work -- worth it on thin
 // grids (2-D: two of every three T1 planes), a separate instantiation so the deep-grid
 // kernel's code is unchanged.
-template <int KIND, bool kSkipOut = false>
+template <int KIND, bool kSkipOut = false, bool kExact = false>
 __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ring, int xbuf, int fbuf, int bbuf,
-                                           double c1, double c2, double* outT, double* outF, double (&mx)[4],
+                                           double c1, double c2, double* outT, double* outF, double (&mx)[5],
                                            uint32_t& seq, uint32_t& phase_mask, const double* s_wtab) {
     // Register-blocked layout: thread t owns column xl = t % 64 and rows ry0 = 2*(t/64), ry0+1 of
     // the 64 x 16 tile for the whole z-march, so its z-1/z/z+1 values of X and T1 and its own
@@ -402,6 +402,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
     const int64_t q_begin = cw.qb, q_end = cw.qe;
     if (tid == 0) fence_proxy_async_global();
     const uint64_t pol_labels = l2_policy_evict_last();
+    unsigned mk[4] = {0u, 0u, 0u, 0u};  // bounding maxima (kExact == false): see max_key
 
     for (int64_t q = q_begin; q < q_end;) {
         const int64_t tile = q / cw.len;
@@ -583,6 +584,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 } else {
                     const double* XM = ring.x(sM);
                     const double xo0 = XM[oX], xo1 = XM[oX + kXPitch];
+                    if constexpr (kExact) mx[4] = max_abs(max_abs(mx[4], xo0), xo1);
                     if (KIND == k2Next) {
                         const double* Fo = ring.f(sM);
                         fp0 = __dadd_rn(Fo[oF], xo0);
@@ -597,10 +599,17 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 // The maxima drop NaN like std::max(m, |x|) (m is never NaN): expact.cpp:15-19.
                 // They need no domain test: past the grid edge every input is zero-filled and the
                 // row is dead (palette index 0), so T1, T2, F1 and F2 are signed zeros there.
-                mx[0] = max_abs(max_abs(mx[0], T3[r][0]), T3[r][1]);
-                mx[1] = max_abs(max_abs(mx[1], f10), f11);
-                mx[2] = max_abs(max_abs(mx[2], t20), t21);
-                mx[3] = max_abs(max_abs(mx[3], f20), f21);
+                if constexpr (kExact) {
+                    mx[0] = max_abs(max_abs(mx[0], T3[r][0]), T3[r][1]);
+                    mx[1] = max_abs(max_abs(mx[1], f10), f11);
+                    mx[2] = max_abs(max_abs(mx[2], t20), t21);
+                    mx[3] = max_abs(max_abs(mx[3], f20), f21);
+                } else {
+                    mk[0] = max(max(mk[0], max_key(T3[r][0])), max_key(T3[r][1]));
+                    mk[1] = max(max(mk[1], max_key(f10)), max_key(f11));
+                    mk[2] = max(max(mk[2], max_key(t20)), max_key(t21));
+                    mk[3] = max(max(mk[3], max_key(f20)), max_key(f21));
+                }
                 if (in0) {
                     pT[0] = t20;
                     pF[0] = f10;
@@ -638,6 +647,10 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             if (zb + 2 <= z1) iter(zb + 2, std::integral_constant<int, 2>{});
         }
         seq = base + static_cast<uint32_t>(np);
+    }
+    if constexpr (!kExact) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mx[k] = key_lower(mk[k]);
     }
     fence_proxy_async_global();
 }
@@ -1504,7 +1517,20 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
       } else {
         // Fused two-term sweeps; the decisions are taken term by term exactly as the
         // reference's loop (expact.cpp:81-95), on the four maxima of each sweep.
+        //
+        // The sweep first computes bounding maxima (max_key: the high words of |x|), and the
+        // decisions are taken on intervals: by the monotonicity of rounded + and *, a test is
+        // settled when fl(U_prev + U_cur) <= fl(tol * L_f) (the reference stops) or
+        // fl(L_prev + L_cur) > fl(tol * U_f) (it goes on), and so is every later use of the
+        // bounds.  Otherwise (a test within ~2^-20 of its threshold, or an inf/NaN anywhere)
+        // the same sweep runs again with exact NaN-dropping maxima -- its outputs are
+        // rewritten with the same bits -- plus the exact max|X| of its input, which is the
+        // exact value of an inexact `prev` (prev is ||T_j|| = ||X|| inside a stage and
+        // ||f|| = ||X|| (merged with f_n = 1 when bordered) at a stage's first sweep), and the
+        // reference's tests run on exact values.  SolveParams::exact_max = 1 always runs the
+        // exact sweep, 2 always reruns (test modes).
         int fsel = 0, tsel = 0;
+        double prevU = prev;  // prev's upper bound; prev (the lower bound) == prevU when exact
         for (int stage = 0; stage < s_st; ++stage) {
             const int fstart = stage_start(stage);
             if (fstart == kBufF0) fsel = 1;
@@ -1516,35 +1542,101 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                 const double c1 = __ddiv_rn(tau_s, static_cast<double>(used + 1));  // expact.cpp:83
                 const double c2 = __ddiv_rn(tau_s, static_cast<double>(used + 2));
                 const int fout = kBufF0 + fsel, tout = kBufT0 + tsel;
-                double mx[4] = {0.0, 0.0, 0.0, 0.0};
-                {
+                auto run_sweep = [&](auto exactc, double (&mx)[5]) {
+                    constexpr bool kEx = decltype(exactc)::value;
                     const int xb_ = xb < 0 ? 0 : xb, fb_ = fb < 0 ? 0 : fb;
                     double* oT = p.buf[tout];
                     double* oF = p.buf[fout];
                     constexpr bool kSkip = FUSE == 4;
                     if (kind == k2Next)
-                        sweep2_tma<k2Next, kSkip>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2, sm.wtab);
-                    else if (kind == k2FirstBorder)
-                        sweep2_tma<k2FirstBorder, kSkip>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2,
-                                                         sm.wtab);
-                    else if (kind == k2FirstZero)
-                        sweep2_tma<k2FirstZero, kSkip>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2,
+                        sweep2_tma<k2Next, kSkip, kEx>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2,
                                                        sm.wtab);
+                    else if (kind == k2FirstBorder)
+                        sweep2_tma<k2FirstBorder, kSkip, kEx>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2,
+                                                              pmask2, sm.wtab);
+                    else if (kind == k2FirstZero)
+                        sweep2_tma<k2FirstZero, kSkip, kEx>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2,
+                                                            pmask2, sm.wtab);
                     else
-                        sweep2_tma<k2FirstPlain, kSkip>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2,
-                                                        sm.wtab);
-                }
-                block_reduce<4, true>(mx, sm);
-                if (threadIdx.x == 0) {
-                    unsigned long long* sl = p.slots + (round % 3) * 8;
+                        sweep2_tma<k2FirstPlain, kSkip, kEx>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2,
+                                                             pmask2, sm.wtab);
+                    block_reduce<5, true>(mx, sm);
+                    if (threadIdx.x == 0) {
+                        unsigned long long* sl = p.slots + (round % 3) * 8;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (mx[q] > 0.0) atomicMax(sl + q, static_cast<unsigned long long>(__double_as_longlong(mx[q])));
+                        for (int q = 0; q < 5; ++q)
+                            if (mx[q] > 0.0) atomicMax(sl + q, static_cast<unsigned long long>(__double_as_longlong(mx[q])));
+                    }
+                    sync_round(kind == k2Next ? kTrFusedNext : kTrFusedFirst);
+                    const unsigned long long* sl = p.slots + ((round - 1) % 3) * 8;
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) mx[q] = slot_read(sl + q);
+                };
+                // maxima: [0] |T1|, [1] |F1|, [2] |T2|, [3] |F2|, [4] |X| (exact sweep only)
+                double lo[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+                if (p.exact_max != 1) {
+                    run_sweep(std::false_type{}, lo);
+                    // settle both tests on the bounds, or fall back to the exact sweep
+                    double fL[2] = {lo[1], lo[3]}, fU[2] = {key_upper(lo[1]), key_upper(lo[3])};
+                    const double cL[2] = {lo[0], lo[2]}, cU[2] = {key_upper(lo[0]), key_upper(lo[2])};
+                    if (bordered)
+                        for (int k = 0; k < 2; ++k) {
+                            fL[k] = nan_dropping_max(fL[k], 1.0);  // f_n == 1 (expact.cpp:89)
+                            fU[k] = nan_dropping_max(fU[k], 1.0);
+                        }
+                    bool settled = p.exact_max != 2 && !isinf(lo[0]) && !isinf(lo[1]) && !isinf(lo[2]) &&
+                                   !isinf(lo[3]);
+                    // test of term used+k+1 on bounds: 1 stop, 0 go on, -1 unsettled
+                    auto test = [&](int k, double pl, double pu, double cl, double cu, double fl, double fu) {
+                        if (used + k + 1 == m_deg || __dadd_rn(pu, cu) <= __dmul_rn(p.tol, fl)) return 1;
+                        return __dadd_rn(pl, cl) <= __dmul_rn(p.tol, fu) ? -1 : 0;
+                    };
+                    int stop = 0;  // 1: after T1, 2: after T2
+                    if (settled) {
+                        const int a = test(0, prev, prevU, cL[0], cU[0], fL[0], fU[0]);
+                        if (a < 0) settled = false;
+                        else if (a == 1) stop = 1;
+                        else {
+                            const int b = test(1, cL[0], cU[0], cL[1], cU[1], fL[1], fU[1]);
+                            if (b < 0) settled = false;
+                            else if (b == 1) stop = 2;
+                        }
+                    }
+                    if (settled) {
+                        if (stop == 1) {
+                            ++used;
+                            prev = fL[0];
+                            prevU = fU[0];
+                            fres = fout;
+                            tres = -1;
+                            break;
+                        }
+                        used += 2;
+                        if (stop == 2) {
+                            prev = fL[1];
+                            prevU = fU[1];
+                            fres = fout;
+                            tres = tout;
+                            break;
+                        }
+                        prev = cL[1];
+                        prevU = cU[1];
+                        kind = k2Next;
+                        xb = tout;
+                        fb = fout;
+                        fsel ^= 1;
+                        tsel ^= 1;
+                        continue;
+                    }
+                    for (int q = 0; q < 5; ++q) lo[q] = 0.0;
                 }
-                sync_round(kind == k2Next ? kTrFusedNext : kTrFusedFirst);
-                const unsigned long long* sl = p.slots + ((round - 1) % 3) * 8;
-                double cur[2] = {slot_read(sl + 0), slot_read(sl + 2)};
-                double fn[2] = {slot_read(sl + 1), slot_read(sl + 3)};
+                run_sweep(std::true_type{}, lo);  // one call site per instantiation: all inlined
+                // exact maxima: the reference's tests verbatim
+                if (prev != prevU) {  // prev = ||X|| (stage start: ||f|| with f_n = 1 merged)
+                    prev = (kind != k2Next && bordered) ? nan_dropping_max(lo[4], 1.0) : lo[4];
+                }
+                double cur[2] = {lo[0], lo[2]};
+                double fn[2] = {lo[1], lo[3]};
                 if (bordered) {
                     fn[0] = nan_dropping_max(fn[0], 1.0);  // f_n == 1 (expact.cpp:89)
                     fn[1] = nan_dropping_max(fn[1], 1.0);
@@ -1553,7 +1645,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                 ++used;
                 if (!finite_or_fail(cur[0], fn[0])) return;
                 if (__dadd_rn(prev, cur[0]) <= __dmul_rn(p.tol, fn[0]) || used == m_deg) {
-                    prev = fn[0];
+                    prev = prevU = fn[0];
                     fres = fout;
                     tres = -1;
                     break;
@@ -1563,12 +1655,12 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                 ++used;
                 if (!finite_or_fail(cur[1], fn[1])) return;
                 if (__dadd_rn(prev, cur[1]) <= __dmul_rn(p.tol, fn[1]) || used == m_deg) {
-                    prev = fn[1];
+                    prev = prevU = fn[1];
                     fres = fout;
                     tres = tout;
                     break;
                 }
-                prev = cur[1];
+                prev = prevU = cur[1];
                 kind = k2Next;
                 xb = tout;
                 fb = fout;

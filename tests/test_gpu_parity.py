@@ -266,10 +266,14 @@ def test_constants_preserved_by_expmv(G):
     assert np.allclose(y, 1.0, rtol=1e-12, atol=0)
 
 
-@pytest.mark.parametrize("fuse", ["2", "3"])
+@pytest.mark.parametrize("fuse", ["2", "3", "2exact", "2rerun"])
 def test_mid_size_step_vs_oracle(G, port, fuse, monkeypatch):
-    """64^3 phantom, several steps: bitwise against the oracle given the device sums."""
-    monkeypatch.setenv("GS_FUSE", fuse)
+    """64^3 phantom, several steps: bitwise against the oracle given the device sums.  The
+    two-term sweeps decide on bounding maxima with an exact fallback; "2exact" runs the exact
+    maxima always (GS_EXACT_MAX=1), "2rerun" takes the fallback on every sweep (=2)."""
+    monkeypatch.setenv("GS_FUSE", fuse[0])
+    if fuse != "2" and fuse != "3":
+        monkeypatch.setenv("GS_EXACT_MAX", "1" if fuse == "2exact" else "2")
     from paper_2402_02273_b200 import phantom
     n = 64
     inten = phantom.shell_phantom(n, n, n, seed=31)
@@ -300,18 +304,30 @@ TMA_SHAPES = [(48, 32, 20), (80, 40, 12), (64, 48, 1), (32, 32, 32), (16, 16, 16
               (20, 12, 10), (33, 7, 5)]
 
 
-@pytest.mark.parametrize("shape", TMA_SHAPES)
-@pytest.mark.parametrize("path", ["cluster", "tma2", "tma3", "l1"])
-def test_sweep_paths_vs_oracle(G, port, shape, path, monkeypatch):
-    """Every sweep implementation: the single-cluster small-grid path, fused two-term TMA,
-    fused three-term TMA (GS_FUSE=3) and the L1 single-term fallback -- bitwise against the
-    oracle."""
+SWEEP_PATHS = ["cluster", "tma2", "tma2exact", "tma2rerun", "tma3", "l1"]
+
+
+def sweep_path_env(path, monkeypatch):
+    """cluster: the single-cluster small-grid path; tma2: fused two-term TMA (bounding maxima,
+    exact fallback); tma2exact / tma2rerun: the same with exact maxima always / the fallback
+    on every sweep; tma3: fused three-term TMA; l1: the L1 single-term fallback."""
     if path != "cluster":
         monkeypatch.setenv("GS_NO_CLUSTER", "1")
     if path == "l1":
         monkeypatch.setenv("GS_DISABLE_TMA", "1")
     if path == "tma3":
         monkeypatch.setenv("GS_FUSE", "3")
+    if path == "tma2exact":
+        monkeypatch.setenv("GS_EXACT_MAX", "1")
+    if path == "tma2rerun":
+        monkeypatch.setenv("GS_EXACT_MAX", "2")
+
+
+@pytest.mark.parametrize("shape", TMA_SHAPES)
+@pytest.mark.parametrize("path", SWEEP_PATHS)
+def test_sweep_paths_vs_oracle(G, port, shape, path, monkeypatch):
+    """Every sweep implementation (sweep_path_env) -- bitwise against the oracle."""
+    sweep_path_env(path, monkeypatch)
     rng = np.random.default_rng(sum(shape))
     n = int(np.prod(shape))
     table = np.array([0.0, 0.13, 0.013, 0.05])
@@ -331,6 +347,35 @@ def test_sweep_paths_vs_oracle(G, port, shape, path, monkeypatch):
         got_e = G.expmv(20.0, op, x, 1e-10)
         want_e, _ = port.expmv(20.0, op_o, x, 1e-10)
         assert np.array_equal(got_e, want_e)
+
+
+@pytest.mark.parametrize("path", SWEEP_PATHS)
+def test_non_finite_inputs_vs_oracle(G, port, path, monkeypatch):
+    """NaN and inf in the input vector on every sweep path.  The reference's norms drop NaN
+    (expact.cpp:15-19), so a NaN spreads through the terms while the tests run on the rest:
+    the result equals the oracle's bit for bit, NaNs in the same places.  An inf makes a
+    norm infinite: numeric_error in both (expact.cpp:90-91).  On the two-term TMA path both
+    cases go through the exact-maxima fallback (a non-finite key leaves the bounds open)."""
+    sweep_path_env(path, monkeypatch)
+    shape = (48, 32, 12) if path != "cluster" else (24, 16, 12)
+    rng = np.random.default_rng(5)
+    n = int(np.prod(shape))
+    d = np.array([0.0, 0.13, 0.013, 0.05])[rng.integers(0, 4, n)]
+    op_o = port.stencil(shape, 2.0, d)
+    x = rng.uniform(-1, 1, n)
+    x[n // 2 + 7] = np.nan
+    with G.assemble_diffusion(G.Grid(*shape, h=2.0), d) as op:
+        if path == "cluster" and not op.uses_cluster():
+            pytest.skip("grid too large (or too thin) for the single-cluster path")
+        got = G.expmv(2.0, op, x, 1e-10)
+        want, _ = port.expmv(2.0, op_o, x, 1e-10)
+        assert np.isnan(got).any() and np.isnan(got).sum() < n
+        assert np.array_equal(got, want, equal_nan=True)
+        x[n // 3] = np.inf
+        with pytest.raises(G.NumericError):
+            G.expmv(2.0, op, x, 1e-10)
+        with pytest.raises(Exception):
+            port.expmv(2.0, op_o, x, 1e-10)
 
 
 # ---- the C++ drop-in against the reference, called like a reference user calls it --------
