@@ -99,6 +99,23 @@ __device__ __forceinline__ double row_apply_nc(double w, bool live, double negcn
     return live ? acc : 0.0;
 }
 
+// The same without the dead-row select, for sweeps whose results are checked: with w = 0 and
+// finite inputs every product is a signed zero and the sum is +0.0, the select's value; only
+// a non-finite neighbour makes a dead row non-finite (0 * inf), and a sweep whose bounding
+// maxima see a non-finite value is rerun with the selects (sweep2_tma<.., kExact = true>).
+__device__ __forceinline__ double row_apply_ns(double w, double negcnt, double xzm, double xym, double xxm, double xc,
+                                               double xxp, double xyp, double xzp) {
+    const double diag = __dmul_rn(negcnt, w);
+    double acc = __dadd_rn(0.0, __dmul_rn(w, xzm));
+    acc = __dadd_rn(acc, __dmul_rn(w, xym));
+    acc = __dadd_rn(acc, __dmul_rn(w, xxm));
+    acc = __dadd_rn(acc, __dmul_rn(diag, xc));
+    acc = __dadd_rn(acc, __dmul_rn(w, xxp));
+    acc = __dadd_rn(acc, __dmul_rn(w, xyp));
+    acc = __dadd_rn(acc, __dmul_rn(w, xzp));
+    return acc;
+}
+
 // ---------------------------------------------------------------------------------
 // Order-free reductions
 // ---------------------------------------------------------------------------------

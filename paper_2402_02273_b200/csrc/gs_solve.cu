@@ -372,6 +372,12 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
     constexpr uint32_t kLTx = (kTmaTY + 2) * kLPitch;
     constexpr int kRing = 2 * (kTmaTX + 2) + 2 * kTmaTY;  // 164 halo-ring points of T1
     const StencilOp& op = p.op;
+    // dead-row selects only in the exact instantiation (row_apply_ns)
+    auto rowap = [](double w, bool live, double negcnt, double a, double b, double c, double d, double e, double f,
+                    double g) {
+        if constexpr (kExact) return row_apply_nc(w, live, negcnt, a, b, c, d, e, f, g);
+        else return row_apply_ns(w, negcnt, a, b, c, d, e, f, g);
+    };
     const int tid = threadIdx.x;
     const int xl = tid & (kTmaTX - 1);
     const int ry0 = 2 * (tid / kTmaTX);
@@ -482,8 +488,8 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             } else {
                 const double xr0m = Xc[oX - 1], xr0p = Xc[oX + 1], xr1m = Xc[oX + kXPitch - 1], xr1p = Xc[oX + kXPitch + 1];
                 const double xym0 = Xc[oX - kXPitch], xyp1 = Xc[oX + 2 * kXPitch];
-                s0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), xm[0], xym0, xr0m, xc[0], xr0p, xc[1], xp[0]);
-                s1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dhz), xm[1], xc[0], xr1m, xc[1], xr1p, xyp1, xp[1]);
+                s0 = rowap(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), xm[0], xym0, xr0m, xc[0], xr0p, xc[1], xp[0]);
+                s1 = rowap(w1, w1 != 0.0, __dsub_rn(ncxy1, dhz), xm[1], xc[0], xr1m, xc[1], xr1p, xyp1, xp[1]);
                 if (KIND == k2FirstBorder) {
                     s0 = __dadd_rn(s0, B[oB]);
                     s1 = __dadd_rn(s1, B[oB + kXPitch]);
@@ -506,7 +512,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 } else {
                     const double* Xm = ring.x(sm_);
                     const double* Xp = ring.x(sp_);
-                    sc = row_apply_nc(w, w != 0.0, __dsub_rn(rncxy, dhz), Xm[rX], Xc[rX - kXPitch], Xc[rX - 1], Xc[rX],
+                    sc = rowap(w, w != 0.0, __dsub_rn(rncxy, dhz), Xm[rX], Xc[rX - kXPitch], Xc[rX - 1], Xc[rX],
                                       Xc[rX + 1], Xc[rX + kXPitch], Xp[rX]);
                     if (KIND == k2FirstBorder) sc = __dadd_rn(sc, B[rB]);
                 }
@@ -572,9 +578,9 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
                 const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
                 const double dhz = static_cast<double>((zo > 0) + (zo < op.nz - 1));
                 const double y0m = T1s[oT - kT1Pitch], y1p = T1s[oT + 2 * kT1Pitch];
-                const double a0 = row_apply_nc(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), T3[r2][0], y0m, T1s[oT - 1],
+                const double a0 = rowap(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), T3[r2][0], y0m, T1s[oT - 1],
                                                T3[r][0], T1s[oT + 1], T3[r][1], T3[r1][0]);
-                const double a1 = row_apply_nc(w1, w1 != 0.0, __dsub_rn(ncxy1, dhz), T3[r2][1], T3[r][0],
+                const double a1 = rowap(w1, w1 != 0.0, __dsub_rn(ncxy1, dhz), T3[r2][1], T3[r][0],
                                                T1s[oT + kT1Pitch - 1], T3[r][1], T1s[oT + kT1Pitch + 1], y1p, T3[r1][1]);
                 const double t20 = __dmul_rn(c2, a0), t21 = __dmul_rn(c2, a1);
                 double fp0, fp1;
