@@ -451,7 +451,8 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
         p.trace = c->trace.as<unsigned long long>();
         p.trace_cap = c->trace_cap;
     }
-    const size_t dyn = p.use_tma ? gs::kDynSmemBytes : 0;
+    const size_t dyn = gs::kDynSmemBytes;  // the Taylor kernel's reduction scratch is dynamic (kRedOffset)
+    const size_t dyn_prep = p.use_tma ? gs::kRingBytes : 0;
     const dim3 blk(gs::kSolveThreads);
     // optional per-kernel CUDA-event timing: record (kind, start, end) around each launch
     std::vector<std::pair<int, int>> marks;  // (kind, event index of start)
@@ -512,7 +513,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
         GS_CUDA(c, ev_end());
     } else if (p.mode == gs::kModeApply) {
         GS_CUDA(c, ev(0));
-        gs::prep_kernel<<<gb, blk, dyn, c->stream>>>(p, 0);
+        gs::prep_kernel<<<gb, blk, dyn_prep, c->stream>>>(p, 0);
         GS_CUDA(c, cudaGetLastError());
         GS_CUDA(c, ev_end());
     } else {
@@ -533,7 +534,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             void* args[] = {&p, &border_blocks, &neg};
             bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
             if (ok) {
-                gs::prep_kernel<<<gb, blk, dyn, c->stream>>>(p, -1);
+                gs::prep_kernel<<<gb, blk, dyn_prep, c->stream>>>(p, -1);
                 gs::border_kernel<<<sb, blk, 0, c->stream>>>(p, gb, -1);
                 cudaLaunchCooperativeKernel(gs::taylor_kernel_fn(p.fuse), dim3(gb), blk, args, dyn, c->stream);
                 gs::update_kernel<<<sb, blk, 0, c->stream>>>(p, -1);
@@ -555,7 +556,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
         }
         for (int step = 0; step < steps && !graphed; ++step) {
             GS_CUDA(c, ev(0));
-            gs::prep_kernel<<<gb, blk, dyn, c->stream>>>(p, step);
+            gs::prep_kernel<<<gb, blk, dyn_prep, c->stream>>>(p, step);
             GS_CUDA(c, cudaGetLastError());
             GS_CUDA(c, ev_end());
             GS_CUDA(c, ev(1));
@@ -782,10 +783,13 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
         return GS_ECUDA;
     }
     c->num_sms = prop.multiProcessorCount;
-    for (const void* fn : {gs::taylor_kernel_fn(2), gs::taylor_kernel_fn(3), gs::taylor_kernel_fn(4),
-                           reinterpret_cast<const void*>(gs::prep_kernel)})
+    for (const void* fn : {gs::taylor_kernel_fn(2), gs::taylor_kernel_fn(3), gs::taylor_kernel_fn(4)})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kDynSmemBytes)) != cudaSuccess)
             return bail(e, "cudaFuncSetAttribute(smem)");
+    // prep sweeps with the single-term ring only
+    if ((e = cudaFuncSetAttribute(reinterpret_cast<const void*>(gs::prep_kernel),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kRingBytes)) != cudaSuccess)
+        return bail(e, "cudaFuncSetAttribute(smem prep)");
     int per_sm = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::taylor_kernel_fn(2), gs::kSolveThreads,
                                                            gs::kDynSmemBytes)) != cudaSuccess)

@@ -55,6 +55,10 @@ constexpr int kT1Rows = kTmaTY + 2;
 constexpr int kT1Bytes = kT1Rows * kT1Pitch * 8;
 constexpr int kT1Planes = 3;  // T1(z+1) is written while T1(z-1) is read; T1(z) is kept for the next iteration
 constexpr int k2RingBytes = k2Stages * k2SlotBytes + kT1Planes * kT1Bytes + 128;
+// implicit-X ring (a stage's first sweep reads f = F + T): F and T halo-2 tiles per slot
+constexpr int k2IStages = 6;
+constexpr int k2ISlotBytes = 2 * k2XBytes + k2FBBytes + k2LBytes;
+constexpr int k2IRingBytes = k2IStages * k2ISlotBytes + kT1Planes * kT1Bytes + 128;
 
 // Three-term fused sweep: T_{j+1} on the tile plus a two-voxel ring (4-plane shared ring),
 // T_{j+2} on the tile plus a one-voxel ring (3-plane shared ring), T_{j+3} on the tile; the
@@ -82,8 +86,16 @@ constexpr int k3T2Bytes = k3T2Rows * k3T2Pitch * 8;
 constexpr int k3T2Planes = 3;
 constexpr int k3RingBytes = k3XStages * k3XSlotBytes + k3FBStages * k3FBBytes + k3T1Planes * k3T1Bytes +
                             k3T2Planes * k3T2Bytes + 128;
-constexpr int kMaxRing = kRingBytes > k2RingBytes ? kRingBytes : k2RingBytes;
+constexpr int kMaxRing0 = kRingBytes > k2RingBytes ? kRingBytes : k2RingBytes;
+constexpr int kMaxRing = kMaxRing0 > k2IRingBytes ? kMaxRing0 : k2IRingBytes;
 constexpr int kDynSmemBytes = kMaxRing > k3RingBytes ? kMaxRing : k3RingBytes;
+// the Taylor kernel's block-reduction scratch (16 x 6 doubles) at the end of the dynamic
+// region: past every TMA-written byte of every ring (the implicit ring's T1 planes, generic)
+constexpr int kRedOffset = kDynSmemBytes - 128 - 768;
+static_assert(kRedOffset >= k2IStages * k2ISlotBytes && kRedOffset >= k2Stages * k2SlotBytes &&
+                  kRedOffset >= kTmaStages * kSlotBytes && kRedOffset >= k3XStages * k3XSlotBytes + k3FBStages * k3FBBytes,
+              "reduction scratch overlaps a TMA-written region");
+static_assert(kDynSmemBytes + 2304 <= 232448, "dynamic + static shared memory over the 227 KB block limit");
 
 // Device-resident control block shared by the kernels of one launch sequence.
 struct Ctrl {

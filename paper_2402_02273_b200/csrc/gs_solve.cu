@@ -33,14 +33,25 @@ namespace gs {
 
 namespace {
 
-struct Smem {
+struct SmemCore {
     double wtab[256];
-    double red[kSolveThreads / 32][6];
     double bcast[4];
     uint64_t bar1[kTmaStages];   // single-term ring
-    uint64_t bar2[k2Stages];     // fused two-term ring
+    uint64_t bar2[k2Stages];     // fused two-term rings (the implicit-X ring uses the first k2IStages)
     uint64_t bar3x[k3XStages];   // fused three-term ring: input + labels
     uint64_t bar3f[k3FBStages];  // fused three-term ring: F or b/gamma
+};
+
+// Static shared memory of the streaming kernels.
+struct Smem : SmemCore {
+    double red[kSolveThreads / 32][6];
+};
+
+// The Taylor kernel's: its reduction scratch lives in dynamic shared memory (kRedOffset,
+// only ever touched by generic stores and idle during sweeps), which leaves the largest
+// TMA ring (k2IRingBytes) room under the 227 KB per-block limit.
+struct SmemT : SmemCore {
+    double (*red)[6];
 };
 
 struct Ring {
@@ -53,8 +64,8 @@ struct Ring {
 };
 
 // Block reduction of up to 4 values with a fixed shape; result valid in thread 0.
-template <int K, bool kMax>
-__device__ __forceinline__ void block_reduce(double (&v)[K], Smem& sm) {
+template <int K, bool kMax, class S>
+__device__ __forceinline__ void block_reduce(double (&v)[K], S& sm) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int q = 0; q < K; ++q) v[q] = kMax ? warp_max(v[q]) : warp_sum(v[q]);
@@ -75,7 +86,8 @@ __device__ __forceinline__ void block_reduce(double (&v)[K], Smem& sm) {
 }
 
 // Deterministic sum of the per-CTA partials; every CTA computes the same value.
-__device__ double grid_sum(const double* part, int nb, Smem& sm) {
+template <class S>
+__device__ double grid_sum(const double* part, int nb, S& sm) {
     if (threadIdx.x < 32) {
         double acc = 0.0;
         for (int b = threadIdx.x; b < nb; b += 32) acc = __dadd_rn(acc, __ldcg(part + b));
@@ -339,23 +351,37 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
 //          next          X = T_j, Fprev = F_{j-1} + T_j (state kept as (T_j, F_{j-1}))
 enum Fused2Kind { k2FirstZero = 0, k2FirstBorder = 1, k2FirstPlain = 2, k2Next = 3 };
 
-struct Ring2 {
+// Two-term ring layouts.  Plain: slots of [X halo-2 | F own or b/gamma halo-1 | labels].
+// Implicit X (kImp, a stage's first sweep from f = F + T): [F halo-2, combined in place into
+// X | T halo-2 | b/gamma halo-1 | labels], fewer stages.  T1 planes follow the slots.
+template <int kSt, bool kImpl>
+struct Ring2T {
+    static constexpr int kStages = kSt;
+    static constexpr bool kImp = kImpl;
+    static constexpr int kSlot = kImpl ? k2ISlotBytes : k2SlotBytes;
+    static constexpr int kFBOff = kImpl ? 2 * k2XBytes : k2XBytes;
     unsigned char* base;
     uint64_t* bar;
-    __device__ double* x(int s) const { return reinterpret_cast<double*>(base + s * k2SlotBytes); }
-    __device__ double* f(int s) const { return reinterpret_cast<double*>(base + s * k2SlotBytes + k2XBytes); }
-    __device__ double* b(int s) const { return reinterpret_cast<double*>(base + s * k2SlotBytes + k2XBytes); }
-    __device__ uint8_t* l(int s) const { return base + s * k2SlotBytes + k2XBytes + k2FBBytes; }
-    __device__ double* t1(int q) const {
-        return reinterpret_cast<double*>(base + k2Stages * k2SlotBytes + q * kT1Bytes);
-    }
+    __device__ double* x(int s) const { return reinterpret_cast<double*>(base + s * kSlot); }
+    __device__ double* t(int s) const { return reinterpret_cast<double*>(base + s * kSlot + k2XBytes); }
+    __device__ double* f(int s) const { return reinterpret_cast<double*>(base + s * kSlot + kFBOff); }
+    __device__ double* b(int s) const { return reinterpret_cast<double*>(base + s * kSlot + kFBOff); }
+    __device__ uint8_t* l(int s) const { return base + s * kSlot + kFBOff + k2FBBytes; }
+    __device__ double* t1(int q) const { return reinterpret_cast<double*>(base + kSt * kSlot + q * kT1Bytes); }
 };
+using Ring2 = Ring2T<k2Stages, false>;
+using Ring2I = Ring2T<k2IStages, true>;
 
 // kSkipOut: planes past the grid skip their (all-zero) T1 stencil work -- worth it on thin
 // grids (2-D: two of every three T1 planes), a separate instantiation so the deep-grid
 // kernel's code is unchanged.
-template <int KIND, bool kSkipOut = false, bool kExact = false>
-__device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ring, int xbuf, int fbuf, int bbuf,
+//
+// Implicit X (R::kImp): the stage's start vector f = F[xbuf] + T[fbuf] is never stored: each
+// plane's two halo tiles land by TMA and are summed in place (the same __dadd_rn as the
+// reference's f += term), each thread its own points, its T1-ring point and one outer-halo
+// point, so nothing is read before its own thread wrote it until the plane's barrier.
+template <int KIND, bool kSkipOut = false, bool kExact = false, class R = Ring2>
+__device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, int xbuf, int fbuf, int bbuf,
                                            double c1, double c2, double* outT, double* outF, double (&mx)[5],
                                            uint32_t& seq, uint32_t& phase_mask, const double* s_wtab) {
     // Register-blocked layout: thread t owns column xl = t % 64 and rows ry0 = 2*(t/64), ry0+1 of
@@ -365,6 +391,9 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
     // All per-thread shared-memory offsets are fixed per tile; ring slots rotate by increment and
     // barrier parities are tracked in a bit mask (identical in every thread).
     constexpr bool needX = KIND != k2FirstZero;
+    constexpr bool kImp = R::kImp;
+    constexpr int kSt = R::kStages;
+    static_assert(!kImp || KIND == k2FirstBorder || KIND == k2FirstPlain, "implicit X only starts a stage");
     constexpr bool needF = KIND == k2Next;
     constexpr bool needB = KIND == k2FirstZero || KIND == k2FirstBorder;
     constexpr uint32_t kXTx = k2XRows * kXPitch * 8;
@@ -422,14 +451,16 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
         const int np = plast - pfirst + 1;
 
         auto issue = [&](int pl) {  // thread 0 only
-            const int slot = static_cast<int>((base + static_cast<uint32_t>(pl - pfirst)) % k2Stages);
+            const int slot = static_cast<int>((base + static_cast<uint32_t>(pl - pfirst)) % kSt);
             uint64_t* bar = ring.bar + slot;
             const bool ownF = needF && pl >= z0 && pl < z1;
             const bool haloB = needB && pl >= z0 - 1 && pl <= z1;
             const bool haloL = pl >= z0 - 1 && pl <= z1;
-            const uint32_t bytes = (needX ? kXTx : 0) + (ownF ? kOBytes : 0) + (haloB ? kBTx : 0) + (haloL ? kLTx : 0);
+            const uint32_t bytes = (needX ? kXTx : 0) + (kImp ? kXTx : 0) + (ownF ? kOBytes : 0) + (haloB ? kBTx : 0) +
+                                   (haloL ? kLTx : 0);
             mbar_arrive_expect_tx(bar, bytes);
             if (needX) tma_load_3d(ring.x(slot), &p.x2map[xbuf], x0 - kXHalo, y0 - 2, pl, bar);
+            if (kImp) tma_load_3d(ring.t(slot), &p.x2map[fbuf], x0 - kXHalo, y0 - 2, pl, bar);
             if (ownF) tma_load_3d(ring.f(slot), &p.omap[fbuf], x0, y0, pl, bar);
             if (haloB) tma_load_3d(ring.b(slot), &p.xmap[bbuf], x0 - kXHalo, y0 - 1, pl, bar);
             // labels (1 B/voxel, 16.8 MB at 256^3) are re-read by every sweep: keep them in L2
@@ -440,10 +471,10 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             mbar_wait(ring.bar + slot, (phase_mask >> slot) & 1u);
             phase_mask ^= 1u << slot;
         };
-        auto next_slot = [](int s) { return s + 1 == k2Stages ? 0 : s + 1; };
+        auto next_slot = [](int s) { return s + 1 == kSt ? 0 : s + 1; };
 
         if (tid == 0) {
-            const int pre = min(k2Stages, np);
+            const int pre = min(kSt, np);
             for (int k = 0; k < pre; ++k) issue(pfirst + k);
         }
 
@@ -520,14 +551,40 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             }
         };
 
-        int s0 = static_cast<int>(base % k2Stages);  // slot of plane z0-2
+        // implicit X: X = F + T over plane slot s, this thread's points (see above); returns
+        // the own rows' values
+        auto combine = [&](int s, double (&xo)[2]) {
+            double* Xs = ring.x(s);
+            const double* Ts = ring.t(s);
+            xo[0] = Xs[oX] = __dadd_rn(Xs[oX], Ts[oX]);
+            xo[1] = Xs[oX + kXPitch] = __dadd_rn(Xs[oX + kXPitch], Ts[oX + kXPitch]);
+            if (ringer) Xs[rX] = __dadd_rn(Xs[rX], Ts[rX]);
+            // outer halo (172 points): X-tile rows 0 and 19, then columns 0 and 67 of rows 1..18
+            const int e = tid - kRing;
+            if (e >= 0 && e < 2 * kXPitch + 2 * (kTmaTY + 2)) {
+                const int f = e - 2 * kXPitch;
+                const int o = f < 0 ? (e < kXPitch ? e : (k2XRows - 1) * kXPitch + e - kXPitch)
+                                    : (1 + (f >> 1)) * kXPitch + ((f & 1) ? kXPitch - 1 : 0);
+                Xs[o] = __dadd_rn(Xs[o], Ts[o]);
+            }
+            fence_proxy_async_shared();  // generic writes into a TMA slot before its next fill
+        };
+
+        int s0 = static_cast<int>(base % kSt);  // slot of plane z0-2
         int s1 = next_slot(s0), s2 = next_slot(s1), s3 = next_slot(s2);
         // prologue: T1 of planes z0-1 and z0
         wait_slot(s0);
         wait_slot(s1);
         wait_slot(s2);
         double xz[2] = {0.0, 0.0}, xa[2] = {0.0, 0.0}, xb[2] = {0.0, 0.0}, xn[2] = {0.0, 0.0};
-        if (needX) {
+        if constexpr (kImp) {
+            wait_slot(s3);
+            combine(s0, xz);
+            combine(s1, xa);
+            combine(s2, xb);
+            combine(s3, xn);
+            __syncthreads();
+        } else if (needX) {
             const double* X0 = ring.x(s0);
             const double* X1 = ring.x(s1);
             const double* X2 = ring.x(s2);
@@ -541,8 +598,8 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
         // own T1 of planes z-2, z-1, z (relative to the loop's z); w unused here
         double tm1[2], t0[2], lwd[2];
         phaseA(z0 - 1, 0, s0, s1, s2, xz, xa, xb, tm1, lwd);
-        wait_slot(s3);
-        if (needX) {
+        if (!kImp) wait_slot(s3);
+        if (needX && !kImp) {
             const double* X3 = ring.x(s3);
             xn[0] = X3[oX];
             xn[1] = X3[oX + kXPitch];
@@ -554,8 +611,8 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
         xb[1] = xn[1];
         __syncthreads();
         if (tid == 0) {
-            if (pfirst + k2Stages <= plast) issue(pfirst + k2Stages);
-            if (pfirst + 1 + k2Stages <= plast) issue(pfirst + 1 + k2Stages);
+            if (pfirst + kSt <= plast) issue(pfirst + kSt);
+            if (pfirst + 1 + kSt <= plast) issue(pfirst + 1 + kSt);
         }
         // Iteration z: phase A makes T1(z+1) (z < z1), phase B finishes plane z-1 (z > z0) --
         // independent work, so the two dependency chains overlap.  Register rings of three:
@@ -629,7 +686,9 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             }
             if (z < z1) {
                 wait_slot(sC);
-                if (needX) {
+                if constexpr (kImp) {
+                    combine(sC, X3[r2]);
+                } else if (needX) {
                     const double* XC = ring.x(sC);
                     X3[r2][0] = XC[oX];
                     X3[r2][1] = XC[oX + kXPitch];
@@ -643,7 +702,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const Ring2& ri
             sC = next_slot(sC);
             __syncthreads();  // plane z-1's slot and T1(z-1)'s shared plane are free
             if (tid == 0 && z > z0) {
-                const int nxt = z - 1 + k2Stages;
+                const int nxt = z - 1 + kSt;
                 if (nxt <= plast) issue(nxt);
             }
         };
@@ -1020,7 +1079,8 @@ __device__ __forceinline__ void sweep3_tma(const SolveParams& p, const Ring3& ri
 enum TermKind { kFirstZero, kFirstBorder, kFirstPlain, kNext };
 
 // Per-block setup shared by the kernels: w table in shared memory, mbarriers for TMA.
-__device__ __forceinline__ void block_setup(const SolveParams& p, Smem& sm, bool with_tma) {
+template <class S>
+__device__ __forceinline__ void block_setup(const SolveParams& p, S& sm, bool with_tma) {
     if (p.op.pal)
         for (int q = threadIdx.x; q < 256; q += blockDim.x) sm.wtab[q] = __ldg(p.op.wtab + q);
     if (with_tma && threadIdx.x == 0) {
@@ -1047,8 +1107,8 @@ __device__ __forceinline__ void trace_mark(const SolveParams& p, int tag) {
 }
 
 // Single-term stencil sweep dispatch (TMA ring or L1 fallback).
-template <class Body>
-__device__ __forceinline__ void stencil_sweep(const SolveParams& p, Smem& sm, const Ring& ring, uint32_t& seq, int xb,
+template <class S, class Body>
+__device__ __forceinline__ void stencil_sweep(const SolveParams& p, S& sm, const Ring& ring, uint32_t& seq, int xb,
                                               int fb, int bb, Body&& body) {
     const bool nf = fb >= 0, nb = bb >= 0;
     if (p.op.csr_offs) {
@@ -1284,15 +1344,17 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                                                                   int border_blocks, int step) {
     if (step < 0) step = __ldcg(&p.ctrl->step);  // graph replay: the step lives on the device
     cg::grid_group grid = cg::this_grid();
-    __shared__ Smem sm;
+    __shared__ SmemT sm;
     extern __shared__ __align__(128) unsigned char dyn[];
     Ctrl* ctrl = p.ctrl;
     if (ctrl->status) return;
     trace_mark(p, kTrTaylorIn);
     const StencilOp& op = p.op;
+    if (threadIdx.x == 0) sm.red = reinterpret_cast<double (*)[6]>(dyn + kRedOffset);
     block_setup(p, sm, p.use_tma);
     Ring ring{dyn, sm.bar1};
     Ring2 ring2{dyn, sm.bar2};
+    Ring2I ring2i{dyn, sm.bar2};
     Ring3 ring3{dyn, sm.bar3x, sm.bar3f};
     uint32_t seq = 0, seq2 = 0, pmask2 = 0, seq3x = 0, seq3f = 0, pm3x = 0, pm3f = 0;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
@@ -1535,12 +1597,18 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
         // ||f|| = ||X|| (merged with f_n = 1 when bordered) at a stage's first sweep), and the
         // reference's tests run on exact values.  SolveParams::exact_max = 1 always runs the
         // exact sweep, 2 always reruns (test modes).
+        //
+        // A stage that ended on an implicit F + T starts from it without storing f: its first
+        // sweep sums the two in shared memory (sweep2_tma with the Ring2I layout).
         int fsel = 0, tsel = 0;
         double prevU = prev;  // prev's upper bound; prev (the lower bound) == prevU when exact
         for (int stage = 0; stage < s_st; ++stage) {
-            const int fstart = stage_start(stage);
+            const int fstart = stage == 0 ? (bordered ? -1 : kBufG) : fres;
+            int timp = stage == 0 ? -1 : tres;  // f = F[fstart] + T[timp] when timp >= 0
             if (fstart == kBufF0) fsel = 1;
             else if (fstart == kBufF1) fsel = 0;
+            if (timp == kBufT0) tsel = 1;
+            else if (timp == kBufT1) tsel = 0;
             int used = 0;
             int kind = fstart < 0 ? k2FirstZero : (bordered ? k2FirstBorder : k2FirstPlain);
             int xb = fstart, fb = -1;
@@ -1557,6 +1625,12 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                     if (kind == k2Next)
                         sweep2_tma<k2Next, kSkip, kEx>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2, pmask2,
                                                        sm.wtab);
+                    else if (timp >= 0 && kind == k2FirstBorder)
+                        sweep2_tma<k2FirstBorder, kSkip, kEx>(p, ring2i, xb_, timp, kBufG, c1, c2, oT, oF, mx, seq2,
+                                                              pmask2, sm.wtab);
+                    else if (timp >= 0)
+                        sweep2_tma<k2FirstPlain, kSkip, kEx>(p, ring2i, xb_, timp, kBufG, c1, c2, oT, oF, mx, seq2,
+                                                             pmask2, sm.wtab);
                     else if (kind == k2FirstBorder)
                         sweep2_tma<k2FirstBorder, kSkip, kEx>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2,
                                                               pmask2, sm.wtab);
@@ -1628,6 +1702,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                         prev = cL[1];
                         prevU = cU[1];
                         kind = k2Next;
+                        timp = -1;
                         xb = tout;
                         fb = fout;
                         fsel ^= 1;
@@ -1668,6 +1743,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                 }
                 prev = prevU = cur[1];
                 kind = k2Next;
+                timp = -1;
                 xb = tout;
                 fb = fout;
                 fsel ^= 1;
