@@ -37,7 +37,7 @@ typedef enum gs_status {
 typedef struct gs_step_info {
     int32_t s, m;            /* select_params result (expact.cpp:29-61) */
     int32_t branch;          /* 0 Taylor, 1 t == 0, 2 ||b||_1 == 0, 3 small-norm (expact.cpp:108-122) */
-    int32_t pad;
+    int32_t reruns;          /* two-term sweeps re-run with exact maxima (a bounded test was unsettled) */
     int64_t total_terms;     /* Taylor terms = operator applications inside expmv */
     int32_t terms[GS_MAX_LOGGED_STAGES]; /* terms used per stage (expact.cpp:81-95) */
     double bnorm;            /* ||b||_1 (expact.cpp:110), device tree-reduced */

@@ -19,7 +19,7 @@ GS_OK, GS_EINVAL, GS_ENUMERIC, GS_EDATA, GS_ECUDA = range(5)
 
 class GsStepInfo(C.Structure):
     _fields_ = [
-        ("s", C.c_int32), ("m", C.c_int32), ("branch", C.c_int32), ("pad", C.c_int32),
+        ("s", C.c_int32), ("m", C.c_int32), ("branch", C.c_int32), ("reruns", C.c_int32),
         ("total_terms", C.c_int64),
         ("terms", C.c_int32 * MAX_STAGES),
         ("bnorm", C.c_double), ("anorm", C.c_double), ("coln", C.c_double),
@@ -30,7 +30,7 @@ class GsStepInfo(C.Structure):
         return [self.terms[i] for i in range(min(self.s, MAX_STAGES))]
 
     def as_dict(self):
-        return {"s": self.s, "m": self.m, "branch": self.branch, "total_terms": self.total_terms,
+        return {"s": self.s, "m": self.m, "branch": self.branch, "total_terms": self.total_terms, "reruns": self.reruns,
                 "terms": self.stage_terms(), "bnorm": self.bnorm, "anorm": self.anorm, "coln": self.coln,
                 "gamma": self.gamma, "norm_tA": self.norm_tA}
 

@@ -1426,6 +1426,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
     const double tau_s = __ddiv_rn(t, static_cast<double>(s_st));  // expact.cpp:73
     double prev = __ldcg(&ctrl->prev0);
     int64_t total_terms = 0;
+    int reruns = 0;  // two-term sweeps re-run with exact maxima
     int fres = -1, tres = -1;  // stage result: F[fres] (+ T[tres] when tres >= 0, implicit)
     auto finite_or_fail = [&](double cur, double fnorm) {
         if (!isfinite(cur) || !isfinite(fnorm)) {  // expact.cpp:90-91
@@ -1710,6 +1711,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
                         continue;
                     }
                     for (int q = 0; q < 5; ++q) lo[q] = 0.0;
+                    ++reruns;
                 }
                 run_sweep(std::true_type{}, lo);  // one call site per instantiation: all inlined
                 // exact maxima: the reference's tests verbatim
@@ -1822,7 +1824,10 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
         }
         fres = fcur;
     }
-    if (info) info->total_terms = total_terms;
+    if (info) {
+        info->total_terms = total_terms;
+        info->reruns = reruns;
+    }
     if (leader) {
         ctrl->fres = fres;
         ctrl->tres = tres;
