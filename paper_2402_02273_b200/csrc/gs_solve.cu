@@ -1856,6 +1856,10 @@ __global__ void __launch_bounds__(kSolveThreads) update_kernel(const __grid_cons
     if (step < 0) step = __ldcg(&p.ctrl->step);  // graph replay: the step lives on the device
     __shared__ Smem sm;
     const Ctrl* ctrl = p.ctrl;
+    // The Taylor kernel leaves its last round's maxima in one rotating slot; the next step's
+    // first rounds expect all three slots zero (their atomicMax would otherwise see the stale
+    // ||f|| of the previous step's last sweep).  The Taylor kernel has finished: stream order.
+    if (blockIdx.x == 0 && threadIdx.x < 24) p.slots[threadIdx.x] = 0ull;
     if (__ldcg(&ctrl->status)) return;
     trace_mark(p, kTrUpdateIn);
     const int branch = __ldcg(&ctrl->branch);

@@ -296,6 +296,37 @@ def test_mid_size_step_vs_oracle(G, port, fuse, monkeypatch):
             u = got
 
 
+@pytest.mark.parametrize("path", ["tma2", "tma2exact", "l1", "cluster"])
+@pytest.mark.parametrize("tol", [0.03, 1e-3])
+def test_multi_step_run_loose_tol_vs_oracle(G, port, path, tol, monkeypatch):
+    """Several steps in ONE gs_run call at loose tolerances (s ~ 140, 10-16 terms per stage),
+    every step bitwise against the oracle given that step's device sums.  Covers the rotating
+    max slots across the steps of one launch sequence: the Taylor kernel leaves its last
+    round's maxima in one slot and the update kernel zeroes all three before the next step."""
+    sweep_path_env(path, monkeypatch)
+    shape = (48, 32, 20) if path != "cluster" else (24, 16, 12)
+    rng = np.random.default_rng(17)
+    n = int(np.prod(shape))
+    d = np.array([0.0, 0.13, 0.013, 0.05])[rng.integers(0, 4, n)]
+    h = 0.25
+    op_o = port.stencil(shape, h, d)
+    u0 = np.zeros(n)
+    u0[rng.integers(0, n, 40)] = rng.uniform(0.2, 1.0, 40)
+    u0[d == 0.0] = 0.0
+    k = 4
+    with G.assemble_diffusion(G.Grid(*shape, h=h), d) as op:
+        if path == "cluster" and not op.uses_cluster():
+            pytest.skip("grid too large (or too thin) for the single-cluster path")
+        op.set_state(u0)
+        _, inf = op.run_resident(k, 0.1, 33.5, tol, metrics=False, infos=True)
+        got = op.get_state()
+    u = u0
+    for q in range(k):
+        u, log = port.step(op_o, u, 0.1, 33.5, tol, bnorm=inf[q].bnorm, coln=inf[q].coln)
+        assert inf[q].stage_terms() == log.stage_terms(), q
+    assert np.array_equal(got, u)
+
+
 # ---- both stencil sweep paths (TMA z-slab ring and the L1 fallback) on awkward shapes ------
 
 # nx % 16 != 0 (20, 33) cannot be described by TMA: those shapes take the L1 fallback
