@@ -417,6 +417,7 @@ def run_ensemble(args, w, rank, world, local):
     partitioned over ranks (replicas, no data-path collective); value = member-steps/s."""
     import torch
     from paper_2402_02273_b200 import ensemble as E
+    from paper_2402_02273_b200 import gliosim as G
     from paper_2402_02273_b200 import workloads as W
 
     torch.cuda.set_device(local)
@@ -428,7 +429,7 @@ def run_ensemble(args, w, rank, world, local):
     members = E.members_for_rank(w.members, rank, world)
     runner = E.EnsembleRunner(w, members, device=local)
     runner.reset()
-    runner.run(args.warmup)
+    runner.run(args.warmup, batched=not os.environ.get("GS_ENS_SEQUENTIAL"))
     runner.reset()
     torch.cuda.synchronize()
     if dist:
@@ -437,7 +438,7 @@ def run_ensemble(args, w, rank, world, local):
     t1 = torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         t0.record()
-        results = runner.run(args.steps)  # synchronous per member (gs_run returns after its stream sync)
+        results = runner.run(args.steps, batched=not os.environ.get("GS_ENS_SEQUENTIAL"))  # synchronous
         t1.record()
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
@@ -459,7 +460,8 @@ def run_ensemble(args, w, rank, world, local):
             t = torch.empty(w.n, dtype=torch.float64, pin_memory=True)
             t.numpy()[:] = u
             pin_ins.append(t)
-        pin_out = torch.empty(w.n, dtype=torch.float64, pin_memory=True)
+        pin_outs = [torch.empty(w.n, dtype=torch.float64, pin_memory=True) for _ in runner.ops]
+        batched = not os.environ.get("GS_ENS_SEQUENTIAL")
         info = N.GsStepInfo()
         if dist:
             dist.barrier()
@@ -467,9 +469,17 @@ def run_ensemble(args, w, rank, world, local):
         # device-timed (events on the idle default stream bracket the synchronous calls)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for op, pin_in, rho in zip(runner.ops, pin_ins, runner.rhos):
-            rc = op.lib.gs_step_host(op.ctx, pin_in.numpy(), rho, w.tau, W.TOL, pin_out.numpy(), C.byref(info))
-            assert rc == 0
+        if batched:
+            # every member's u H2D (gs_set_state), one batched step, every u' D2H (gs_get_state)
+            for op, pin_in in zip(runner.ops, pin_ins):
+                assert op.lib.gs_set_state(op.ctx, pin_in.numpy()) == 0
+            G.run_ensemble(runner.ops, 1, runner.rhos, w.tau, W.TOL, metrics=False)
+            for op, pin_out in zip(runner.ops, pin_outs):
+                assert op.lib.gs_get_state(op.ctx, pin_out.numpy()) == 0
+        else:
+            for op, pin_in, pin_out, rho in zip(runner.ops, pin_ins, pin_outs, runner.rhos):
+                rc = op.lib.gs_step_host(op.ctx, pin_in.numpy(), rho, w.tau, W.TOL, pin_out.numpy(), C.byref(info))
+                assert rc == 0
         e1.record()
         torch.cuda.synchronize()
         dt = e0.elapsed_time(e1) / 1e3
@@ -479,7 +489,9 @@ def run_ensemble(args, w, rank, world, local):
             dt = float(t.item())
         e2e = {"value": w.members / dt, "unit": "member-steps/s", "h2d_bytes_per_step": 8 * w.n * w.members,
                "d2h_bytes_per_step": 8 * w.n * w.members,
-               "api": "gs_step_host per member (drop-in step(): u H2D from pinned, u' D2H)"}
+               "api": ("gs_set_state per member (u H2D from pinned) + one gs_run_ensemble step + gs_get_state per "
+                       "member (u' D2H)" if batched else
+                       "gs_step_host per member (drop-in step(): u H2D from pinned, u' D2H)")}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -499,10 +511,14 @@ def run_ensemble(args, w, rank, world, local):
         "data": "synthetic (seeded shell phantoms, one per member)",
         "config": {"workload": f"{w.name}: {w.note}", "members": w.members, "grid": [w.nx, w.ny, w.nz],
                    "members_per_rank": len(members), "parallelism": f"members partitioned over {world} rank(s)",
+                   "batching": ("gs_run_ensemble: one launch per kernel of the step for all members; the Taylor "
+                                "launch runs 16 members at a time on groups of 9 SMs, longest members first"
+                                if not os.environ.get("GS_ENS_SEQUENTIAL") else "sequential gs_run per member"),
                    "terms_per_member_step": float(terms.mean()),
                    "rho_range": [float(min(runner.rhos)), float(max(runner.rhos))] if world == 1 else None,
                    "l2": "64 resident members x 7 x 16 MiB >> L2"},
-        "gpu_launches": 4 * len(members) * args.steps + len(members),
+        "gpu_launches": (5 * args.steps + 1) if not os.environ.get("GS_ENS_SEQUENTIAL")
+        else 4 * len(members) * args.steps + len(members),
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
         "metrics_all_finite": bool(np.isfinite(table).all()),
     }

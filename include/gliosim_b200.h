@@ -124,6 +124,19 @@ gs_status gs_step_host(gs_ctx* ctx, const double* u, double rho, double tau, dou
 gs_status gs_run(gs_ctx* ctx, int n_steps, double rho, double tau, double tol, const double origin[3],
                  const double seed_center[3], double front_threshold, gs_metrics* metrics,
                  gs_step_info* infos);
+/* An ensemble of independent runs (BASELINE C5; run() of integrator.cpp:91-138 per member):
+ * member i is context ctxs[i] (its own operator and resident state) with rho = rhos[i],
+ * origin = origins[3i..], seed centre = centers[3i..]; every member advances n_steps steps
+ * with the same tau and tol.  metrics: n_members * (n_steps+1) records (member-major) or
+ * NULL; infos: n_members * n_steps records or NULL.  All members live on one device.  The
+ * members' steps are batched: one launch per kernel of the step serves every member, and
+ * the Taylor launch runs `groups` members at a time on groups of SMs (groups <= 0: the
+ * default).  Members the batched path cannot take (CSR operators, shapes without TMA,
+ * mixed 2-D/3-D) run one after another through gs_run.  Each member's result is that of
+ * gs_run on its own context, up to the ulps of the per-CTA partial sums. */
+gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const double* rhos, double tau,
+                          double tol, const double* origins, const double* centers, double front_threshold,
+                          gs_metrics* metrics, gs_step_info* infos, int groups);
 
 /* ---- host helpers with libm parity --------------------------------------------------- */
 /* seed_initial (integrator.cpp:32-50): u = amplitude*exp(-width*|x-c|^2), zero where the

@@ -50,7 +50,8 @@ EXPORTS = [
     "gs_create", "gs_create_csr", "gs_destroy", "gs_last_error", "gs_num_points", "gs_stream",
     "gs_set_intensity", "gs_set_labels", "gs_set_diffusion", "gs_get_labels", "gs_get_diffusion",
     "gs_one_norm", "gs_apply", "gs_set_state", "gs_get_state", "gs_state_device_ptr",
-    "gs_select_params", "gs_expmv", "gs_phi1v", "gs_step", "gs_step_host", "gs_run", "gs_seed_initial",
+    "gs_select_params", "gs_expmv", "gs_phi1v", "gs_step", "gs_step_host", "gs_run", "gs_run_ensemble",
+    "gs_seed_initial",
     "gs_set_trace", "gs_get_trace", "gs_set_kernel_timing", "gs_get_kernel_times",
     "gs_write_vtk", "gs_read_vtk", "gs_write_metrics_csv", "gs_snapshot_vtk", "gs_snapshot_flush",
     "gs_load_stack", "gs_load_raw_volume", "gs_write_label_volume", "gs_read_label_volume",
@@ -99,6 +100,9 @@ def load(path: str | None = None):
     L.gs_step_host.argtypes = [vp, _dp, C.c_double, C.c_double, C.c_double, _dp, C.POINTER(GsStepInfo)]
     L.gs_run.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_double, _d3, _d3, C.c_double, vp, vp]
     L.gs_seed_initial.argtypes = [vp, _d3, C.c_double, C.c_double, _d3, C.c_int, _dp]
+    if hasattr(L, "gs_run_ensemble"):
+        L.gs_run_ensemble.argtypes = [C.POINTER(vp), C.c_int, C.c_int, _dp, C.c_double, C.c_double, vp, vp,
+                                      C.c_double, vp, vp, C.c_int]
     if hasattr(L, "gs_set_trace"):  # diagnostics
         L.gs_set_trace.argtypes = [vp, C.c_int]
         L.gs_get_trace.argtypes = [vp, np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS"), C.c_int,

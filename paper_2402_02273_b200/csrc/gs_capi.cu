@@ -61,6 +61,10 @@ constexpr int64_t kClusterMaxVoxels = 40000;
 // Taylor terms per fused TMA sweep (2 or 3); GS_FUSE overrides it per launch.
 constexpr int kDefaultFuse = 2;
 
+// gs_run_ensemble: CTA groups of the batched Taylor launch (members run concurrently, one per
+// group of num_sms / groups SMs); GS_ENS_GROUPS or the call's `groups` argument override it.
+constexpr int kEnsembleGroups = 16;
+
 struct SnapSlot {
     DevBuf dev;                  // device copy of the state at the snapshot
     cudaEvent_t ready = nullptr; // the device copy is complete (recorded on the compute stream)
@@ -107,6 +111,8 @@ struct gs_ctx {
     DevBuf u, g, f0, f1, t0, t1, out;
     // scratch
     DevBuf part_b, part_c, part_u, slots, mslots, ctrl, metrics, infos, normbits;
+    // gs_run_ensemble (this context as member 0): the members' SolveParams and the group control words
+    DevBuf ens_params, ens_ctl;
 
     gs::StencilOp op{};
     int grid_blocks = 0;
@@ -325,6 +331,21 @@ gs_status compute_anorm(gs_ctx* c) {
     return GS_OK;
 }
 
+// The cluster kernel's dynamic shared-memory limit is a per-function attribute shared by every
+// context in the process: it only ever grows (to the largest grid's need), so a context created
+// later for a smaller grid cannot invalidate the launches of an earlier, larger one.
+bool raise_cluster_smem(size_t smem) {
+    static std::mutex mu;
+    static size_t cur = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem <= cur) return true;
+    if (cudaFuncSetAttribute(gs::cluster_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess)
+        return false;
+    cur = smem;
+    return true;
+}
+
 gs_status operator_ready(gs_ctx* c) {
     c->has_operator = true;
     c->anorm_valid = false;
@@ -378,16 +399,10 @@ void lockstep_split(const gs_ctx* c, int gb, gs::SolveParams& p) {
     p.lock_zm = static_cast<int>(zm);
 }
 
-gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* metrics, gs_step_info* infos) {
-    int gb = c->grid_blocks;              // prep / taylor (co-resident)
-    if (c->tma_ok && c->palette_mode && !c->is_csr) {
-        // the TMA sweeps hand out tile-planes: CTAs beyond their count would only join the
-        // grid barriers (C1/C2: 64 tile-planes; 64 CTAs run 8-10% faster than 148)
-        const int64_t q = static_cast<int64_t>((c->nx + gs::kTmaTX - 1) / gs::kTmaTX) *
-                          ((c->ny + gs::kTmaTY - 1) / gs::kTmaTY) * c->nz;
-        gb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(gb, q)));
-    }
-    const int sb = stream_blocks(c);      // border / update / metrics
+// Scratch, state staging and the context-dependent SolveParams fields of one run on the
+// context's stream: gb CTAs for prep / taylor, sb for the streaming kernels.
+gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps, gs_metrics* metrics,
+                      gs_step_info* infos) {
     const int pb = std::max(gb, sb);
     GS_CUDA(c, c->part_b.alloc(sizeof(double) * pb));
     GS_CUDA(c, c->part_c.alloc(sizeof(double) * pb));
@@ -450,6 +465,29 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
         GS_CUDA(c, cudaMemsetAsync(c->trace.p, 0, sizeof(uint64_t) * 2 * c->trace_cap, c->stream));
         p.trace = c->trace.as<unsigned long long>();
         p.trace_cap = c->trace_cap;
+    }
+    return GS_OK;
+}
+
+// CTAs of the prep / Taylor launches: one per SM, capped at the TMA sweeps' tile-plane count
+// (CTAs beyond it would only join the grid barriers; C1/C2: 64 tile-planes, 64 CTAs run
+// 8-10% faster than 148).
+int solve_blocks(const gs_ctx* c) {
+    int gb = c->grid_blocks;
+    if (c->tma_ok && c->palette_mode && !c->is_csr) {
+        const int64_t q = static_cast<int64_t>((c->nx + gs::kTmaTX - 1) / gs::kTmaTX) *
+                          ((c->ny + gs::kTmaTY - 1) / gs::kTmaTY) * c->nz;
+        gb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(gb, q)));
+    }
+    return gb;
+}
+
+gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* metrics, gs_step_info* infos) {
+    const int gb = solve_blocks(c);       // prep / taylor (co-resident)
+    const int sb = stream_blocks(c);      // border / update / metrics
+    {
+        const gs_status st = setup_solve(c, p, gb, sb, n_steps, metrics, infos);
+        if (st != GS_OK) return st;
     }
     const size_t dyn = gs::kDynSmemBytes;  // the Taylor kernel's reduction scratch is dynamic (kRedOffset)
     const size_t dyn_prep = p.use_tma ? gs::kRingBytes : 0;
@@ -786,10 +824,13 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
     for (const void* fn : {gs::taylor_kernel_fn(2), gs::taylor_kernel_fn(3), gs::taylor_kernel_fn(4)})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kDynSmemBytes)) != cudaSuccess)
             return bail(e, "cudaFuncSetAttribute(smem)");
+    for (const void* fn : {gs::ens_taylor_kernel_fn(2), gs::ens_taylor_kernel_fn(4)})
+        if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kDynSmemBytes)) != cudaSuccess)
+            return bail(e, "cudaFuncSetAttribute(smem ens)");
     // prep sweeps with the single-term ring only
-    if ((e = cudaFuncSetAttribute(reinterpret_cast<const void*>(gs::prep_kernel),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kRingBytes)) != cudaSuccess)
-        return bail(e, "cudaFuncSetAttribute(smem prep)");
+    for (const void* fn : {reinterpret_cast<const void*>(gs::prep_kernel), reinterpret_cast<const void*>(gs::ens_prep_kernel)})
+        if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kRingBytes)) != cudaSuccess)
+            return bail(e, "cudaFuncSetAttribute(smem prep)");
     int per_sm = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::taylor_kernel_fn(2), gs::kSolveThreads,
                                                            gs::kDynSmemBytes)) != cudaSuccess)
@@ -821,8 +862,7 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
         if (c->n <= kClusterMaxVoxels && slice >= halo && smem + 4096 <= static_cast<size_t>(optin) &&
             cudaFuncSetAttribute(gs::cluster_run_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                 cudaSuccess &&
-            cudaFuncSetAttribute(gs::cluster_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)) == cudaSuccess) {
+            raise_cluster_smem(smem)) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(gs::kClusterCTAs);
             cfg.blockDim = dim3(gs::kSolveThreads);
@@ -946,7 +986,7 @@ void gs_destroy(gs_ctx* c) {
         b->release();
     for (DevBuf* b : {&c->pal, &c->dvox, &c->wtab, &c->dtab, &c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out,
                       &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->ctrl, &c->metrics, &c->infos,
-                      &c->normbits, &c->trace})
+                      &c->normbits, &c->trace, &c->ens_params, &c->ens_ctl})
         b->release();
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -1203,6 +1243,122 @@ gs_status gs_run(gs_ctx* c, int n_steps, double rho, double tau, double tol, con
     }
     fill_rtab(tol, p.rtab);
     return launch_solve(c, p, n_steps, reinterpret_cast<gs_metrics*>(metrics), infos);
+}
+
+gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const double* rhos, double tau, double tol,
+                          const double* origins, const double* centers, double front_threshold, gs_metrics* metrics,
+                          gs_step_info* infos, int groups) {
+    if (!ctxs || n_members < 1 || !rhos) return fail(nullptr, GS_EINVAL, "run_ensemble: null argument or no members");
+    for (int i = 0; i < n_members; ++i)
+        if (!ctxs[i]) return fail(nullptr, GS_EINVAL, "run_ensemble: null member context");
+    gs_ctx* const c0 = ctxs[0];
+    if (n_steps < 0) return fail(c0, GS_EINVAL, "run: negative step count");
+    if (!tol_ok(tol)) return fail(c0, GS_EINVAL, "phi1v: tolerance must lie in (0, 1)");
+    if (metrics && (!origins || !centers)) return fail(c0, GS_EINVAL, "run: metrics need origin and seed center");
+    bool batched = std::getenv("GS_ENS_SEQUENTIAL") == nullptr && std::getenv("GS_DISABLE_TMA") == nullptr;
+    int thin = 0;
+    for (int i = 0; i < n_members; ++i) {
+        gs_ctx* c = ctxs[i];
+        const gs_status st = ensure_operator(c);
+        if (st != GS_OK) return st;
+        if (c->device != c0->device) return fail(c0, GS_EINVAL, "run_ensemble: members on different devices");
+        batched = batched && c->tma_ok && c->palette_mode && !c->is_csr;
+        thin += c->nz < 8;
+    }
+    batched = batched && (thin == 0 || thin == n_members);  // one Taylor instantiation per launch
+    auto orig = [&](int i) { return origins ? origins + 3 * i : nullptr; };
+    auto cent = [&](int i) { return centers ? centers + 3 * i : nullptr; };
+    if (!batched) {
+        // members the batched path cannot take run one after another, each on the whole GPU
+        for (int i = 0; i < n_members; ++i) {
+            const gs_status st = gs_run(ctxs[i], n_steps, rhos[i], tau, tol, orig(i), cent(i), front_threshold,
+                                        metrics ? metrics + static_cast<size_t>(i) * (n_steps + 1) : nullptr,
+                                        infos ? infos + static_cast<size_t>(i) * n_steps : nullptr);
+            if (st != GS_OK) return st;
+        }
+        return GS_OK;
+    }
+    cudaSetDevice(c0->device);
+    // CTA groups of the Taylor launch: each runs one member at a time on num_sms / groups SMs
+    if (groups <= 0) {
+        groups = kEnsembleGroups;
+        if (const char* e = std::getenv("GS_ENS_GROUPS")) groups = std::atoi(e);
+    }
+    groups = std::max(1, std::min({groups, n_members, c0->num_sms}));
+    const int grp = c0->num_sms / groups;
+    int sb = 1;
+    for (int i = 0; i < n_members; ++i) sb = std::max(sb, stream_blocks(ctxs[i]));
+    std::vector<gs::SolveParams> P(static_cast<size_t>(n_members));
+    for (int i = 0; i < n_members; ++i) {
+        gs_ctx* c = ctxs[i];
+        gs::SolveParams& p = P[i];
+        p = gs::SolveParams{};
+        p.mode = gs::kModeRun;
+        p.n_steps = n_steps;
+        p.rho = rhos[i];
+        p.tau = tau;
+        p.tol = tol;
+        p.h = c->h;
+        p.front_threshold = front_threshold;
+        for (int a = 0; a < 3; ++a) {
+            p.origin[a] = orig(i) ? orig(i)[a] : 0.0;
+            p.center[a] = cent(i) ? cent(i)[a] : 0.0;
+        }
+        fill_rtab(tol, p.rtab);
+        gs_status st = setup_solve(c, p, grp, sb, n_steps, metrics, infos);
+        if (st != GS_OK) return st;
+        GS_CUDA(c, cudaStreamSynchronize(c->stream));  // the member's scratch is ready for c0's stream
+    }
+    const int fuse = thin ? 4 : 2;
+    GS_CUDA(c0, c0->ens_params.alloc(sizeof(gs::SolveParams) * static_cast<size_t>(n_members)));
+    GS_CUDA(c0, c0->ens_ctl.alloc(sizeof(unsigned) * (gs::ens_ctl_words(groups) + n_members)));
+    GS_CUDA(c0, cudaMemcpyAsync(c0->ens_params.p, P.data(), sizeof(gs::SolveParams) * static_cast<size_t>(n_members),
+                                cudaMemcpyHostToDevice, c0->stream));
+    const gs::SolveParams* dP = c0->ens_params.as<gs::SolveParams>();
+    unsigned* ctl = c0->ens_ctl.as<unsigned>();
+    const unsigned* order = ctl + gs::ens_ctl_words(groups);
+    const dim3 blk(gs::kSolveThreads);
+    cudaStream_t st = c0->stream;
+    if (metrics) {
+        gs::ens_metrics_kernel<<<n_members * sb, blk, 0, st>>>(dP, sb);
+        GS_CUDA(c0, cudaGetLastError());
+    }
+    for (int step = 0; step < n_steps; ++step) {
+        gs::ens_prep_kernel<<<n_members * grp, blk, gs::kRingBytes, st>>>(dP, grp, step);
+        GS_CUDA(c0, cudaGetLastError());
+        gs::ens_border_kernel<<<n_members * sb, blk, 0, st>>>(dP, sb, grp, step);
+        GS_CUDA(c0, cudaGetLastError());
+        gs::ens_order_kernel<<<1, 256, 0, st>>>(dP, n_members, ctl + gs::ens_ctl_words(groups));
+        GS_CUDA(c0, cudaGetLastError());
+        GS_CUDA(c0, cudaMemsetAsync(ctl, 0, sizeof(unsigned) * gs::ens_ctl_words(groups), st));
+        int nm = n_members, g = grp, bb = sb, sp = step;
+        void* args[] = {&dP, &nm, &g, &bb, &sp, &ctl, &order};
+        GS_CUDA(c0, cudaLaunchCooperativeKernel(gs::ens_taylor_kernel_fn(fuse), dim3(groups * grp), blk, args,
+                                                gs::kDynSmemBytes, st));
+        gs::ens_update_kernel<<<n_members * sb, blk, 0, st>>>(dP, sb, step);
+        GS_CUDA(c0, cudaGetLastError());
+    }
+    std::vector<gs::Ctrl> ctrl(static_cast<size_t>(n_members));
+    for (int i = 0; i < n_members; ++i) {
+        gs_ctx* c = ctxs[i];
+        GS_CUDA(c0, cudaMemcpyAsync(&ctrl[i], c->ctrl.p, sizeof(gs::Ctrl), cudaMemcpyDeviceToHost, st));
+        if (metrics)
+            GS_CUDA(c0, cudaMemcpyAsync(metrics + static_cast<size_t>(i) * (n_steps + 1), c->metrics.p,
+                                        sizeof(double) * 4 * (n_steps + 1), cudaMemcpyDeviceToHost, st));
+        if (infos && n_steps > 0)
+            GS_CUDA(c0, cudaMemcpyAsync(infos + static_cast<size_t>(i) * n_steps, c->infos.p,
+                                        sizeof(gs_step_info) * n_steps, cudaMemcpyDeviceToHost, st));
+    }
+    GS_CUDA(c0, cudaStreamSynchronize(st));
+    for (int i = 0; i < n_members; ++i) {
+        if (ctrl[i].status == GS_OK) continue;
+        const std::string who = "run_ensemble: member " + std::to_string(i) + ": ";
+        if (ctrl[i].detail == 2) return fail(c0, GS_ENUMERIC, who + "expmv: series diverged to non-finite values; reduce t");
+        if (ctrl[i].status == GS_EINVAL)
+            return fail(c0, GS_EINVAL, who + "select_params: operator norm must be finite and nonnegative");
+        return fail(c0, GS_ENUMERIC, who + "select_params: scaled operator norm too large for any stage count");
+    }
+    return GS_OK;
 }
 
 gs_status gs_step(gs_ctx* c, double rho, double tau, double tol, gs_step_info* info) {

@@ -106,6 +106,7 @@ struct Ctrl {
     unsigned int ticket;  // last-block-done counter (metrics)
     int ntrace;
     int step;             // current step of a graph-replayed run (kernels launched with step < 0)
+    int last_terms;       // Taylor terms of the last step (ensemble: longest members first)
 };
 
 struct SolveParams {
@@ -196,5 +197,20 @@ __global__ void advance_kernel(Ctrl* ctrl);
 // terms with the past-the-grid planes skipped (thin grids).
 const void* taylor_kernel_fn(int fuse);
 __global__ void update_kernel(const __grid_constant__ SolveParams p, int step);
+
+// Ensemble (C5) forms of the step's kernels: one launch serves every member; P is a device
+// array of the members' SolveParams (TMA descriptors read from global memory).  CTA b of the
+// streaming/prep launches works for member b / cpm as CTA b % cpm of cpm.  The Taylor kernel
+// is cooperative: gridDim.x / group CTA groups take members from a queue, each running one
+// member's Taylor loop on its group with a software group barrier.  ctl: 4 words per group
+// plus the queue head, zeroed before each launch, then n_members words of the queue's order
+// (ens_order_kernel: members by their last step's Taylor terms, most first).
+__global__ void ens_metrics_kernel(const SolveParams* P, int cpm);
+__global__ void ens_prep_kernel(const SolveParams* P, int cpm, int step);
+__global__ void ens_border_kernel(const SolveParams* P, int cpm, int prep_blocks, int step);
+__global__ void ens_update_kernel(const SolveParams* P, int cpm, int step);
+__global__ void ens_order_kernel(const SolveParams* P, int n_members, unsigned* order);
+const void* ens_taylor_kernel_fn(int fuse);  // fuse 2 or 4 (args: P, n_members, group, border_blocks, step, ctl, order)
+inline int ens_ctl_words(int groups) { return 4 * groups + 1; }
 
 }  // namespace gs

@@ -33,6 +33,20 @@ namespace gs {
 
 namespace {
 
+// Virtual grid: this CTA's index and the CTA count of the work it belongs to.  A plain launch
+// is its own virtual grid; the ensemble kernels cut one launch into per-member virtual grids
+// (a CTA group per member, ens_* below).  Set first thing by every kernel (vgrid_set).
+__shared__ int s_vgrid[2];
+__device__ __forceinline__ void vgrid_set(int cta, int ncta) {
+    if (threadIdx.x == 0) {
+        s_vgrid[0] = cta;
+        s_vgrid[1] = ncta;
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ int vcta() { return s_vgrid[0]; }
+__device__ __forceinline__ int vncta() { return s_vgrid[1]; }
+
 struct SmemCore {
     double wtab[256];
     double bcast[4];
@@ -133,8 +147,8 @@ __device__ int select_params_dev(double norm_tA, const double* rtab, int* s_out,
 // Pointwise sweep: grid-stride over voxels, no neighbours.
 template <class Body>
 __device__ __forceinline__ void sweep_points(const StencilOp& op, Body&& body) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < op.n; v += stride) body(v);
+    const int64_t stride = static_cast<int64_t>(vncta()) * blockDim.x;
+    for (int64_t v = static_cast<int64_t>(vcta()) * blockDim.x + threadIdx.x; v < op.n; v += stride) body(v);
 }
 
 // Fallback stencil sweep (L1-cached loads, z-march in registers); used where TMA cannot
@@ -145,7 +159,8 @@ __device__ __forceinline__ void sweep_l1(const StencilOp& op, const double* X, c
     const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
     const int ty_n = blockDim.x >> 5;
     const int64_t tiles = static_cast<int64_t>(op.tiles_x) * op.tiles_y;
-    for (int64_t item = blockIdx.x; item < op.n_items; item += gridDim.x) {
+    const int64_t vc = vcta(), vn = vncta();
+    for (int64_t item = vc; item < op.n_items; item += vn) {
         const int64_t tile = item % tiles;
         const int chunk = static_cast<int>(item / tiles);
         const int i = static_cast<int>(tile % op.tiles_x) * 32 + lx;
@@ -196,7 +211,7 @@ struct CtaWork {
 
 __device__ __forceinline__ CtaWork cta_work(const SolveParams& p, int64_t tiles) {
     CtaWork w;
-    const int64_t b = blockIdx.x, G = gridDim.x;
+    const int64_t b = vcta(), G = vncta();
     const int k = p.lock_groups;
     if (k > 0 && G >= k * tiles) {
         const int64_t kP = k * tiles;
@@ -1080,22 +1095,28 @@ enum TermKind { kFirstZero, kFirstBorder, kFirstPlain, kNext };
 
 // Per-block setup shared by the kernels: w table in shared memory, mbarriers for TMA.
 template <class S>
-__device__ __forceinline__ void block_setup(const SolveParams& p, S& sm, bool with_tma) {
+__device__ __forceinline__ void block_setup(const SolveParams& p, S& sm, bool with_tma, bool reinit = false) {
     if (p.op.pal)
         for (int q = threadIdx.x; q < 256; q += blockDim.x) sm.wtab[q] = __ldg(p.op.wtab + q);
     if (with_tma && threadIdx.x == 0) {
+        if (reinit) {  // every load on these barriers has completed and been waited for
+            for (int s = 0; s < kTmaStages; ++s) mbar_inval(sm.bar1 + s);
+            for (int s = 0; s < k2Stages; ++s) mbar_inval(sm.bar2 + s);
+            for (int s = 0; s < k3XStages; ++s) mbar_inval(sm.bar3x + s);
+            for (int s = 0; s < k3FBStages; ++s) mbar_inval(sm.bar3f + s);
+        }
         for (int s = 0; s < kTmaStages; ++s) mbar_init(sm.bar1 + s, 1);
         for (int s = 0; s < k2Stages; ++s) mbar_init(sm.bar2 + s, 1);
         for (int s = 0; s < k3XStages; ++s) mbar_init(sm.bar3x + s, 1);
         for (int s = 0; s < k3FBStages; ++s) mbar_init(sm.bar3f + s, 1);
         mbar_fence_init();
-        for (int b = 0; b < kNumBufs; ++b) tma_prefetch_desc(&p.xmap[b]);
+        for (int b = 0; b < kNumBufs; ++b) tma_prefetch_desc(&p.xmap[b]);  // generic address: param or global
     }
     __syncthreads();
 }
 
 __device__ __forceinline__ void trace_mark(const SolveParams& p, int tag) {
-    if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.trace && vcta() == 0 && threadIdx.x == 0) {
         const int k = atomicAdd(&p.ctrl->ntrace, 1);
         if (k < p.trace_cap) {
             unsigned long long tnow;
@@ -1172,14 +1193,14 @@ __device__ void metrics_commit(const SolveParams& p, Smem& sm, MetricAcc& a, int
     }
     __shared__ bool last;
     if (threadIdx.x == 0) {
-        p.part_u[blockIdx.x] = s[0];
+        p.part_u[vcta()] = s[0];
         __threadfence();
-        last = atomicAdd(&p.ctrl->ticket, 1u) == gridDim.x - 1;
+        last = atomicAdd(&p.ctrl->ticket, 1u) == static_cast<unsigned>(vncta()) - 1;
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
-    const double sum = grid_sum(p.part_u, gridDim.x, sm);
+    const double sum = grid_sum(p.part_u, vncta(), sm);
     if (threadIdx.x == 0) {
         const double cell = __dmul_rn(__dmul_rn(p.h, p.h), p.h);
         double* out = p.metrics + 4 * node;
@@ -1200,7 +1221,7 @@ __device__ void metrics_commit(const SolveParams& p, Smem& sm, MetricAcc& a, int
 // ------------------------------------------------------------------------------------------
 // k_metrics: compute_metrics of the resident state (run node 0)
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSolveThreads) metrics_kernel(const __grid_constant__ SolveParams p) {
+__device__ __forceinline__ void metrics_body(const SolveParams& p) {
     __shared__ Smem sm;
     if (p.ctrl->status) return;
     const double* U = p.buf[kBufU];
@@ -1213,7 +1234,7 @@ __global__ void __launch_bounds__(kSolveThreads) metrics_kernel(const __grid_con
 // K2 prep: RHS g = A u + rho u(1-u) and ||g||_1 partials (run); ||b||_1 / ||b||_inf
 // partials (phi1v / expmv); y = A x (apply)
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSolveThreads, 1) prep_kernel(const __grid_constant__ SolveParams p, int step) {
+__device__ __forceinline__ void prep_body(const SolveParams& p, int step) {
     __shared__ Smem sm;
     extern __shared__ __align__(128) unsigned char dyn[];
     if (p.ctrl->status) return;
@@ -1243,21 +1264,20 @@ __global__ void __launch_bounds__(kSolveThreads, 1) prep_kernel(const __grid_con
     double s[1] = {part};
     if (p.mode == kModeExpmv) block_reduce<1, true>(s, sm);
     else block_reduce<1, false>(s, sm);
-    if (threadIdx.x == 0) p.part_b[blockIdx.x] = s[0];
+    if (threadIdx.x == 0) p.part_b[vcta()] = s[0];
     if (p.use_tma) fence_proxy_async_global();
 }
 
 // ------------------------------------------------------------------------------------------
 // bordered column: ||b||_1, the degenerate branches, gamma and b/gamma + its column sum
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_constant__ SolveParams p, int prep_blocks,
-                                                               int step) {
+__device__ __forceinline__ void border_body(const SolveParams& p, int prep_blocks, int step) {
     if (step < 0) step = __ldcg(&p.ctrl->step);  // graph replay: the step lives on the device
     __shared__ Smem sm;
     Ctrl* ctrl = p.ctrl;
     if (ctrl->status) return;
     trace_mark(p, kTrBorderIn);
-    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool leader = vcta() == 0 && threadIdx.x == 0;
     gs_step_info* info = (p.infos && leader) ? p.infos + step : nullptr;
     const double t = p.tau;
     double* const G = p.buf[kBufG];
@@ -1302,8 +1322,8 @@ __global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_cons
     if (branch != 0) return;
     // b/gamma in place where b != 0 (expact.cpp:137-138) and its column sum (sparse.cpp:36-38)
     double csum = 0.0;
-    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t tid = static_cast<int64_t>(vcta()) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(vncta()) * blockDim.x;
     const int64_t n = p.op.n;
     const int64_t n2 = n >> 1;
     double2* G2 = reinterpret_cast<double2*>(G);
@@ -1330,7 +1350,7 @@ __global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_cons
     }
     double s[1] = {csum};
     block_reduce<1, false>(s, sm);
-    if (threadIdx.x == 0) p.part_c[blockIdx.x] = s[0];
+    if (threadIdx.x == 0) p.part_c[vcta()] = s[0];
     if (p.use_tma) fence_proxy_async_global();
 }
 
@@ -1339,11 +1359,10 @@ __global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_cons
 // two-term sweeps (TMA) or single-term sweeps (fallback) with the in-kernel termination
 // test; grid barriers between terms.  The small-norm branch's stencil pass lives here too.
 // ------------------------------------------------------------------------------------------
-template <int FUSE>
-__global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_constant__ SolveParams p,
-                                                                  int border_blocks, int step) {
+template <int FUSE, class GridBar>
+__device__ __forceinline__ void taylor_body(const SolveParams& p, int border_blocks, int step, GridBar&& grid_bar,
+                                            bool reinit) {
     if (step < 0) step = __ldcg(&p.ctrl->step);  // graph replay: the step lives on the device
-    cg::grid_group grid = cg::this_grid();
     __shared__ SmemT sm;
     extern __shared__ __align__(128) unsigned char dyn[];
     Ctrl* ctrl = p.ctrl;
@@ -1351,19 +1370,19 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
     trace_mark(p, kTrTaylorIn);
     const StencilOp& op = p.op;
     if (threadIdx.x == 0) sm.red = reinterpret_cast<double (*)[6]>(dyn + kRedOffset);
-    block_setup(p, sm, p.use_tma);
+    block_setup(p, sm, p.use_tma, reinit);
     Ring ring{dyn, sm.bar1};
     Ring2 ring2{dyn, sm.bar2};
     Ring2I ring2i{dyn, sm.bar2};
     Ring3 ring3{dyn, sm.bar3x, sm.bar3f};
     uint32_t seq = 0, seq2 = 0, pmask2 = 0, seq3x = 0, seq3f = 0, pm3x = 0, pm3f = 0;
-    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool leader = vcta() == 0 && threadIdx.x == 0;
     gs_step_info* info = (p.infos && leader) ? p.infos + step : nullptr;
     // Grid barrier; with TMA, first order this thread's generic global writes before any
     // later async-proxy (TMA) read of them.
     auto gsync = [&](int tag) {
         if (p.use_tma) fence_proxy_async_global();
-        grid.sync();
+        grid_bar();
         trace_mark(p, tag);
     };
     int round = 0;  // per-term max-reduction rounds (slot rotation, identical in every CTA)
@@ -1447,8 +1466,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
         const double* Tb = p.buf[tres];
         const int fo = (fres == kBufF0) ? kBufF1 : kBufF0;
         double* Fw = p.buf[fo];
-        const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-        const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+        const int64_t tid = static_cast<int64_t>(vcta()) * blockDim.x + threadIdx.x;
+        const int64_t stride = static_cast<int64_t>(vncta()) * blockDim.x;
         const int64_t n2 = op.n >> 1;
         const double2* A2 = reinterpret_cast<const double2*>(Fa);
         const double2* B2 = reinterpret_cast<const double2*>(Tb);
@@ -1831,35 +1850,25 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
     if (leader) {
         ctrl->fres = fres;
         ctrl->tres = tres;
+        ctrl->last_terms = static_cast<int>(total_terms);
     }
     if (p.use_tma) fence_proxy_async_global();
 }
 
-template __global__ void taylor_kernel<2>(const __grid_constant__ SolveParams, int, int);
-template __global__ void taylor_kernel<3>(const __grid_constant__ SolveParams, int, int);
-template __global__ void taylor_kernel<4>(const __grid_constant__ SolveParams, int, int);
-
 __global__ void advance_kernel(Ctrl* ctrl) { ctrl->step += 1; }
-
-// Host-side handles of the instantiations (kept in this translation unit).
-const void* taylor_kernel_fn(int fuse) {
-    return fuse == 3   ? reinterpret_cast<const void*>(taylor_kernel<3>)
-           : fuse == 4 ? reinterpret_cast<const void*>(taylor_kernel<4>)
-                       : reinterpret_cast<const void*>(taylor_kernel<2>);
-}
 
 // ------------------------------------------------------------------------------------------
 // K5 update: u <- u + tau * (gamma/tau) * y (run, + compute_metrics) or out = scale * y
 // ------------------------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(kSolveThreads) update_kernel(const __grid_constant__ SolveParams p, int step) {
+__device__ __forceinline__ void update_body(const SolveParams& p, int step) {
     if (step < 0) step = __ldcg(&p.ctrl->step);  // graph replay: the step lives on the device
     __shared__ Smem sm;
     const Ctrl* ctrl = p.ctrl;
     // The Taylor kernel leaves its last round's maxima in one rotating slot; the next step's
     // first rounds expect all three slots zero (their atomicMax would otherwise see the stale
     // ||f|| of the previous step's last sweep).  The Taylor kernel has finished: stream order.
-    if (blockIdx.x == 0 && threadIdx.x < 24) p.slots[threadIdx.x] = 0ull;
+    if (vcta() == 0 && threadIdx.x < 24) p.slots[threadIdx.x] = 0ull;
     if (__ldcg(&ctrl->status)) return;
     trace_mark(p, kTrUpdateIn);
     const int branch = __ldcg(&ctrl->branch);
@@ -1893,6 +1902,138 @@ __global__ void __launch_bounds__(kSolveThreads) update_kernel(const __grid_cons
     } else {
         sweep_points(p.op, [&](int64_t v) { OUT[v] = incr(v); });
     }
+}
+
+// Software barrier of one CTA group (the ensemble's per-member virtual grid); the pattern of
+// cooperative groups' grid.sync: fence, arrive, the last arriver opens the next generation.
+struct GroupBarrier {
+    unsigned* count;
+    unsigned* gen;
+    unsigned n;
+    __device__ __forceinline__ void sync() const {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned g0 = ld_acquire_gpu(gen);
+            __threadfence();
+            if (atomicAdd(count, 1u) == n - 1) {
+                atomicExch(count, 0u);
+                __threadfence();
+                atomicAdd(gen, 1u);
+            } else {
+                while (ld_acquire_gpu(gen) == g0) {
+                }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    }
+};
+
+template <int FUSE>
+__global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_constant__ SolveParams p,
+                                                                  int border_blocks, int step) {
+    vgrid_set(blockIdx.x, gridDim.x);
+    cg::grid_group grid = cg::this_grid();
+    taylor_body<FUSE>(p, border_blocks, step, [&] { grid.sync(); }, false);
+}
+
+// Ensemble Taylor kernel (cooperative): the grid is cut into gridDim.x / group CTA groups; each
+// group takes members from a queue and runs a member's whole Taylor loop on its virtual grid,
+// with a software group barrier in place of grid.sync.  ctl: per group {count, gen, member[2]}
+// followed by the queue head, zeroed before the launch.
+template <int FUSE>
+__global__ void __launch_bounds__(kSolveThreads, 1) ens_taylor_kernel(const SolveParams* __restrict__ P, int n_members,
+                                                                      int group, int border_blocks, int step,
+                                                                      unsigned* ctl, const unsigned* order) {
+    const int g = blockIdx.x / group;
+    vgrid_set(blockIdx.x % group, group);
+    unsigned* mine = ctl + 4 * g;
+    unsigned* queue = ctl + 4 * (gridDim.x / group);
+    const GroupBarrier bar{mine, mine + 1, static_cast<unsigned>(group)};
+    bool reinit = false;
+    for (int it = 0;; ++it) {
+        // the group leader takes the next member; slots alternate so that a CTA still reading
+        // this iteration's never sees the next one's (the leader passes a group barrier first)
+        if (vcta() == 0 && threadIdx.x == 0) mine[2 + (it & 1)] = atomicAdd(queue, 1u);
+        bar.sync();
+        const int q = static_cast<int>(__ldcg(mine + 2 + (it & 1)));
+        if (q >= n_members) return;  // uniform within the group
+        const int m = static_cast<int>(__ldg(order + q));
+        taylor_body<FUSE>(P[m], border_blocks, step, [&] { bar.sync(); }, reinit);
+        reinit = true;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Kernels of one member (plain launches) and their ensemble forms: CTA b of an ensemble launch
+// works for member b / cpm as CTA b % cpm of cpm.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSolveThreads) metrics_kernel(const __grid_constant__ SolveParams p) {
+    vgrid_set(blockIdx.x, gridDim.x);
+    metrics_body(p);
+}
+__global__ void __launch_bounds__(kSolveThreads, 1) prep_kernel(const __grid_constant__ SolveParams p, int step) {
+    vgrid_set(blockIdx.x, gridDim.x);
+    prep_body(p, step);
+}
+__global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_constant__ SolveParams p, int prep_blocks,
+                                                               int step) {
+    vgrid_set(blockIdx.x, gridDim.x);
+    border_body(p, prep_blocks, step);
+}
+__global__ void __launch_bounds__(kSolveThreads) update_kernel(const __grid_constant__ SolveParams p, int step) {
+    vgrid_set(blockIdx.x, gridDim.x);
+    update_body(p, step);
+}
+__global__ void __launch_bounds__(kSolveThreads) ens_metrics_kernel(const SolveParams* __restrict__ P, int cpm) {
+    vgrid_set(blockIdx.x % cpm, cpm);
+    metrics_body(P[blockIdx.x / cpm]);
+}
+__global__ void __launch_bounds__(kSolveThreads, 1) ens_prep_kernel(const SolveParams* __restrict__ P, int cpm, int step) {
+    vgrid_set(blockIdx.x % cpm, cpm);
+    prep_body(P[blockIdx.x / cpm], step);
+}
+__global__ void __launch_bounds__(kSolveThreads) ens_border_kernel(const SolveParams* __restrict__ P, int cpm,
+                                                                   int prep_blocks, int step) {
+    vgrid_set(blockIdx.x % cpm, cpm);
+    border_body(P[blockIdx.x / cpm], prep_blocks, step);
+}
+__global__ void __launch_bounds__(kSolveThreads) ens_update_kernel(const SolveParams* __restrict__ P, int cpm, int step) {
+    vgrid_set(blockIdx.x % cpm, cpm);
+    update_body(P[blockIdx.x / cpm], step);
+}
+
+template __global__ void taylor_kernel<2>(const __grid_constant__ SolveParams, int, int);
+template __global__ void taylor_kernel<3>(const __grid_constant__ SolveParams, int, int);
+template __global__ void taylor_kernel<4>(const __grid_constant__ SolveParams, int, int);
+template __global__ void ens_taylor_kernel<2>(const SolveParams*, int, int, int, int, unsigned*, const unsigned*);
+template __global__ void ens_taylor_kernel<4>(const SolveParams*, int, int, int, int, unsigned*, const unsigned*);
+
+// The queue's order for the next Taylor launch: members by their last step's Taylor terms,
+// most first (ties by index) -- the longest runs start first, so the groups finish together
+// (longest-processing-time-first).  Before the first step every count is 0: index order.
+__global__ void ens_order_kernel(const SolveParams* __restrict__ P, int n_members, unsigned* order) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_members; i += gridDim.x * blockDim.x) {
+        const int wi = __ldcg(&P[i].ctrl->last_terms);
+        int rank = 0;
+        for (int j = 0; j < n_members; ++j) {
+            const int wj = __ldcg(&P[j].ctrl->last_terms);
+            rank += (wj > wi) || (wj == wi && j < i);
+        }
+        order[rank] = static_cast<unsigned>(i);
+    }
+}
+
+
+// Host-side handles of the instantiations (kept in this translation unit).
+const void* taylor_kernel_fn(int fuse) {
+    return fuse == 3   ? reinterpret_cast<const void*>(taylor_kernel<3>)
+           : fuse == 4 ? reinterpret_cast<const void*>(taylor_kernel<4>)
+                       : reinterpret_cast<const void*>(taylor_kernel<2>);
+}
+const void* ens_taylor_kernel_fn(int fuse) {
+    return fuse == 4 ? reinterpret_cast<const void*>(ens_taylor_kernel<4>)
+                     : reinterpret_cast<const void*>(ens_taylor_kernel<2>);
 }
 
 }  // namespace gs

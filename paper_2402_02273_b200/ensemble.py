@@ -60,7 +60,20 @@ class EnsembleRunner:
         for op, u in zip(self.ops, self.u0):
             op.set_state(u)
 
-    def run(self, steps: int) -> list[MemberResult]:
+    def run(self, steps: int, batched: bool = True, groups: int = 0) -> list[MemberResult]:
+        """Advance every member `steps` steps.  batched: one gs_run_ensemble call (the step's
+        kernels serve all members; the Taylor launch runs `groups` members at a time on
+        groups of SMs); otherwise one gs_run per member, each on the whole GPU."""
+        if batched and self.members:
+            m, inf = self.G.run_ensemble(self.ops, steps, self.rhos, self.w.tau, W.TOL, np.zeros((len(self.ops), 3)),
+                                         np.array(self.centers, dtype=np.float64), 0.1, metrics=True, infos=True,
+                                         groups=groups)
+            out = []
+            for i, (mb, rho) in enumerate(zip(self.members, self.rhos)):
+                met = np.array([[x.total_mass, x.max_density, x.min_density, x.radius] for x in m[i]])
+                terms = np.array([inf[i][q].total_terms for q in range(steps)])
+                out.append(MemberResult(mb, rho, steps, met, terms, float("nan")))
+            return out
         out = []
         for mb, op, c, rho in zip(self.members, self.ops, self.centers, self.rhos):
             m, inf = op.run_resident(steps, rho, self.w.tau, W.TOL, (0.0, 0.0, 0.0), c, 0.1, metrics=True, infos=True)

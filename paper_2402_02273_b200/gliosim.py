@@ -449,6 +449,36 @@ def seed_initial(a: StencilOperator, cfg: SimConfig, mask: bool = True) -> np.nd
     return u
 
 
+def run_ensemble(ops, n_steps: int, rhos, tau: float, tol: float, origins=None, centers=None,
+                 front_threshold: float = 0.1, metrics: bool = True, infos: bool = False, groups: int = 0):
+    """gs_run_ensemble: every member (a StencilOperator with its resident state) advances
+    n_steps steps of run()'s loop (integrator.cpp:91-138), batched over the members.
+    Returns (metrics, infos): per member a list of GsMetrics nodes / GsStepInfo records (or
+    None)."""
+    ops = list(ops)
+    n = len(ops)
+    if n == 0:
+        raise ValueError("run_ensemble: no members")
+    lib = ops[0].lib
+    rhos = np.ascontiguousarray(rhos, dtype=np.float64)
+    if rhos.size != n:
+        raise ValueError("run_ensemble: one rho per member")
+    org = np.ascontiguousarray(origins if origins is not None else np.zeros((n, 3)), dtype=np.float64).reshape(n, 3)
+    cen = np.ascontiguousarray(centers if centers is not None else np.zeros((n, 3)), dtype=np.float64).reshape(n, 3)
+    ctxs = (C.c_void_p * n)(*[o.ctx for o in ops])
+    m = (N.GsMetrics * (n * (n_steps + 1)))() if metrics else None
+    inf = (N.GsStepInfo * max(1, n * n_steps))() if infos else None
+    rc = lib.gs_run_ensemble(ctxs, n, n_steps, rhos, tau, tol, org.ctypes.data_as(C.c_void_p),
+                             cen.ctypes.data_as(C.c_void_p), front_threshold,
+                             C.cast(m, C.c_void_p) if m is not None else None,
+                             C.cast(inf, C.c_void_p) if inf is not None else None, groups)
+    if rc != N.GS_OK:
+        _raise(rc, lib.gs_last_error(ops[0].ctx).decode("utf-8", "surrogateescape"))
+    per_m = [list(m[i * (n_steps + 1):(i + 1) * (n_steps + 1)]) for i in range(n)] if m is not None else None
+    per_i = [list(inf[i * n_steps:(i + 1) * n_steps]) for i in range(n)] if inf is not None else None
+    return per_m, per_i
+
+
 def run(cfg: SimConfig, a: StencilOperator, u0, snapshot=None, on_range=None, on_step=None,
         with_infos: bool = False, _vtk=None) -> RunResult:
     """integrator.cpp:91-138: the time loop runs on the GPU as one launch per segment

@@ -84,3 +84,101 @@ def test_ensemble_members_match_single_runs():
         assert np.linalg.norm(got - u) / np.linalg.norm(u) <= 1e-10
     assert len({round(x, 12) for x in runner.rhos}) == 2
     runner.close()
+
+
+def _random_members(port, shape, k, seed):
+    """k members on one shape: random material fields, sparse initial states, distinct rho."""
+    rng = np.random.default_rng(seed)
+    n = int(np.prod(shape))
+    out = []
+    for i in range(k):
+        d = np.array([0.0, 0.13, 0.013, 0.05])[rng.integers(0, 4, n)]
+        u0 = np.zeros(n)
+        u0[rng.integers(0, n, 60)] = rng.uniform(0.2, 1.0, 60)
+        u0[d == 0.0] = 0.0
+        out.append((d, u0, 0.025 * float(np.exp(rng.uniform(np.log(0.25), np.log(4.0))))))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,groups", [((48, 32, 20), 2), ((48, 32, 20), 3), ((64, 48, 1), 2)])
+def test_batched_ensemble_bitwise_vs_oracle(port, shape, groups):
+    """gs_run_ensemble (one launch per kernel for all members; `groups` members at a time in the
+    Taylor launch, taken from a queue): every member, every step bitwise against the oracle given
+    that member's device sums, terms per stage equal, metrics of the final node exact."""
+    from paper_2402_02273_b200 import gliosim as G
+    h, tau, tol, steps = 2.0, 33.5, 1e-8, 3
+    members = _random_members(port, shape, 5, sum(shape) + groups)
+    ops = [G.assemble_diffusion(G.Grid(*shape, h=h), d) for d, _, _ in members]
+    try:
+        for op, (_, u0, _) in zip(ops, members):
+            op.set_state(u0)
+        centers = np.array([[10.0, 8.0, 4.0 * (i + 1)] for i in range(len(ops))])
+        mets, infos = G.run_ensemble(ops, steps, [r for _, _, r in members], tau, tol, None, centers, 0.1,
+                                     metrics=True, infos=True, groups=groups)
+        for i, (op, (d, u0, rho)) in enumerate(zip(ops, members)):
+            op_o = port.stencil(shape, h, d)
+            u = u0
+            for q in range(steps):
+                inf = infos[i][q]
+                u, log = port.step(op_o, u, rho, tau, tol, bnorm=inf.bnorm, coln=inf.coln)
+                assert inf.stage_terms() == log.stage_terms(), (i, q)
+            got = op.get_state()
+            assert np.array_equal(got, u), i
+            assert mets[i][steps].max_density == got.max()
+            assert mets[i][steps].min_density == got.min()
+    finally:
+        for op in ops:
+            op.close()
+
+
+@pytest.mark.gpu
+def test_batched_ensemble_matches_sequential_runs(port, monkeypatch):
+    """The batched ensemble against the same members run one after another (gs_run each): the
+    same terms per stage, states equal up to the ulps of the per-CTA partial sums."""
+    from paper_2402_02273_b200 import gliosim as G
+    shape, h, tau, tol, steps = (48, 32, 20), 2.0, 33.5, 1e-8, 4
+    members = _random_members(port, shape, 4, 99)
+    finals = {}
+    for mode in ("batched", "sequential"):
+        if mode == "sequential":
+            monkeypatch.setenv("GS_ENS_SEQUENTIAL", "1")
+        ops = [G.assemble_diffusion(G.Grid(*shape, h=h), d) for d, _, _ in members]
+        try:
+            for op, (_, u0, _) in zip(ops, members):
+                op.set_state(u0)
+            _, infos = G.run_ensemble(ops, steps, [r for _, _, r in members], tau, tol, metrics=False, infos=True)
+            finals[mode] = ([op.get_state() for op in ops],
+                            [[infos[i][q].stage_terms() for q in range(steps)] for i in range(len(ops))])
+        finally:
+            for op in ops:
+                op.close()
+    (ub, tb), (us, ts) = finals["batched"], finals["sequential"]
+    assert tb == ts
+    for a, b in zip(ub, us):
+        assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(b)
+
+
+@pytest.mark.gpu
+def test_ensemble_mixed_shapes_fall_back_to_sequential(port):
+    """Members the batched path cannot take together (here 2-D with 3-D) run one by one."""
+    from paper_2402_02273_b200 import gliosim as G
+    specs = [((48, 32, 20), 7), ((64, 48, 1), 8)]
+    ops, refs = [], []
+    try:
+        for shape, seed in specs:
+            (d, u0, rho), = _random_members(port, shape, 1, seed)
+            op = G.assemble_diffusion(G.Grid(*shape, h=2.0), d)
+            op.set_state(u0)
+            ops.append(op)
+            refs.append((shape, d, u0, rho))
+        _, infos = G.run_ensemble(ops, 2, [r[3] for r in refs], 33.5, 1e-8, metrics=False, infos=True)
+        for i, (op, (shape, d, u0, rho)) in enumerate(zip(ops, refs)):
+            u = u0
+            for q in range(2):
+                u, _ = port.step(port.stencil(shape, 2.0, d), u, rho, 33.5, 1e-8, bnorm=infos[i][q].bnorm,
+                                 coln=infos[i][q].coln)
+            assert np.array_equal(op.get_state(), u)
+    finally:
+        for op in ops:
+            op.close()
