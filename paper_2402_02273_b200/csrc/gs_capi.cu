@@ -474,6 +474,8 @@ gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps
 // 8-10% faster than 148).
 int solve_blocks(const gs_ctx* c) {
     int gb = c->grid_blocks;
+    if (const char* e = std::getenv("GS_GRID"))  // A/B of the CTA count (capped at co-residency)
+        gb = std::max(1, std::min(gb, std::atoi(e)));
     if (c->tma_ok && c->palette_mode && !c->is_csr) {
         const int64_t q = static_cast<int64_t>((c->nx + gs::kTmaTX - 1) / gs::kTmaTX) *
                           ((c->ny + gs::kTmaTY - 1) / gs::kTmaTY) * c->nz;
