@@ -32,10 +32,11 @@ def main():
     ap.add_argument("--alg-gb", type=float, default=None, help="algorithmic GB per launch (bench.py)")
     ap.add_argument("--traffic-json", default=None)
     ap.add_argument("--config", default="C4")
+    ap.add_argument("--kernel-desc", default="taylor_kernel<2> (C4 256^3, one exponential-Euler step = 1 launch)")
+    ap.add_argument("--command", default=CMD)
     a = ap.parse_args()
 
-    lines = [f"# ncu --set full, taylor_kernel<2> (C4 256^3, one exponential-Euler step = 1 launch), {a.title}",
-             f"# command: {CMD}", ""]
+    lines = [f"# ncu --set full, {a.kernel_desc}, {a.title}", f"# command: {a.command}", ""]
     det = ncu_csv(a.rep, "details")
     h = det[0]
     si, mi, ui, vi = (h.index(k) for k in ("Section Name", "Metric Name", "Metric Unit", "Metric Value"))
