@@ -1251,8 +1251,11 @@ gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const
                           const double* origins, const double* centers, double front_threshold, gs_metrics* metrics,
                           gs_step_info* infos, int groups) {
     if (!ctxs || n_members < 1 || !rhos) return fail(nullptr, GS_EINVAL, "run_ensemble: null argument or no members");
-    for (int i = 0; i < n_members; ++i)
+    for (int i = 0; i < n_members; ++i) {
         if (!ctxs[i]) return fail(nullptr, GS_EINVAL, "run_ensemble: null member context");
+        for (int j = 0; j < i; ++j)  // a member's buffers must belong to it alone
+            if (ctxs[j] == ctxs[i]) return fail(ctxs[i], GS_EINVAL, "run_ensemble: a context appears twice");
+    }
     gs_ctx* const c0 = ctxs[0];
     if (n_steps < 0) return fail(c0, GS_EINVAL, "run: negative step count");
     if (!tol_ok(tol)) return fail(c0, GS_EINVAL, "phi1v: tolerance must lie in (0, 1)");

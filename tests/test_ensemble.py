@@ -182,3 +182,24 @@ def test_ensemble_mixed_shapes_fall_back_to_sequential(port):
     finally:
         for op in ops:
             op.close()
+
+
+@pytest.mark.gpu
+def test_ensemble_argument_errors(port):
+    """Bad ensembles fail like the reference's run() does for one member (std::invalid_argument
+    -> ValueError), before any device work."""
+    from paper_2402_02273_b200 import gliosim as G
+    (d, u0, rho), = _random_members(port, (48, 32, 20), 1, 3)
+    with G.assemble_diffusion(G.Grid(48, 32, 20, h=2.0), d) as a, \
+            G.assemble_diffusion(G.Grid(48, 32, 20, h=2.0), d) as b:
+        a.set_state(u0)
+        b.set_state(u0)
+        with pytest.raises(ValueError, match="appears twice"):
+            G.run_ensemble([a, a], 1, [rho, rho], 33.5, 1e-8)
+        with pytest.raises(ValueError, match="tolerance"):
+            G.run_ensemble([a, b], 1, [rho, rho], 33.5, 1.5)
+        with pytest.raises(ValueError, match="one rho per member"):
+            G.run_ensemble([a, b], 1, [rho], 33.5, 1e-8)
+        with pytest.raises(ValueError, match="no members"):
+            G.run_ensemble([], 1, [], 33.5, 1e-8)
+        assert np.array_equal(a.get_state(), u0) and np.array_equal(b.get_state(), u0)
