@@ -84,14 +84,55 @@ def measured_peak():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region: an NVML
+    thread polls every 2 ms between __enter__ and __exit__ (the first sample is taken on
+    entry, so even a ~0.1 s region has samples); nvidia-smi -lms is the fallback."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index):
         self.index = index
+        self.samples = []
+        self.max_mhz = 0.0
+        self.nvml = None
         self.proc = None
         self.path = f"/tmp/gs_clocks_{os.getpid()}.csv"
+        try:
+            import threading
+
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            nvml_index = torch.cuda._get_nvml_device_index(index)  # honours CUDA_VISIBLE_DEVICES
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(nvml_index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+            self.nvml = pynvml
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+        except Exception:
+            self.nvml = None
+
+    def _sample(self):
+        N = self.nvml
+        sm = float(N.nvmlDeviceGetClockInfo(self.handle, N.NVML_CLOCK_SM))
+        bits = N.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+        self.samples.append((sm, {nm for nm, attr in self.REASONS if bits & getattr(N, attr)}))
+
+    def _poll(self):
+        while not self.stop.wait(0.002):
+            try:
+                self._sample()
+            except Exception:
+                return
 
     def __enter__(self):
+        if self.nvml:
+            self._sample()
+            self.thread.start()
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
@@ -105,6 +146,13 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
+        if self.nvml:
+            self.stop.set()
+            self.thread.join(timeout=5)
+            try:
+                self._sample()
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -113,12 +161,18 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
+        if self.nvml:
+            if not self.samples:
+                return None
+            reasons = set().union(*(r for _, r in self.samples))
+            return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                    "reasons": sorted(reasons), "samples": len(self.samples), "source": "nvml (2 ms)"}
         try:
             rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
         except Exception:
             return None
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        names = [nm for nm, _ in self.REASONS]
         for r in rows:
             try:
                 sm.append(float(r[0]))
@@ -130,7 +184,8 @@ class Clocks:
                 continue
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvidia-smi -lms 50"}
 
 
 def build_case(w, member=0):
