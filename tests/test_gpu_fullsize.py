@@ -74,3 +74,33 @@ def test_c4_uniform_diffusion_conserves_mass_and_semigroup(c4):
         assert y.min() >= -1e-12 * u0.max() and y.max() <= u0.max() * (1 + 1e-12)  # max principle
         y_ab = G.expmv(120.0, a, G.expmv(80.0, a, u0, 1e-12), 1e-12)
         assert rel_l2(y_ab, y) <= 1e-9
+
+
+def test_c5_batched_members_match_oracle(port):
+    """C5 at full member size (128^3): three members of the real ensemble (lowest, highest and
+    a middle rho) advanced two batched steps (gs_run_ensemble, 16 groups, the members taken from
+    the queue) -- every member and step bitwise against the oracle given that member's device
+    sums, terms per stage exact, and within the per-step bar without the sums."""
+    from paper_2402_02273_b200 import ensemble as E
+    from paper_2402_02273_b200 import workloads as W
+    w = W.get("C5")
+    rhos = [W.member_rho(w, mb) for mb in range(w.members)]
+    pick = sorted({int(np.argmin(rhos)), int(np.argmax(rhos)), w.members // 2})
+    runner = E.EnsembleRunner(w, pick)
+    try:
+        runner.reset()
+        from paper_2402_02273_b200 import gliosim as G
+        _, infos = G.run_ensemble(runner.ops, 2, runner.rhos, w.tau, W.TOL, metrics=False, infos=True)
+        for i, (op, u0, rho) in enumerate(zip(runner.ops, runner.u0, runner.rhos)):
+            op_o = port.stencil((w.nx, w.ny, w.nz), w.h, port.diffusion_from_labels(op.labels()))
+            u = u0
+            for q in range(2):
+                inf = infos[i][q]
+                want, log = port.step(op_o, u, rho, w.tau, W.TOL, bnorm=inf.bnorm, coln=inf.coln)
+                assert inf.stage_terms() == log.stage_terms(), (i, q)
+                plain, _ = port.step(op_o, u, rho, w.tau, W.TOL)
+                assert rel_l2(want, plain) <= 1e-10
+                u = want
+            assert np.array_equal(op.get_state(), u), i
+    finally:
+        runner.close()
