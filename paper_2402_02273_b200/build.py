@@ -44,9 +44,12 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+    if not force and not stale() and "GS_LIB_OUT" not in os.environ:
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB,
+    # GS_NVCC_EXTRA (e.g. "-DGS_TILE8") and GS_LIB_OUT build A/B variants of the library
+    extra = os.environ.get("GS_NVCC_EXTRA", "").split()
+    out = os.environ.get("GS_LIB_OUT", LIB)
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", out,
            *[os.path.join(CSRC, s) for s in SOURCES]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(CSRC, "build.log")

@@ -22,9 +22,18 @@ enum Buf : int { kBufU = 0, kBufG = 1, kBufF0 = 2, kBufF1 = 3, kBufT0 = 4, kBufT
 // TMA z-slab pipeline geometry: a CTA owns tiles of kTmaTX x kTmaTY columns and
 // streams their z-planes through a kTmaStages-deep shared-memory ring.
 constexpr int kTmaTX = 64;
+#ifdef GS_TILE8
+// A/B variant: 64 x 8 tiles, 256 threads, two CTAs per SM (each CTA's per-plane barrier then
+// overlaps the other CTA's work).
+constexpr int kTmaTY = 8;
+constexpr int kSolveThreads = 256;
+constexpr int kMinBlocks = 2;        // __launch_bounds__ of the TMA kernels: 2 CTAs/SM, 128 regs
+#else
 constexpr int kTmaTY = 16;
-constexpr int kTmaStages = 6;
 constexpr int kSolveThreads = 512;   // 16 warps: warp w owns tile row w, two columns per lane
+constexpr int kMinBlocks = 1;
+#endif
+constexpr int kTmaStages = 6;
 
 // The halo box starts two voxels left of the tile: TMA needs the innermost start coordinate
 // times the element size to be a multiple of 16 bytes (measured: x0-1 faults on sm_100a).
@@ -39,7 +48,11 @@ constexpr int kRingBytes = kTmaStages * kSlotBytes + 128;              // + barr
 // Two-term fused sweep (temporal blocking): T_{j+1} is computed on the tile plus a one-voxel
 // halo and kept in a 3-plane shared ring, T_{j+2} on the tile; the input therefore needs a
 // two-voxel halo in x, y and z.
+#ifdef GS_TILE8
+constexpr int k2Stages = 7;
+#else
 constexpr int k2Stages = 8;
+#endif
 constexpr int k2XRows = kTmaTY + 4;                                     // y halo 2
 constexpr int k2XBytes = (k2XRows * kXPitch * 8 + 127) / 128 * 128;    // 20 x 68 doubles
 constexpr int k2BRows = kTmaTY + 2;                                     // y halo 1
@@ -56,7 +69,11 @@ constexpr int kT1Bytes = kT1Rows * kT1Pitch * 8;
 constexpr int kT1Planes = 3;  // T1(z+1) is written while T1(z-1) is read; T1(z) is kept for the next iteration
 constexpr int k2RingBytes = k2Stages * k2SlotBytes + kT1Planes * kT1Bytes + 128;
 // implicit-X ring (a stage's first sweep reads f = F + T): F and T halo-2 tiles per slot
+#ifdef GS_TILE8
+constexpr int k2IStages = 4;
+#else
 constexpr int k2IStages = 6;
+#endif
 constexpr int k2ISlotBytes = 2 * k2XBytes + k2FBBytes + k2LBytes;
 constexpr int k2IRingBytes = k2IStages * k2ISlotBytes + kT1Planes * kT1Bytes + 128;
 
@@ -71,11 +88,19 @@ constexpr int k3XBytes = (k3XRows * k3XPitch * 8 + 127) / 128 * 128;    // 22 x 
 constexpr int k3LRows = kTmaTY + 4;                                     // labels, y halo 2
 constexpr int k3LBytes = (k3LRows * kLPitch + 127) / 128 * 128;         // 20 x 96 labels
 constexpr int k3XSlotBytes = k3XBytes + k3LBytes;
+#ifdef GS_TILE8
+constexpr int k3XStages = 5;
+#else
 constexpr int k3XStages = 7;
+#endif
 constexpr int k3BRows = kTmaTY + 4;                                     // b/gamma, y halo 2
 constexpr int k3BBytes = (k3BRows * k3XPitch * 8 + 127) / 128 * 128;    // 20 x 72 doubles
 constexpr int k3FBBytes = kOBytes > k3BBytes ? kOBytes : k3BBytes;
+#ifdef GS_TILE8
+constexpr int k3FBStages = 2;
+#else
 constexpr int k3FBStages = 3;
+#endif
 constexpr int k3T1Pitch = kTmaTX + 4;
 constexpr int k3T1Rows = kTmaTY + 4;
 constexpr int k3T1Bytes = k3T1Rows * k3T1Pitch * 8;
@@ -91,7 +116,7 @@ constexpr int kMaxRing = kMaxRing0 > k2IRingBytes ? kMaxRing0 : k2IRingBytes;
 constexpr int kDynSmemBytes = kMaxRing > k3RingBytes ? kMaxRing : k3RingBytes;
 // the Taylor kernel's block-reduction scratch (16 x 6 doubles) at the end of the dynamic
 // region: past every TMA-written byte of every ring (the implicit ring's T1 planes, generic)
-constexpr int kRedOffset = kDynSmemBytes - 128 - 768;
+constexpr int kRedOffset = kDynSmemBytes - 128 - 768;  // (kSolveThreads / 32) x 6 doubles <= 768 B
 static_assert(kRedOffset >= k2IStages * k2ISlotBytes && kRedOffset >= k2Stages * k2SlotBytes &&
                   kRedOffset >= kTmaStages * kSlotBytes && kRedOffset >= k3XStages * k3XSlotBytes + k3FBStages * k3FBBytes,
               "reduction scratch overlaps a TMA-written region");

@@ -574,9 +574,11 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
             xo[0] = Xs[oX] = __dadd_rn(Xs[oX], Ts[oX]);
             xo[1] = Xs[oX + kXPitch] = __dadd_rn(Xs[oX + kXPitch], Ts[oX + kXPitch]);
             if (ringer) Xs[rX] = __dadd_rn(Xs[rX], Ts[rX]);
-            // outer halo (172 points): X-tile rows 0 and 19, then columns 0 and 67 of rows 1..18
-            const int e = tid - kRing;
-            if (e >= 0 && e < 2 * kXPitch + 2 * (kTmaTY + 2)) {
+            // outer halo (172 points with 16-row tiles): X-tile rows 0 and k2XRows-1, then columns
+            // 0 and kXPitch-1 of the rows between; threads from kRing on, wrapping if too few
+            constexpr int kOuter = 2 * kXPitch + 2 * (kTmaTY + 2);
+            for (int e = tid - kRing; e < kOuter; e += kSolveThreads - kRing) {
+                if (e < 0) break;
                 const int f = e - 2 * kXPitch;
                 const int o = f < 0 ? (e < kXPitch ? e : (k2XRows - 1) * kXPitch + e - kXPitch)
                                     : (1 + (f >> 1)) * kXPitch + ((f & 1) ? kXPitch - 1 : 0);
@@ -778,7 +780,7 @@ __device__ __forceinline__ void sweep3_tma(const SolveParams& p, const Ring3& ri
     constexpr uint32_t kBTx = k3BRows * k3XPitch * 8;
     constexpr int kARing = 2 * (kTmaTX + 4) * 2 + 4 * kTmaTY;  // 336 points of T1's two-voxel ring
     constexpr int kBRing = 2 * (kTmaTX + 2) + 2 * kTmaTY;      // 164 points of T2's one-voxel ring
-    static_assert(kARing + kBRing <= kSolveThreads, "ring points need one thread each");
+    static_assert(KIND < 0 || kARing + kBRing <= kSolveThreads, "ring points need one thread each");
     const StencilOp& op = p.op;
     const int tid = threadIdx.x;
     const int xl = tid & (kTmaTX - 1);
@@ -1930,7 +1932,7 @@ struct GroupBarrier {
 };
 
 template <int FUSE>
-__global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_constant__ SolveParams p,
+__global__ void __launch_bounds__(kSolveThreads, kMinBlocks) taylor_kernel(const __grid_constant__ SolveParams p,
                                                                   int border_blocks, int step) {
     vgrid_set(blockIdx.x, gridDim.x);
     cg::grid_group grid = cg::this_grid();
@@ -1942,7 +1944,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) taylor_kernel(const __grid_c
 // with a software group barrier in place of grid.sync.  ctl: per group {count, gen, member[2]}
 // followed by the queue head, zeroed before the launch.
 template <int FUSE>
-__global__ void __launch_bounds__(kSolveThreads, 1) ens_taylor_kernel(const SolveParams* __restrict__ P, int n_members,
+__global__ void __launch_bounds__(kSolveThreads, kMinBlocks) ens_taylor_kernel(const SolveParams* __restrict__ P, int n_members,
                                                                       int group, int border_blocks, int step,
                                                                       unsigned* ctl, const unsigned* order) {
     const int g = blockIdx.x / group;
@@ -1972,7 +1974,7 @@ __global__ void __launch_bounds__(kSolveThreads) metrics_kernel(const __grid_con
     vgrid_set(blockIdx.x, gridDim.x);
     metrics_body(p);
 }
-__global__ void __launch_bounds__(kSolveThreads, 1) prep_kernel(const __grid_constant__ SolveParams p, int step) {
+__global__ void __launch_bounds__(kSolveThreads, kMinBlocks) prep_kernel(const __grid_constant__ SolveParams p, int step) {
     vgrid_set(blockIdx.x, gridDim.x);
     prep_body(p, step);
 }
@@ -1989,7 +1991,7 @@ __global__ void __launch_bounds__(kSolveThreads) ens_metrics_kernel(const SolveP
     vgrid_set(blockIdx.x % cpm, cpm);
     metrics_body(P[blockIdx.x / cpm]);
 }
-__global__ void __launch_bounds__(kSolveThreads, 1) ens_prep_kernel(const SolveParams* __restrict__ P, int cpm, int step) {
+__global__ void __launch_bounds__(kSolveThreads, kMinBlocks) ens_prep_kernel(const SolveParams* __restrict__ P, int cpm, int step) {
     vgrid_set(blockIdx.x % cpm, cpm);
     prep_body(P[blockIdx.x / cpm], step);
 }
@@ -2004,7 +2006,9 @@ __global__ void __launch_bounds__(kSolveThreads) ens_update_kernel(const SolvePa
 }
 
 template __global__ void taylor_kernel<2>(const __grid_constant__ SolveParams, int, int);
+#ifndef GS_TILE8
 template __global__ void taylor_kernel<3>(const __grid_constant__ SolveParams, int, int);
+#endif
 template __global__ void taylor_kernel<4>(const __grid_constant__ SolveParams, int, int);
 template __global__ void ens_taylor_kernel<2>(const SolveParams*, int, int, int, int, unsigned*, const unsigned*);
 template __global__ void ens_taylor_kernel<4>(const SolveParams*, int, int, int, int, unsigned*, const unsigned*);
@@ -2027,9 +2031,14 @@ __global__ void ens_order_kernel(const SolveParams* __restrict__ P, int n_member
 
 // Host-side handles of the instantiations (kept in this translation unit).
 const void* taylor_kernel_fn(int fuse) {
+#ifdef GS_TILE8
+    // the three-term rings need more threads than a 64 x 8 tile has
+    return fuse == 4 ? reinterpret_cast<const void*>(taylor_kernel<4>) : reinterpret_cast<const void*>(taylor_kernel<2>);
+#else
     return fuse == 3   ? reinterpret_cast<const void*>(taylor_kernel<3>)
            : fuse == 4 ? reinterpret_cast<const void*>(taylor_kernel<4>)
                        : reinterpret_cast<const void*>(taylor_kernel<2>);
+#endif
 }
 const void* ens_taylor_kernel_fn(int fuse) {
     return fuse == 4 ? reinterpret_cast<const void*>(ens_taylor_kernel<4>)
