@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <condition_variable>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -409,11 +410,15 @@ gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps
     GS_CUDA(c, c->part_u.alloc(sizeof(double) * pb));
     GS_CUDA(c, c->slots.alloc(sizeof(unsigned long long) * 24));
     GS_CUDA(c, c->mslots.alloc(sizeof(unsigned long long) * 4));
+    const bool fresh_ctrl = c->ctrl.p == nullptr;
     GS_CUDA(c, c->ctrl.alloc(sizeof(gs::Ctrl)));
     GS_CUDA(c, cudaMemsetAsync(c->slots.p, 0, sizeof(unsigned long long) * 24, c->stream));
     const unsigned long long ms_init[4] = {0ull, ~0ull, 0ull, 0ull};
     GS_CUDA(c, cudaMemcpyAsync(c->mslots.p, ms_init, sizeof ms_init, cudaMemcpyHostToDevice, c->stream));
-    GS_CUDA(c, cudaMemsetAsync(c->ctrl.p, 0, sizeof(gs::Ctrl), c->stream));
+    // a new run starts from a clean control block, except last_terms (the previous call's
+    // Taylor terms, which orders the next ensemble queue): it is the last field
+    GS_CUDA(c, cudaMemsetAsync(c->ctrl.p, 0, fresh_ctrl ? sizeof(gs::Ctrl) : offsetof(gs::Ctrl, last_terms),
+                               c->stream));
     if (c->stage_in)
         GS_CUDA(c, cudaMemcpyAsync(c->u.p, c->stage_in, sizeof(double) * static_cast<size_t>(c->n),
                                    cudaMemcpyHostToDevice, c->stream));
