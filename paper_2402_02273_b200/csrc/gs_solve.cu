@@ -414,7 +414,9 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
     constexpr uint32_t kXTx = k2XRows * kXPitch * 8;
     constexpr uint32_t kBTx = k2BRows * kXPitch * 8;
     constexpr uint32_t kLTx = (kTmaTY + 2) * kLPitch;
-    constexpr int kRing = 2 * (kTmaTX + 2) + 2 * kTmaTY;  // 164 halo-ring points of T1
+    // T1 halo ring: rows -1 and 16 over columns 0..63, columns -1 and 64 over rows 0..15 --
+    // phase B's 5-point in-plane stencil never reads the four corners.  160 points: warps 0-4.
+    constexpr int kRing = 2 * kTmaTX + 2 * kTmaTY;
     const StencilOp& op = p.op;
     // dead-row selects only in the exact instantiation (row_apply_ns)
     auto rowap = [](double w, bool live, double negcnt, double a, double b, double c, double d, double e, double f,
@@ -430,15 +432,16 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
     const int oL = (ry0 + 1) * kLPitch + xl + kLHaloX;  // own row 0 in the label tile
     const int oB = oX - kXPitch;                        // own row 0 in the b/gamma tile
     const int oF = ry0 * kTmaTX + xl;                   // own row 0 in the F tile
-    // this thread's ring point (rows -1 and 16, then columns -1 and 64)
+    // this thread's ring point (rows -1 and 16, then columns -1 and 64); ring coordinates
+    // (rr, rc) count from row -1 / column -1
     const bool ringer = tid < kRing;
     int rr = 0, rc = 0;
     if (ringer) {
-        if (tid < 2 * (kTmaTX + 2)) {
-            rr = tid < kTmaTX + 2 ? 0 : kTmaTY + 1;
-            rc = tid < kTmaTX + 2 ? tid : tid - (kTmaTX + 2);
+        if (tid < 2 * kTmaTX) {
+            rr = tid < kTmaTX ? 0 : kTmaTY + 1;
+            rc = (tid & (kTmaTX - 1)) + 1;
         } else {
-            const int e = tid - 2 * (kTmaTX + 2);
+            const int e = tid - 2 * kTmaTX;
             rr = 1 + (e >> 1);
             rc = (e & 1) ? kTmaTX + 1 : 0;
         }
@@ -575,13 +578,22 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
             xo[1] = Xs[oX + kXPitch] = __dadd_rn(Xs[oX + kXPitch], Ts[oX + kXPitch]);
             if (ringer) Xs[rX] = __dadd_rn(Xs[rX], Ts[rX]);
             // outer halo (172 points with 16-row tiles): X-tile rows 0 and k2XRows-1, then columns
-            // 0 and kXPitch-1 of the rows between; threads from kRing on, wrapping if too few
-            constexpr int kOuter = 2 * kXPitch + 2 * (kTmaTY + 2);
+            // 0 and kXPitch-1 of the rows between; then the four ring corners (row -1 / 16 x
+            // column -1 / 64: not T1 ring points, but x-neighbours of the ring's end points);
+            // threads from kRing on, wrapping if too few
+            constexpr int kEdge = 2 * kXPitch + 2 * (kTmaTY + 2);
+            constexpr int kOuter = kEdge + 4;
             for (int e = tid - kRing; e < kOuter; e += kSolveThreads - kRing) {
                 if (e < 0) break;
                 const int f = e - 2 * kXPitch;
-                const int o = f < 0 ? (e < kXPitch ? e : (k2XRows - 1) * kXPitch + e - kXPitch)
-                                    : (1 + (f >> 1)) * kXPitch + ((f & 1) ? kXPitch - 1 : 0);
+                int o;
+                if (e >= kEdge) {
+                    const int k = e - kEdge;
+                    o = ((k & 2) ? kTmaTY + 2 : 1) * kXPitch + ((k & 1) ? kTmaTX + 2 : 1);
+                } else {
+                    o = f < 0 ? (e < kXPitch ? e : (k2XRows - 1) * kXPitch + e - kXPitch)
+                              : (1 + (f >> 1)) * kXPitch + ((f & 1) ? kXPitch - 1 : 0);
+                }
                 Xs[o] = __dadd_rn(Xs[o], Ts[o]);
             }
             fence_proxy_async_shared();  // generic writes into a TMA slot before its next fill
