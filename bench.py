@@ -85,8 +85,8 @@ def measured_peak():
 
 class Clocks:
     """SM clock and clock-event (throttle) reasons sampled DURING the timed region: an NVML
-    thread polls every 2 ms between __enter__ and __exit__ (the first sample is taken on
-    entry, so even a ~0.1 s region has samples); nvidia-smi -lms is the fallback."""
+    thread polls every 10 ms between __enter__ and __exit__, with one sample on entry and one
+    on exit, so even a short region has samples; nvidia-smi -lms is the fallback."""
 
     REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
                ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -100,7 +100,11 @@ class Clocks:
         self.nvml = None
         self.proc = None
         self.path = f"/tmp/gs_clocks_{os.getpid()}.csv"
+        # 10 ms: NVML queries from a second thread cost launch-bound runs (C1) ~3% at 2 ms
+        self.period = float(os.environ.get("GS_CLOCKS_PERIOD_MS", "10")) / 1e3
         try:
+            if os.environ.get("GS_CLOCKS") == "smi":
+                raise RuntimeError("nvidia-smi sampling requested")
             import threading
 
             import pynvml
@@ -122,7 +126,7 @@ class Clocks:
         self.samples.append((sm, {nm for nm, attr in self.REASONS if bits & getattr(N, attr)}))
 
     def _poll(self):
-        while not self.stop.wait(0.002):
+        while not self.stop.wait(self.period):
             try:
                 self._sample()
             except Exception:
@@ -166,7 +170,8 @@ class Clocks:
                 return None
             reasons = set().union(*(r for _, r in self.samples))
             return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
-                    "reasons": sorted(reasons), "samples": len(self.samples), "source": "nvml (2 ms)"}
+                    "reasons": sorted(reasons), "samples": len(self.samples),
+                    "source": f"nvml every {self.period * 1e3:g} ms (+ entry/exit samples)"}
         try:
             rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
         except Exception:
