@@ -402,7 +402,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
     // Register-blocked layout: thread t owns column xl = t % 64 and rows ry0 = 2*(t/64), ry0+1 of
     // the 64 x 16 tile for the whole z-march, so its z-1/z/z+1 values of X and T1 and its own
     // y-neighbour live in registers; x-neighbours and the outer y-neighbours come from shared
-    // memory.  The 164 halo-ring points of T1 are computed by threads 0..163 from shared memory.
+    // memory.  The 160 halo-ring points of T1 (no corners) are computed by threads 0..159 from shared memory.
     // All per-thread shared-memory offsets are fixed per tile; ring slots rotate by increment and
     // barrier parities are tracked in a bit mask (identical in every thread).
     constexpr bool needX = KIND != k2FirstZero;
