@@ -38,7 +38,14 @@ constexpr int kTmaStages = 6;
 // The halo box starts two voxels left of the tile: TMA needs the innermost start coordinate
 // times the element size to be a multiple of 16 bytes (measured: x0-1 faults on sm_100a).
 constexpr int kXHalo = 2;                                              // x halo (left/right)
-constexpr int kXPitch = kTmaTX + 2 * kXHalo;                           // doubles per halo row
+constexpr int kXCols = kTmaTX + 2 * kXHalo;                            // halo row: x0-2 .. x0+65
+#ifdef GS_XPAD
+// two more (unused) columns per row: a 70-double pitch spreads the column ring's rows over
+// more shared-memory banks (row stride 140 words: 2-way instead of 4-way conflicts)
+constexpr int kXPitch = kXCols + 2;
+#else
+constexpr int kXPitch = kXCols;                                        // doubles per halo row
+#endif
 constexpr int kXBytes = ((kTmaTY + 2) * kXPitch * 8 + 127) / 128 * 128;  // halo plane tile
 constexpr int kOBytes = kTmaTX * kTmaTY * 8;                            // own plane tile (fp64)
 constexpr int kLBytes = kTmaTX * kTmaTY;                                // own plane tile (labels)
@@ -71,6 +78,8 @@ constexpr int k2RingBytes = k2Stages * k2SlotBytes + kT1Planes * kT1Bytes + 128;
 // implicit-X ring (a stage's first sweep reads f = F + T): F and T halo-2 tiles per slot
 #ifdef GS_TILE8
 constexpr int k2IStages = 4;
+#elif defined(GS_XPAD)
+constexpr int k2IStages = 5;
 #else
 constexpr int k2IStages = 6;
 #endif

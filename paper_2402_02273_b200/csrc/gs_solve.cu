@@ -597,7 +597,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
                     o = ((k & 2) ? kTmaTY + 2 : 1) * kXPitch + ((k & 1) ? kTmaTX + 2 : 1);
                 } else {
                     o = f < 0 ? (e < kXPitch ? e : (k2XRows - 1) * kXPitch + e - kXPitch)
-                              : (1 + (f >> 1)) * kXPitch + ((f & 1) ? kXPitch - 1 : 0);
+                              : (1 + (f >> 1)) * kXPitch + ((f & 1) ? kXCols - 1 : 0);
                 }
                 Xs[o] = __dadd_rn(Xs[o], Ts[o]);
             }
