@@ -203,3 +203,46 @@ def test_ensemble_argument_errors(port):
         with pytest.raises(ValueError, match="no members"):
             G.run_ensemble([], 1, [], 33.5, 1e-8)
         assert np.array_equal(a.get_state(), u0) and np.array_equal(b.get_state(), u0)
+
+
+@pytest.mark.gpu
+def test_batched_ensemble_heterogeneous_members(port):
+    """Members of different 3-D shapes and the degenerate branches of phi1v in one batched
+    call: b = 0 (u = 0: expact.cpp:111, the Taylor body returns before any group barrier),
+    A = 0 (D = 0 everywhere: the small-norm branch, expact.cpp:114-121) and ordinary members,
+    2 groups, several steps -- each member bitwise against the oracle given its device sums."""
+    from paper_2402_02273_b200 import gliosim as G
+    rng = np.random.default_rng(11)
+    specs = []
+    for shape, kind in [((48, 32, 20), "plain"), ((64, 48, 24), "zero_u"), ((48, 32, 20), "zero_d"),
+                        ((64, 16, 12), "plain"), ((32, 32, 32), "plain")]:
+        n = int(np.prod(shape))
+        d = np.array([0.0, 0.13, 0.013, 0.05])[rng.integers(0, 4, n)]
+        if kind == "zero_d":
+            d = np.zeros(n)
+        u0 = np.zeros(n)
+        if kind != "zero_u":
+            u0[rng.integers(0, n, 50)] = rng.uniform(0.2, 1.0, 50)
+            u0[d == 0.0] = 0.0 if kind != "zero_d" else u0[d == 0.0]
+        specs.append((shape, d, u0, 0.025 * (1 + len(specs))))
+    ops = [G.assemble_diffusion(G.Grid(*sh, h=2.0), d) for sh, d, _, _ in specs]
+    try:
+        for op, (_, _, u0, _) in zip(ops, specs):
+            op.set_state(u0)
+        steps = 3
+        _, infos = G.run_ensemble(ops, steps, [r for *_, r in specs], 33.5, 1e-8, metrics=False, infos=True,
+                                  groups=2)
+        branches = set()
+        for i, (op, (shape, d, u0, rho)) in enumerate(zip(ops, specs)):
+            op_o = port.stencil(shape, 2.0, d)
+            u = u0
+            for q in range(steps):
+                inf = infos[i][q]
+                branches.add(inf.branch)
+                u, log = port.step(op_o, u, rho, 33.5, 1e-8, bnorm=inf.bnorm, coln=inf.coln)
+                assert inf.stage_terms() == log.stage_terms(), (i, q)
+            assert np.array_equal(op.get_state(), u), i
+        assert {0, 2, 3} <= branches
+    finally:
+        for op in ops:
+            op.close()
