@@ -1270,7 +1270,7 @@ gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const
     for (int i = 0; i < n_members; ++i) {
         gs_ctx* c = ctxs[i];
         const gs_status st = ensure_operator(c);
-        if (st != GS_OK) return st;
+        if (st != GS_OK) return fail(c0, st, "run_ensemble: member " + std::to_string(i) + ": " + c->err);
         if (c->device != c0->device) return fail(c0, GS_EINVAL, "run_ensemble: members on different devices");
         batched = batched && c->tma_ok && c->palette_mode && !c->is_csr;
         thin += c->nz < 8;
@@ -1315,9 +1315,11 @@ gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const
             p.center[a] = cent(i) ? cent(i)[a] : 0.0;
         }
         fill_rtab(tol, p.rtab);
+        // errors are reported on ctxs[0] (the context the caller asks), naming the member
         gs_status st = setup_solve(c, p, grp, sb, n_steps, metrics, infos);
-        if (st != GS_OK) return st;
-        GS_CUDA(c, cudaStreamSynchronize(c->stream));  // the member's scratch is ready for c0's stream
+        if (st == GS_OK) st = c->stream && cudaStreamSynchronize(c->stream) != cudaSuccess ? GS_ECUDA : GS_OK;
+        if (st != GS_OK)
+            return fail(c0, st, "run_ensemble: member " + std::to_string(i) + ": " + (c->err.empty() ? "CUDA error" : c->err));
     }
     const int fuse = thin ? 4 : 2;
     GS_CUDA(c0, c0->ens_params.alloc(sizeof(gs::SolveParams) * static_cast<size_t>(n_members)));

@@ -202,6 +202,12 @@ def test_ensemble_argument_errors(port):
             G.run_ensemble([a, b], 1, [rho], 33.5, 1e-8)
         with pytest.raises(ValueError, match="no members"):
             G.run_ensemble([], 1, [], 33.5, 1e-8)
+        bare = G.StencilOperator(G.Grid(48, 32, 20, h=2.0))  # no operator set
+        try:
+            with pytest.raises(ValueError, match="member 1: operator not set"):
+                G.run_ensemble([a, bare], 1, [rho, rho], 33.5, 1e-8)
+        finally:
+            bare.close()
         assert np.array_equal(a.get_state(), u0) and np.array_equal(b.get_state(), u0)
 
 
