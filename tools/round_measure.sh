@@ -1,10 +1,12 @@
 # Round-end measurement batch (run on the GPU box from the repo root):
-#   bash tools/round_measure.sh
-# GPU tests, the C4 bench line (both arms), the ncu launch list of the same default bench command,
-# and one ncu --set full capture of the Taylor kernel (each ncu pass only after its command exited 0).
+#   bash tools/round_measure.sh          (then, here: bash tools/round_collect.sh rNN)
+# GPU tests, smoke(), the C4 bench line (both arms), the ncu launch list of the same default bench
+# command, one ncu --set full capture of the Taylor kernel (each ncu pass only after its command
+# exited 0), and the bench lines of the other configurations.
 set -u
 mkdir -p gpurun_out
 timeout 1800 python -m pytest tests -m gpu -q -x > gpurun_out/m_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/m_tests.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/m_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/m_smoke.log
 timeout 900 python bench.py > gpurun_out/m_bench.json 2> gpurun_out/m_bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference > gpurun_out/m_bench_ref.json 2> gpurun_out/m_bench_ref.err; echo "ref rc=$?"
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/m_launches.csv \
@@ -12,4 +14,5 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --
 timeout 900 python tools/prof_step.py --config C4 --steps 1 --repeat 2 > gpurun_out/m_prof_plain.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:taylor_kernel -s 1 -c 1 \
     -o gpurun_out/m_taylor python tools/prof_step.py --config C4 --steps 1 --repeat 2 > gpurun_out/m_ncu_full.log 2>&1; echo "full rc=$?"
+bash tools/configs_measure.sh C1 C2 C3 C5 C4x4
 tail -3 gpurun_out/m_tests.log
