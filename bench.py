@@ -530,12 +530,10 @@ def run_ensemble(args, w, rank, world, local):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if batched:
-            # every member's u H2D (gs_set_state), one batched step, every u' D2H (gs_get_state)
-            for op, pin_in in zip(runner.ops, pin_ins):
-                assert op.lib.gs_set_state(op.ctx, pin_in.numpy()) == 0
-            G.run_ensemble(runner.ops, 1, runner.rhos, w.tau, W.TOL, metrics=False)
-            for op, pin_out in zip(runner.ops, pin_outs):
-                assert op.lib.gs_get_state(op.ctx, pin_out.numpy()) == 0
+            # every member's u H2D, one batched step, every u' D2H: gs_step_ensemble_host, whose
+            # member chunks' copies overlap the other chunks' steps
+            G.step_ensemble_host(runner.ops, [t.numpy() for t in pin_ins], runner.rhos, w.tau, W.TOL,
+                                 outs=[t.numpy() for t in pin_outs])
         else:
             for op, pin_in, pin_out, rho in zip(runner.ops, pin_ins, pin_outs, runner.rhos):
                 rc = op.lib.gs_step_host(op.ctx, pin_in.numpy(), rho, w.tau, W.TOL, pin_out.numpy(), C.byref(info))
@@ -549,8 +547,8 @@ def run_ensemble(args, w, rank, world, local):
             dt = float(t.item())
         e2e = {"value": w.members / dt, "unit": "member-steps/s", "h2d_bytes_per_step": 8 * w.n * w.members,
                "d2h_bytes_per_step": 8 * w.n * w.members,
-               "api": ("gs_set_state per member (u H2D from pinned) + one gs_run_ensemble step + gs_get_state per "
-                       "member (u' D2H)" if batched else
+               "api": ("gs_step_ensemble_host: every member's u H2D from pinned, one batched step, u' D2H; 4 member "
+                       "chunks whose copies overlap the other chunks' steps" if batched else
                        "gs_step_host per member (drop-in step(): u H2D from pinned, u' D2H)")}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -137,6 +137,15 @@ gs_status gs_run(gs_ctx* ctx, int n_steps, double rho, double tau, double tol, c
 gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const double* rhos, double tau,
                           double tol, const double* origins, const double* centers, double front_threshold,
                           gs_metrics* metrics, gs_step_info* infos, int groups);
+/* One step of every member with host vectors (step() of integrator.cpp:52-63 per member, value
+ * semantics as gs_step_host): member i's u from u_in[i], u' into u_out[i] (each ctxs[i]'s point
+ * count).  The members run batched as in gs_run_ensemble, in `chunks` consecutive groups of
+ * members (<= 0: the default) whose host-to-device and device-to-host copies, on their own
+ * streams, overlap the other chunks' steps; with pinned host vectors the copies are
+ * asynchronous.  infos: n_members records or NULL.  The resident states are overwritten. */
+gs_status gs_step_ensemble_host(gs_ctx* const* ctxs, int n_members, const double* const* u_in, double* const* u_out,
+                                const double* rhos, double tau, double tol, gs_step_info* infos, int groups,
+                                int chunks);
 
 /* ---- host helpers with libm parity --------------------------------------------------- */
 /* seed_initial (integrator.cpp:32-50): u = amplitude*exp(-width*|x-c|^2), zero where the

@@ -51,6 +51,7 @@ EXPORTS = [
     "gs_set_intensity", "gs_set_labels", "gs_set_diffusion", "gs_get_labels", "gs_get_diffusion",
     "gs_one_norm", "gs_apply", "gs_set_state", "gs_get_state", "gs_state_device_ptr",
     "gs_select_params", "gs_expmv", "gs_phi1v", "gs_step", "gs_step_host", "gs_run", "gs_run_ensemble",
+    "gs_step_ensemble_host",
     "gs_seed_initial",
     "gs_set_trace", "gs_get_trace", "gs_set_kernel_timing", "gs_get_kernel_times",
     "gs_write_vtk", "gs_read_vtk", "gs_write_metrics_csv", "gs_snapshot_vtk", "gs_snapshot_flush",
@@ -103,6 +104,9 @@ def load(path: str | None = None):
     if hasattr(L, "gs_run_ensemble"):
         L.gs_run_ensemble.argtypes = [C.POINTER(vp), C.c_int, C.c_int, _dp, C.c_double, C.c_double, vp, vp,
                                       C.c_double, vp, vp, C.c_int]
+    if hasattr(L, "gs_step_ensemble_host"):
+        L.gs_step_ensemble_host.argtypes = [C.POINTER(vp), C.c_int, C.POINTER(vp), C.POINTER(vp), _dp, C.c_double,
+                                            C.c_double, vp, C.c_int, C.c_int]
     if hasattr(L, "gs_set_trace"):  # diagnostics
         L.gs_set_trace.argtypes = [vp, C.c_int]
         L.gs_get_trace.argtypes = [vp, np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS"), C.c_int,

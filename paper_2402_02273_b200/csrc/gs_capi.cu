@@ -65,6 +65,8 @@ constexpr int kDefaultFuse = 2;
 // gs_run_ensemble: CTA groups of the batched Taylor launch (members run concurrently, one per
 // group of num_sms / groups SMs); GS_ENS_GROUPS or the call's `groups` argument override it.
 constexpr int kEnsembleGroups = 16;
+// gs_step_ensemble_host: member chunks whose copies overlap the other chunks' steps.
+constexpr int kEnsembleChunks = 4;
 
 struct SnapSlot {
     DevBuf dev;                  // device copy of the state at the snapshot
@@ -114,6 +116,9 @@ struct gs_ctx {
     DevBuf part_b, part_c, part_u, slots, mslots, ctrl, metrics, infos, normbits;
     // gs_run_ensemble (this context as member 0): the members' SolveParams and the group control words
     DevBuf ens_params, ens_ctl;
+    // gs_step_ensemble_host: copy streams and chunk events
+    cudaStream_t ens_h2d = nullptr, ens_d2h = nullptr;
+    std::vector<cudaEvent_t> ens_events;
 
     gs::StencilOp op{};
     int grid_blocks = 0;
@@ -996,6 +1001,9 @@ void gs_destroy(gs_ctx* c) {
                       &c->normbits, &c->trace, &c->ens_params, &c->ens_ctl})
         b->release();
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ens_events) cudaEventDestroy(e);
+    if (c->ens_h2d) cudaStreamDestroy(c->ens_h2d);
+    if (c->ens_d2h) cudaStreamDestroy(c->ens_d2h);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -1252,9 +1260,20 @@ gs_status gs_run(gs_ctx* c, int n_steps, double rho, double tau, double tol, con
     return launch_solve(c, p, n_steps, reinterpret_cast<gs_metrics*>(metrics), infos);
 }
 
-gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const double* rhos, double tau, double tol,
-                          const double* origins, const double* centers, double front_threshold, gs_metrics* metrics,
-                          gs_step_info* infos, int groups) {
+namespace {
+
+// gs_run_ensemble / gs_step_ensemble_host: the members' SolveParams and launch geometry.
+struct EnsPlan {
+    std::vector<gs::SolveParams> P;
+    int groups = 1, grp = 1, sb = 1, fuse = 2;
+    bool batched = false;
+};
+
+// Validate the members and, when they can take the batched path, set up every member's
+// scratch and SolveParams (errors on ctxs[0], naming the member).
+gs_status ens_prepare(gs_ctx* const* ctxs, int n_members, int n_steps, const double* rhos, double tau, double tol,
+                      const double* origins, const double* centers, double front_threshold, gs_metrics* metrics,
+                      gs_step_info* infos, int groups, EnsPlan& plan) {
     if (!ctxs || n_members < 1 || !rhos) return fail(nullptr, GS_EINVAL, "run_ensemble: null argument or no members");
     for (int i = 0; i < n_members; ++i) {
         if (!ctxs[i]) return fail(nullptr, GS_EINVAL, "run_ensemble: null member context");
@@ -1275,34 +1294,23 @@ gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const
         batched = batched && c->tma_ok && c->palette_mode && !c->is_csr;
         thin += c->nz < 8;
     }
-    batched = batched && (thin == 0 || thin == n_members);  // one Taylor instantiation per launch
-    auto orig = [&](int i) { return origins ? origins + 3 * i : nullptr; };
-    auto cent = [&](int i) { return centers ? centers + 3 * i : nullptr; };
-    if (!batched) {
-        // members the batched path cannot take run one after another, each on the whole GPU
-        for (int i = 0; i < n_members; ++i) {
-            const gs_status st = gs_run(ctxs[i], n_steps, rhos[i], tau, tol, orig(i), cent(i), front_threshold,
-                                        metrics ? metrics + static_cast<size_t>(i) * (n_steps + 1) : nullptr,
-                                        infos ? infos + static_cast<size_t>(i) * n_steps : nullptr);
-            if (st != GS_OK) return st;
-        }
-        return GS_OK;
-    }
+    plan.batched = batched && (thin == 0 || thin == n_members);  // one Taylor instantiation per launch
+    if (!plan.batched) return GS_OK;
     cudaSetDevice(c0->device);
     // CTA groups of the Taylor launch: each runs one member at a time on num_sms / groups SMs
     if (groups <= 0) {
         groups = kEnsembleGroups;
         if (const char* e = std::getenv("GS_ENS_GROUPS")) groups = std::atoi(e);
     }
-    groups = std::max(1, std::min({groups, n_members, c0->num_sms}));
-    const int grp = c0->num_sms / groups;
-    int sb = 1;
-    for (int i = 0; i < n_members; ++i) sb = std::max(sb, stream_blocks(ctxs[i]));
-    std::vector<gs::SolveParams> P(static_cast<size_t>(n_members));
+    plan.groups = std::max(1, std::min({groups, n_members, c0->num_sms}));
+    plan.grp = c0->num_sms / plan.groups;
+    plan.sb = 1;
+    for (int i = 0; i < n_members; ++i) plan.sb = std::max(plan.sb, stream_blocks(ctxs[i]));
+    plan.fuse = thin ? 4 : 2;
+    plan.P.assign(static_cast<size_t>(n_members), gs::SolveParams{});
     for (int i = 0; i < n_members; ++i) {
         gs_ctx* c = ctxs[i];
-        gs::SolveParams& p = P[i];
-        p = gs::SolveParams{};
+        gs::SolveParams& p = plan.P[i];
         p.mode = gs::kModeRun;
         p.n_steps = n_steps;
         p.rho = rhos[i];
@@ -1311,45 +1319,89 @@ gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const
         p.h = c->h;
         p.front_threshold = front_threshold;
         for (int a = 0; a < 3; ++a) {
-            p.origin[a] = orig(i) ? orig(i)[a] : 0.0;
-            p.center[a] = cent(i) ? cent(i)[a] : 0.0;
+            p.origin[a] = origins ? origins[3 * i + a] : 0.0;
+            p.center[a] = centers ? centers[3 * i + a] : 0.0;
         }
         fill_rtab(tol, p.rtab);
-        // errors are reported on ctxs[0] (the context the caller asks), naming the member
-        gs_status st = setup_solve(c, p, grp, sb, n_steps, metrics, infos);
+        gs_status st = setup_solve(c, p, plan.grp, plan.sb, n_steps, metrics, infos);
         if (st == GS_OK) st = c->stream && cudaStreamSynchronize(c->stream) != cudaSuccess ? GS_ECUDA : GS_OK;
         if (st != GS_OK)
             return fail(c0, st, "run_ensemble: member " + std::to_string(i) + ": " + (c->err.empty() ? "CUDA error" : c->err));
     }
-    const int fuse = thin ? 4 : 2;
-    GS_CUDA(c0, c0->ens_params.alloc(sizeof(gs::SolveParams) * static_cast<size_t>(n_members)));
-    GS_CUDA(c0, c0->ens_ctl.alloc(sizeof(unsigned) * (gs::ens_ctl_words(groups) + n_members)));
-    GS_CUDA(c0, cudaMemcpyAsync(c0->ens_params.p, P.data(), sizeof(gs::SolveParams) * static_cast<size_t>(n_members),
-                                cudaMemcpyHostToDevice, c0->stream));
-    const gs::SolveParams* dP = c0->ens_params.as<gs::SolveParams>();
-    unsigned* ctl = c0->ens_ctl.as<unsigned>();
+    return GS_OK;
+}
+
+// n_steps batched steps of the n members whose SolveParams start at dP, on stream st; ctl
+// holds ens_ctl_words(groups) + n words.
+cudaError_t ens_launch(const EnsPlan& plan, const gs::SolveParams* dP, int n, int n_steps, bool metrics,
+                       unsigned* ctl, cudaStream_t st) {
+    const int groups = std::min(plan.groups, n), grp = plan.grp, sb = plan.sb;
     const unsigned* order = ctl + gs::ens_ctl_words(groups);
     const dim3 blk(gs::kSolveThreads);
-    cudaStream_t st = c0->stream;
+    cudaError_t e = cudaSuccess;
     if (metrics) {
-        gs::ens_metrics_kernel<<<n_members * sb, blk, 0, st>>>(dP, sb);
-        GS_CUDA(c0, cudaGetLastError());
+        gs::ens_metrics_kernel<<<n * sb, blk, 0, st>>>(dP, sb);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     for (int step = 0; step < n_steps; ++step) {
-        gs::ens_prep_kernel<<<n_members * grp, blk, gs::kRingBytes, st>>>(dP, grp, step);
-        GS_CUDA(c0, cudaGetLastError());
-        gs::ens_border_kernel<<<n_members * sb, blk, 0, st>>>(dP, sb, grp, step);
-        GS_CUDA(c0, cudaGetLastError());
-        gs::ens_order_kernel<<<1, 256, 0, st>>>(dP, n_members, ctl + gs::ens_ctl_words(groups));
-        GS_CUDA(c0, cudaGetLastError());
-        GS_CUDA(c0, cudaMemsetAsync(ctl, 0, sizeof(unsigned) * gs::ens_ctl_words(groups), st));
-        int nm = n_members, g = grp, bb = sb, sp = step;
-        void* args[] = {&dP, &nm, &g, &bb, &sp, &ctl, &order};
-        GS_CUDA(c0, cudaLaunchCooperativeKernel(gs::ens_taylor_kernel_fn(fuse), dim3(groups * grp), blk, args,
-                                                gs::kDynSmemBytes, st));
-        gs::ens_update_kernel<<<n_members * sb, blk, 0, st>>>(dP, sb, step);
-        GS_CUDA(c0, cudaGetLastError());
+        gs::ens_prep_kernel<<<n * grp, blk, gs::kRingBytes, st>>>(dP, grp, step);
+        gs::ens_border_kernel<<<n * sb, blk, 0, st>>>(dP, sb, grp, step);
+        gs::ens_order_kernel<<<1, 256, 0, st>>>(dP, n, ctl + gs::ens_ctl_words(groups));
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(ctl, 0, sizeof(unsigned) * gs::ens_ctl_words(groups), st)) != cudaSuccess) return e;
+        int nm = n, g = grp, bb = sb, sp = step;
+        void* args[] = {const_cast<gs::SolveParams**>(&dP), &nm, &g, &bb, &sp, &ctl, const_cast<unsigned**>(&order)};
+        if ((e = cudaLaunchCooperativeKernel(gs::ens_taylor_kernel_fn(plan.fuse), dim3(groups * grp), blk, args,
+                                             gs::kDynSmemBytes, st)) != cudaSuccess)
+            return e;
+        gs::ens_update_kernel<<<n * sb, blk, 0, st>>>(dP, sb, step);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
+    return e;
+}
+
+// Per-member status after a batched run: the first failure, reported on ctxs[0].
+gs_status ens_status(gs_ctx* const* ctxs, int n_members, const std::vector<gs::Ctrl>& ctrl) {
+    for (int i = 0; i < n_members; ++i) {
+        if (ctrl[i].status == GS_OK) continue;
+        const std::string who = "run_ensemble: member " + std::to_string(i) + ": ";
+        if (ctrl[i].detail == 2)
+            return fail(ctxs[0], GS_ENUMERIC, who + "expmv: series diverged to non-finite values; reduce t");
+        if (ctrl[i].status == GS_EINVAL)
+            return fail(ctxs[0], GS_EINVAL, who + "select_params: operator norm must be finite and nonnegative");
+        return fail(ctxs[0], GS_ENUMERIC, who + "select_params: scaled operator norm too large for any stage count");
+    }
+    return GS_OK;
+}
+
+}  // namespace
+
+gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const double* rhos, double tau, double tol,
+                          const double* origins, const double* centers, double front_threshold, gs_metrics* metrics,
+                          gs_step_info* infos, int groups) {
+    EnsPlan plan;
+    gs_status st0 = ens_prepare(ctxs, n_members, n_steps, rhos, tau, tol, origins, centers, front_threshold, metrics,
+                                infos, groups, plan);
+    if (st0 != GS_OK) return st0;
+    if (!plan.batched) {
+        // members the batched path cannot take run one after another, each on the whole GPU
+        for (int i = 0; i < n_members; ++i) {
+            const gs_status st = gs_run(ctxs[i], n_steps, rhos[i], tau, tol, origins ? origins + 3 * i : nullptr,
+                                        centers ? centers + 3 * i : nullptr, front_threshold,
+                                        metrics ? metrics + static_cast<size_t>(i) * (n_steps + 1) : nullptr,
+                                        infos ? infos + static_cast<size_t>(i) * n_steps : nullptr);
+            if (st != GS_OK) return st;
+        }
+        return GS_OK;
+    }
+    gs_ctx* const c0 = ctxs[0];
+    GS_CUDA(c0, c0->ens_params.alloc(sizeof(gs::SolveParams) * static_cast<size_t>(n_members)));
+    GS_CUDA(c0, c0->ens_ctl.alloc(sizeof(unsigned) * (gs::ens_ctl_words(plan.groups) + n_members)));
+    GS_CUDA(c0, cudaMemcpyAsync(c0->ens_params.p, plan.P.data(), sizeof(gs::SolveParams) * static_cast<size_t>(n_members),
+                                cudaMemcpyHostToDevice, c0->stream));
+    cudaStream_t st = c0->stream;
+    GS_CUDA(c0, ens_launch(plan, c0->ens_params.as<gs::SolveParams>(), n_members, n_steps, metrics != nullptr,
+                           c0->ens_ctl.as<unsigned>(), st));
     std::vector<gs::Ctrl> ctrl(static_cast<size_t>(n_members));
     for (int i = 0; i < n_members; ++i) {
         gs_ctx* c = ctxs[i];
@@ -1362,15 +1414,67 @@ gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const
                                         sizeof(gs_step_info) * n_steps, cudaMemcpyDeviceToHost, st));
     }
     GS_CUDA(c0, cudaStreamSynchronize(st));
-    for (int i = 0; i < n_members; ++i) {
-        if (ctrl[i].status == GS_OK) continue;
-        const std::string who = "run_ensemble: member " + std::to_string(i) + ": ";
-        if (ctrl[i].detail == 2) return fail(c0, GS_ENUMERIC, who + "expmv: series diverged to non-finite values; reduce t");
-        if (ctrl[i].status == GS_EINVAL)
-            return fail(c0, GS_EINVAL, who + "select_params: operator norm must be finite and nonnegative");
-        return fail(c0, GS_ENUMERIC, who + "select_params: scaled operator norm too large for any stage count");
+    return ens_status(ctxs, n_members, ctrl);
+}
+
+gs_status gs_step_ensemble_host(gs_ctx* const* ctxs, int n_members, const double* const* u_in, double* const* u_out,
+                                const double* rhos, double tau, double tol, gs_step_info* infos, int groups,
+                                int chunks) {
+    if (!u_in || !u_out) return fail(ctxs ? ctxs[0] : nullptr, GS_EINVAL, "step_ensemble: null argument");
+    for (int i = 0; ctxs && i < n_members; ++i)
+        if (!u_in[i] || !u_out[i]) return fail(ctxs[0], GS_EINVAL, "step_ensemble: null member vector");
+    EnsPlan plan;
+    gs_status st0 = ens_prepare(ctxs, n_members, 1, rhos, tau, tol, nullptr, nullptr, 0.1, nullptr, infos, groups, plan);
+    if (st0 != GS_OK) return st0;
+    if (!plan.batched) {
+        for (int i = 0; i < n_members; ++i) {
+            const gs_status st = gs_step_host(ctxs[i], u_in[i], rhos[i], tau, tol, u_out[i], infos ? infos + i : nullptr);
+            if (st != GS_OK) return st;
+        }
+        return GS_OK;
     }
-    return GS_OK;
+    gs_ctx* const c0 = ctxs[0];
+    if (chunks <= 0) chunks = kEnsembleChunks;
+    chunks = std::max(1, std::min(chunks, n_members));
+    // H2D, compute and D2H on three streams: chunk k's copies overlap chunk k-1's and k+1's
+    // steps (pinned host vectors make the copies asynchronous)
+    if (!c0->ens_h2d) GS_CUDA(c0, cudaStreamCreateWithFlags(&c0->ens_h2d, cudaStreamNonBlocking));
+    if (!c0->ens_d2h) GS_CUDA(c0, cudaStreamCreateWithFlags(&c0->ens_d2h, cudaStreamNonBlocking));
+    while (static_cast<int>(c0->ens_events.size()) < 2 * chunks) {
+        cudaEvent_t e;
+        GS_CUDA(c0, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c0->ens_events.push_back(e);
+    }
+    GS_CUDA(c0, c0->ens_params.alloc(sizeof(gs::SolveParams) * static_cast<size_t>(n_members)));
+    GS_CUDA(c0, c0->ens_ctl.alloc(sizeof(unsigned) * (gs::ens_ctl_words(plan.groups) + n_members)));
+    GS_CUDA(c0, cudaMemcpyAsync(c0->ens_params.p, plan.P.data(), sizeof(gs::SolveParams) * static_cast<size_t>(n_members),
+                                cudaMemcpyHostToDevice, c0->stream));
+    const gs::SolveParams* dP = c0->ens_params.as<gs::SolveParams>();
+    const size_t bytes = sizeof(double);
+    for (int k = 0; k < chunks; ++k) {
+        const int lo = k * n_members / chunks, hi = (k + 1) * n_members / chunks;
+        for (int i = lo; i < hi; ++i)
+            GS_CUDA(c0, cudaMemcpyAsync(ctxs[i]->u.p, u_in[i], bytes * static_cast<size_t>(ctxs[i]->n),
+                                        cudaMemcpyHostToDevice, c0->ens_h2d));
+        GS_CUDA(c0, cudaEventRecord(c0->ens_events[2 * k], c0->ens_h2d));
+        GS_CUDA(c0, cudaStreamWaitEvent(c0->stream, c0->ens_events[2 * k], 0));
+        GS_CUDA(c0, ens_launch(plan, dP + lo, hi - lo, 1, false, c0->ens_ctl.as<unsigned>(), c0->stream));
+        GS_CUDA(c0, cudaEventRecord(c0->ens_events[2 * k + 1], c0->stream));
+        GS_CUDA(c0, cudaStreamWaitEvent(c0->ens_d2h, c0->ens_events[2 * k + 1], 0));
+        for (int i = lo; i < hi; ++i)
+            GS_CUDA(c0, cudaMemcpyAsync(u_out[i], ctxs[i]->u.p, bytes * static_cast<size_t>(ctxs[i]->n),
+                                        cudaMemcpyDeviceToHost, c0->ens_d2h));
+    }
+    std::vector<gs::Ctrl> ctrl(static_cast<size_t>(n_members));
+    for (int i = 0; i < n_members; ++i) {
+        GS_CUDA(c0, cudaMemcpyAsync(&ctrl[i], ctxs[i]->ctrl.p, sizeof(gs::Ctrl), cudaMemcpyDeviceToHost, c0->ens_d2h));
+        if (infos)
+            GS_CUDA(c0, cudaMemcpyAsync(infos + i, ctxs[i]->infos.p, sizeof(gs_step_info), cudaMemcpyDeviceToHost,
+                                        c0->ens_d2h));
+    }
+    GS_CUDA(c0, cudaStreamSynchronize(c0->ens_d2h));
+    GS_CUDA(c0, cudaStreamSynchronize(c0->stream));
+    return ens_status(ctxs, n_members, ctrl);
 }
 
 gs_status gs_step(gs_ctx* c, double rho, double tau, double tol, gs_step_info* info) {

@@ -479,6 +479,36 @@ def run_ensemble(ops, n_steps: int, rhos, tau: float, tol: float, origins=None, 
     return per_m, per_i
 
 
+def step_ensemble_host(ops, us, rhos, tau: float, tol: float, outs=None, infos: bool = False, groups: int = 0,
+                       chunks: int = 0):
+    """gs_step_ensemble_host: one exponential-Euler step of every member with host vectors
+    (step() per member, integrator.cpp:52-63), batched, the copies overlapping the other member
+    chunks' steps.  `us` / `outs`: one float64 vector per member (pinned memory makes the
+    copies asynchronous).  Returns (outs, infos or None)."""
+    ops = list(ops)
+    n = len(ops)
+    if n == 0:
+        raise ValueError("run_ensemble: no members")
+    lib = ops[0].lib
+    rhos = np.ascontiguousarray(rhos, dtype=np.float64)
+    if rhos.size != n or len(us) != n:
+        raise ValueError("run_ensemble: one rho and one state per member")
+    ins = [np.ascontiguousarray(u, dtype=np.float64) for u in us]
+    for op, u in zip(ops, ins):
+        if u.size != op.grid.num_points():
+            raise ValueError("step: state length does not match the grid")
+    outs = [np.empty_like(u) for u in ins] if outs is None else list(outs)
+    pin = (C.c_void_p * n)(*[u.ctypes.data for u in ins])
+    pout = (C.c_void_p * n)(*[o.ctypes.data for o in outs])
+    ctxs = (C.c_void_p * n)(*[o.ctx for o in ops])
+    inf = (N.GsStepInfo * n)() if infos else None
+    rc = lib.gs_step_ensemble_host(ctxs, n, pin, pout, rhos, tau, tol,
+                                   C.cast(inf, C.c_void_p) if inf is not None else None, groups, chunks)
+    if rc != N.GS_OK:
+        _raise(rc, lib.gs_last_error(ops[0].ctx).decode("utf-8", "surrogateescape"))
+    return outs, (list(inf) if inf is not None else None)
+
+
 def run(cfg: SimConfig, a: StencilOperator, u0, snapshot=None, on_range=None, on_step=None,
         with_infos: bool = False, _vtk=None) -> RunResult:
     """integrator.cpp:91-138: the time loop runs on the GPU as one launch per segment

@@ -252,3 +252,36 @@ def test_batched_ensemble_heterogeneous_members(port):
     finally:
         for op in ops:
             op.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunks", [1, 2, 3])
+def test_step_ensemble_host_bitwise_vs_oracle(port, chunks):
+    """gs_step_ensemble_host: value semantics per member (u in, u' out, as the drop-in step()),
+    batched in `chunks` member chunks whose copies overlap the other chunks' steps -- every
+    member bitwise against the oracle given its device sums, from pinned and pageable vectors."""
+    import torch
+    from paper_2402_02273_b200 import gliosim as G
+    shape = (48, 32, 20)
+    members = _random_members(port, shape, 5, 40 + chunks)
+    ops = [G.assemble_diffusion(G.Grid(*shape, h=2.0), d) for d, _, _ in members]
+    try:
+        ins = []
+        for i, (_, u0, _) in enumerate(members):
+            if i % 2 == 0:  # pinned host memory (asynchronous copies)
+                t = torch.empty(u0.size, dtype=torch.float64, pin_memory=True)
+                t.numpy()[:] = u0
+                ins.append(t.numpy())
+            else:
+                ins.append(u0.copy())
+        outs, infos = G.step_ensemble_host(ops, ins, [r for *_, r in members], 33.5, 1e-8, infos=True, groups=2,
+                                           chunks=chunks)
+        for i, (op, (d, u0, rho)) in enumerate(zip(ops, members)):
+            want, log = port.step(port.stencil(shape, 2.0, d), u0, rho, 33.5, 1e-8, bnorm=infos[i].bnorm,
+                                  coln=infos[i].coln)
+            assert infos[i].stage_terms() == log.stage_terms(), i
+            assert np.array_equal(outs[i], want), i
+            assert np.array_equal(ins[i], u0), i  # inputs untouched
+    finally:
+        for op in ops:
+            op.close()
