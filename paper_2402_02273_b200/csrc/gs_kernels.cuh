@@ -21,16 +21,26 @@ enum Buf : int { kBufU = 0, kBufG = 1, kBufF0 = 2, kBufF1 = 3, kBufT0 = 4, kBufT
 
 // TMA z-slab pipeline geometry: a CTA owns tiles of kTmaTX x kTmaTY columns and
 // streams their z-planes through a kTmaStages-deep shared-memory ring.
+//
+// Default: 32 x 32 tiles, 512 threads (16 warps), each thread one column and two rows.  The
+// two-term sweep's T1 halo ring is then 128 points -- exactly warps 0-3, one ring warp per
+// SM sub-partition (measured against 64 x 16 tiles, whose 160-point ring needs five warps:
+// +1.8% at C4, +0.7% at C3).  A/B builds: -DGS_TILE64 (64 x 16), -DGS_TILE8 (64 x 8 tiles,
+// 256 threads, two CTAs per SM).
+#if defined(GS_TILE8)
 constexpr int kTmaTX = 64;
-#ifdef GS_TILE8
-// A/B variant: 64 x 8 tiles, 256 threads, two CTAs per SM (each CTA's per-plane barrier then
-// overlaps the other CTA's work).
 constexpr int kTmaTY = 8;
 constexpr int kSolveThreads = 256;
 constexpr int kMinBlocks = 2;        // __launch_bounds__ of the TMA kernels: 2 CTAs/SM, 128 regs
-#else
+#elif defined(GS_TILE64)
+constexpr int kTmaTX = 64;
 constexpr int kTmaTY = 16;
 constexpr int kSolveThreads = 512;   // 16 warps: warp w owns tile row w, two columns per lane
+constexpr int kMinBlocks = 1;
+#else
+constexpr int kTmaTX = 32;
+constexpr int kTmaTY = 32;
+constexpr int kSolveThreads = 512;   // 16 warps: warp w owns rows w and w + 16 (single-term sweep)
 constexpr int kMinBlocks = 1;
 #endif
 constexpr int kTmaStages = 6;

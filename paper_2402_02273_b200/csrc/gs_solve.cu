@@ -290,10 +290,18 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
             for (int k = 0; k < pre; ++k) issue(z0 - 1 + k);
         }
 
-        // this thread's two columns of the tile
-        const int j = y0 + row;
-        int ii[2] = {x0 + lane, x0 + lane + 32};
-        const bool hy0 = j > 0, hy1 = j < op.ny - 1;
+        // this thread's two points of the tile: two columns of row `row` (64-wide tiles), or
+        // rows `row` and `row + 16` of one column (32-wide tiles)
+        static_assert(kTmaTX * kTmaTY == 2 * kSolveThreads, "two points per thread");
+        constexpr bool kCols = kTmaTX == 64;
+        int lxs[2], rws[2], ii[2], jj[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            lxs[c] = kCols ? lane + 32 * c : lane;
+            rws[c] = kCols ? row : row + (kSolveThreads / 32) * c;
+            ii[c] = x0 + lxs[c];
+            jj[c] = y0 + rws[c];
+        }
         double xm[2], xc[2];
         wait_plane(z0 - 1);
         wait_plane(z0);
@@ -302,9 +310,8 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
             const double* Xc = ring.x(slot_of(z0));
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const int lx = lane + 32 * c;
-                xm[c] = Xm[(row + 1) * kXPitch + lx + kXHalo];
-                xc[c] = Xc[(row + 1) * kXPitch + lx + kXHalo];
+                xm[c] = Xm[(rws[c] + 1) * kXPitch + lxs[c] + kXHalo];
+                xc[c] = Xc[(rws[c] + 1) * kXPitch + lxs[c] + kXHalo];
             }
         }
         for (int z = z0; z < z1; ++z) {
@@ -318,15 +325,16 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
             const bool hz0 = z > 0, hz1 = z < op.nz - 1;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const int lx = lane + 32 * c;
-                const int i = ii[c];
-                const double xp = Xp[(row + 1) * kXPitch + lx + kXHalo];
+                const int lx = lxs[c], rw = rws[c];
+                const int i = ii[c], j = jj[c];
+                const bool hy0 = j > 0, hy1 = j < op.ny - 1;
+                const double xp = Xp[(rw + 1) * kXPitch + lx + kXHalo];
                 if (i < op.nx && j < op.ny) {
-                    const double xym = Xc[row * kXPitch + lx + kXHalo];
-                    const double xyp = Xc[(row + 2) * kXPitch + lx + kXHalo];
-                    const double xxm = Xc[(row + 1) * kXPitch + lx + kXHalo - 1];
-                    const double xxp = Xc[(row + 1) * kXPitch + lx + kXHalo + 1];
-                    const int o = row * kTmaTX + lx;
+                    const double xym = Xc[rw * kXPitch + lx + kXHalo];
+                    const double xyp = Xc[(rw + 2) * kXPitch + lx + kXHalo];
+                    const double xxm = Xc[(rw + 1) * kXPitch + lx + kXHalo - 1];
+                    const double xxp = Xc[(rw + 1) * kXPitch + lx + kXHalo + 1];
+                    const int o = rw * kTmaTX + lx;
                     RowCoef rc;
                     rc.w = s_wtab[Lo[o]];
                     rc.live = rc.w != 0.0;
@@ -399,10 +407,11 @@ template <int KIND, bool kSkipOut = false, bool kExact = false, class R = Ring2>
 __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, int xbuf, int fbuf, int bbuf,
                                            double c1, double c2, double* outT, double* outF, double (&mx)[5],
                                            uint32_t& seq, uint32_t& phase_mask, const double* s_wtab) {
-    // Register-blocked layout: thread t owns column xl = t % 64 and rows ry0 = 2*(t/64), ry0+1 of
-    // the 64 x 16 tile for the whole z-march, so its z-1/z/z+1 values of X and T1 and its own
+    // Register-blocked layout: thread t owns column xl = t % kTmaTX and rows ry0 = 2*(t/kTmaTX),
+    // ry0+1 of the tile for the whole z-march, so its z-1/z/z+1 values of X and T1 and its own
     // y-neighbour live in registers; x-neighbours and the outer y-neighbours come from shared
-    // memory.  The 160 halo-ring points of T1 (no corners) are computed by threads 0..159 from shared memory.
+    // memory.  The halo-ring points of T1 (no corners; 128 with 32 x 32 tiles) are computed by
+    // the first kRing threads from shared memory.
     // All per-thread shared-memory offsets are fixed per tile; ring slots rotate by increment and
     // barrier parities are tracked in a bit mask (identical in every thread).
     constexpr bool needX = KIND != k2FirstZero;
@@ -414,8 +423,9 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
     constexpr uint32_t kXTx = k2XRows * kXPitch * 8;
     constexpr uint32_t kBTx = k2BRows * kXPitch * 8;
     constexpr uint32_t kLTx = (kTmaTY + 2) * kLPitch;
-    // T1 halo ring: rows -1 and 16 over columns 0..63, columns -1 and 64 over rows 0..15 --
-    // phase B's 5-point in-plane stencil never reads the four corners.  160 points: warps 0-4.
+    // T1 halo ring: rows -1 and kTmaTY over the tile's columns, columns -1 and kTmaTX over its
+    // rows -- phase B's 5-point in-plane stencil never reads the four corners.  128 points with
+    // 32 x 32 tiles: warps 0-3, one per SM sub-partition (160 with 64 x 16: warps 0-4).
     constexpr int kRing = 2 * kTmaTX + 2 * kTmaTY;
     // The thread that issues the TMA loads: lane 0 of warp 9 (a warp without ring points, on
     // a scheduler with one ring warp), not thread 0 of ring warp 0: +0.7% at C4 (measured
@@ -437,7 +447,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
     const int oL = (ry0 + 1) * kLPitch + xl + kLHaloX;  // own row 0 in the label tile
     const int oB = oX - kXPitch;                        // own row 0 in the b/gamma tile
     const int oF = ry0 * kTmaTX + xl;                   // own row 0 in the F tile
-    // this thread's ring point (rows -1 and 16, then columns -1 and 64); ring coordinates
+    // this thread's ring point (rows -1 and kTmaTY, then columns -1 and kTmaTX); ring coordinates
     // (rr, rc) count from row -1 / column -1
     const bool ringer = tid < kRing;
     int rr = 0, rc = 0;
@@ -582,7 +592,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
             xo[0] = Xs[oX] = __dadd_rn(Xs[oX], Ts[oX]);
             xo[1] = Xs[oX + kXPitch] = __dadd_rn(Xs[oX + kXPitch], Ts[oX + kXPitch]);
             if (ringer) Xs[rX] = __dadd_rn(Xs[rX], Ts[rX]);
-            // outer halo (172 points with 16-row tiles): X-tile rows 0 and k2XRows-1, then columns
+            // outer halo: X-tile rows 0 and k2XRows-1, then columns
             // 0 and kXPitch-1 of the rows between; then the four ring corners (row -1 / 16 x
             // column -1 / 64: not T1 ring points, but x-neighbours of the ring's end points);
             // threads from kRing on, wrapping if too few
