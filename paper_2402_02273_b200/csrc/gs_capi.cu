@@ -114,6 +114,8 @@ struct gs_ctx {
     DevBuf u, g, f0, f1, t0, t1, out;
     // scratch
     DevBuf part_b, part_c, part_u, slots, mslots, ctrl, metrics, infos, normbits;
+    // exact sequential sums (gs_seqsum.cuh): tile sums/prefixes, per-CTA item lists, counts
+    DevBuf seq_tsum, seq_items, seq_counts;
     // gs_run_ensemble (this context as member 0): the members' SolveParams and the group control words
     DevBuf ens_params, ens_ctl;
     // gs_step_ensemble_host: copy streams and chunk events
@@ -468,6 +470,15 @@ gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps
     p.slots = c->slots.as<unsigned long long>();
     p.mslots = c->mslots.as<unsigned long long>();
     p.ctrl = c->ctrl.as<gs::Ctrl>();
+    // the reference's sequential ||b||_1 and bordered column sum (GS_TREE_SUMS=1: tree sums, A/B)
+    p.seq_exact = std::getenv("GS_TREE_SUMS") == nullptr ? 1 : 0;
+    p.seq_tiles = static_cast<int>((c->n + gs::kSeqTileElems - 1) / gs::kSeqTileElems);
+    GS_CUDA(c, c->seq_tsum.alloc(sizeof(double) * std::max(1, p.seq_tiles)));
+    GS_CUDA(c, c->seq_items.alloc(static_cast<size_t>(gs::kSeqItemBytes) * gs::kSeqItemsPerCta * sb));
+    GS_CUDA(c, c->seq_counts.alloc(sizeof(int) * 2 * sb));
+    p.seq_tsum = c->seq_tsum.as<double>();
+    p.seq_items = c->seq_items.p;
+    p.seq_counts = c->seq_counts.as<int>();
     DevBuf* bufs[gs::kNumBufs] = {&c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out};
     for (int b = 0; b < gs::kNumBufs; ++b) p.buf[b] = bufs[b]->as<double>();
     p.trace = nullptr;
@@ -494,6 +505,14 @@ int solve_blocks(const gs_ctx* c) {
         gb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(gb, q)));
     }
     return gb;
+}
+
+// The exact sequential sum `which` (0: ||b||_1 before the border pass, 1: the bordered column
+// sum after it) on the context's stream; expmv has neither.
+void launch_seqsum(gs_ctx* c, const gs::SolveParams& p, int sb, int which) {
+    if (!p.seq_exact || p.mode == gs::kModeExpmv) return;
+    gs::seqsum_tiles_kernel<<<sb, gs::kSolveThreads, 0, c->stream>>>(p, which);
+    gs::seqsum_items_kernel<<<sb, gs::kSolveThreads, 0, c->stream>>>(p, which);
 }
 
 gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* metrics, gs_step_info* infos) {
@@ -531,6 +550,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
         cp.op = c->op;
         cp.n_steps = n_steps;
         cp.want_metrics = metrics ? 1 : 0;
+        cp.seq_exact = p.seq_exact;
         cp.slice = c->cl_slice;
         cp.halo = c->cl_halo;
         cp.rho = p.rho;
@@ -587,7 +607,9 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
             if (ok) {
                 gs::prep_kernel<<<gb, blk, dyn_prep, c->stream>>>(p, -1);
+                launch_seqsum(c, p, sb, 0);
                 gs::border_kernel<<<sb, blk, 0, c->stream>>>(p, gb, -1);
+                launch_seqsum(c, p, sb, 1);
                 cudaLaunchCooperativeKernel(gs::taylor_kernel_fn(p.fuse), dim3(gb), blk, args, dyn, c->stream);
                 gs::update_kernel<<<sb, blk, 0, c->stream>>>(p, -1);
                 gs::advance_kernel<<<1, 1, 0, c->stream>>>(p.ctrl);
@@ -611,8 +633,10 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             gs::prep_kernel<<<gb, blk, dyn_prep, c->stream>>>(p, step);
             GS_CUDA(c, cudaGetLastError());
             GS_CUDA(c, ev_end());
-            GS_CUDA(c, ev(1));
+            GS_CUDA(c, ev(1));  // border and the two exact sums
+            launch_seqsum(c, p, sb, 0);
             gs::border_kernel<<<sb, blk, 0, c->stream>>>(p, gb, step);
+            launch_seqsum(c, p, sb, 1);
             GS_CUDA(c, cudaGetLastError());
             GS_CUDA(c, ev_end());
             int border_blocks = sb;
@@ -873,7 +897,10 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
         // Measured (tools/cluster_ab.py): C1 (32 K voxels) +39%, C2 (64 K voxels) -5% against the
         // multi-kernel path, whose grid barriers stop dominating as the grid grows.
-        if (c->n <= kClusterMaxVoxels && slice >= halo && smem + 4096 <= static_cast<size_t>(optin) &&
+        cudaFuncAttributes fa{};
+        const size_t stat = cudaFuncGetAttributes(&fa, gs::cluster_run_kernel) == cudaSuccess ? fa.sharedSizeBytes : 65536;
+        if (c->n <= kClusterMaxVoxels && slice >= halo && slice <= 8 * gs::kSolveThreads &&
+            smem + stat + 1024 <= static_cast<size_t>(optin) &&
             cudaFuncSetAttribute(gs::cluster_run_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                 cudaSuccess &&
             raise_cluster_smem(smem)) {
@@ -1269,6 +1296,7 @@ struct EnsPlan {
     std::vector<gs::SolveParams> P;
     int groups = 1, grp = 1, sb = 1, fuse = 2;
     bool batched = false;
+    bool seq_exact = true;  // the members' SolveParams::seq_exact (one environment, one value)
 };
 
 // Validate the members and, when they can take the batched path, set up every member's
@@ -1309,6 +1337,7 @@ gs_status ens_prepare(gs_ctx* const* ctxs, int n_members, int n_steps, const dou
     plan.sb = 1;
     for (int i = 0; i < n_members; ++i) plan.sb = std::max(plan.sb, stream_blocks(ctxs[i]));
     plan.fuse = thin ? 4 : 2;
+    plan.seq_exact = std::getenv("GS_TREE_SUMS") == nullptr;
     plan.P.assign(static_cast<size_t>(n_members), gs::SolveParams{});
     for (int i = 0; i < n_members; ++i) {
         gs_ctx* c = ctxs[i];
@@ -1347,7 +1376,15 @@ cudaError_t ens_launch(const EnsPlan& plan, const gs::SolveParams* dP, int n, in
     }
     for (int step = 0; step < n_steps; ++step) {
         gs::ens_prep_kernel<<<n * grp, blk, gs::kRingBytes, st>>>(dP, grp, step);
+        if (plan.seq_exact) {
+            gs::ens_seqsum_tiles_kernel<<<n * sb, blk, 0, st>>>(dP, sb, 0);
+            gs::ens_seqsum_items_kernel<<<n * sb, blk, 0, st>>>(dP, sb, 0);
+        }
         gs::ens_border_kernel<<<n * sb, blk, 0, st>>>(dP, sb, grp, step);
+        if (plan.seq_exact) {
+            gs::ens_seqsum_tiles_kernel<<<n * sb, blk, 0, st>>>(dP, sb, 1);
+            gs::ens_seqsum_items_kernel<<<n * sb, blk, 0, st>>>(dP, sb, 1);
+        }
         gs::ens_order_kernel<<<1, 256, 0, st>>>(dP, n, ctl + gs::ens_ctl_words(groups));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(ctl, 0, sizeof(unsigned) * gs::ens_ctl_words(groups), st)) != cudaSuccess) return e;

@@ -24,6 +24,8 @@ namespace gs {
 
 namespace {
 
+#include "gs_seqsum.cuh"
+
 constexpr int kCT = kSolveThreads;  // threads per CTA
 
 struct ClusterShared {
@@ -106,11 +108,96 @@ __device__ __forceinline__ void block_to_mbox(ClusterShared& cs, int par, double
     }
 }
 
+// The reference's sequential sum of |B| over the cluster's slices in rank order (= index
+// order), exactly (gs_seqsum.cuh): each CTA builds the run / raw items of its slice from an
+// approximate prefix (the ranks' tree partials in mbox[par][0], after a cluster barrier);
+// after a second barrier every CTA gathers all ranks' lists over DSMEM and walks them the same
+// way, so all CTAs hold the same value.  A list longer than kClItemCap is walked element by
+// element over DSMEM, followed by one more barrier (uniform: every CTA sees the same counts)
+// before anyone overwrites B.
+constexpr int kClItemCap = 32;
+constexpr int kClEPT = 8;  // elements per thread: slices of up to kCT * 8 voxels
+struct ClusterSeq {
+    SeqSmem sm;
+    seq::Item own[kClItemCap];
+    seq::Item all[kClusterCTAs * kClItemCap];
+    int count, cnt[kClusterCTAs];
+    unsigned flags;
+    double result, prefix;
+};
+
+__device__ double cl_exact_sum(cg::cluster_group& cl, ClusterShared& cs, ClusterSeq& q, int par, const double* B,
+                               int64_t len, int64_t lo, int64_t S, int64_t N, int rank, int nranks) {
+    const int tid = threadIdx.x;
+    // approximate sum before this slice; this slice's non-finite flags
+    if (tid < 32) {
+        double v = tid < rank ? *cl.map_shared_rank(&cs.mbox[par][0], tid) : 0.0;
+        v = warp_sum(v);
+        if (tid == 0) {
+            q.prefix = v;
+            q.flags = 0u;
+            seq_open_reset(q.sm);
+        }
+    }
+    __syncthreads();
+    unsigned f = 0;
+    for (int64_t i = tid; i < len; i += kCT) {
+        const double x = B[i];
+        f |= isnan(x) ? seq::kHasNaN : (isinf(x) ? seq::kHasInf : 0u);
+    }
+    f = __reduce_or_sync(0xffffffffu, f);
+    if ((tid & 31) == 0 && f) atomicOr(&q.flags, f);
+    seq_tile_items<kClEPT>(q.sm, [&](int e) { return B[e]; }, lo, static_cast<int>(len), q.prefix, q.own, kClItemCap);
+    if (tid == 0) q.count = len > 0 ? seq_close(q.sm, lo + len, q.own, kClItemCap) : 0;
+    cl.sync();
+    // gather every rank's list (thread r * kClItemCap + k loads item k of rank r)
+    {
+        const int r = tid / kClItemCap, k = tid % kClItemCap;
+        if (r < nranks) {
+            const int cnt = *cl.map_shared_rank(&q.count, r);
+            if (k == 0) {
+                q.cnt[r] = cnt;
+                const unsigned rf = *cl.map_shared_rank(&q.flags, r);
+                if (rf && r != rank) atomicOr(&q.flags, rf);
+            }
+            if (k < cnt && cnt <= kClItemCap) q.all[r * kClItemCap + k] = cl.map_shared_rank(q.own, r)[k];
+        }
+    }
+    __syncthreads();
+    bool overflow = false;
+    for (int r = 0; r < nranks; ++r) overflow = overflow || q.cnt[r] > kClItemCap;
+    if (tid == 0) {
+        double acc = 0.0;
+        if (q.flags & seq::kHasNaN) {
+            acc = __longlong_as_double(0x7ff8000000000000ll);
+        } else if (q.flags & seq::kHasInf) {
+            acc = __longlong_as_double(0x7ff0000000000000ll);
+        } else {
+            for (int r = 0; r < nranks && !isinf(acc); ++r) {
+                const double* RB = cl.map_shared_rank(B, r);
+                const int64_t rlo = r * S;
+                auto walk = [&](double a, int64_t l, int64_t h) {
+                    for (int64_t i = l; i < h; ++i) a = __dadd_rn(a, fabs(RB[i - rlo]));
+                    return a;
+                };
+                if (q.cnt[r] > kClItemCap) acc = walk(acc, rlo, min(N, rlo + S));
+                else
+                    for (int k = 0; k < q.cnt[r]; ++k) seq_apply_item(acc, q.all[r * kClItemCap + k], walk);
+            }
+        }
+        q.result = acc;
+    }
+    if (overflow) cl.sync();  // remote B was read: nobody may overwrite it before everyone is done
+    __syncthreads();
+    return q.result;
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kCT, 1) cluster_run_kernel(const __grid_constant__ ClusterParams p) {
     cg::cluster_group cl = cg::this_cluster();
     __shared__ ClusterShared cs;
+    __shared__ ClusterSeq csq;
     extern __shared__ __align__(128) unsigned char dyn[];
     const StencilOp& op = p.op;
     const int rank = static_cast<int>(cl.block_rank());
@@ -223,8 +310,13 @@ __global__ void __launch_bounds__(kCT, 1) cluster_run_kernel(const __grid_consta
         block_to_mbox<1>(cs, par, part, ks);
         cl.sync();
         const int ksum[1] = {0};
-        cl_combine<1>(cl, cs, par, ksum);
-        const double bnorm = cs.bcast[0];
+        double bnorm;  // expact.cpp:110: the reference's sequential sum (or a rank-order tree sum, A/B)
+        if (p.seq_exact) {
+            bnorm = cl_exact_sum(cl, cs, csq, par, B, len, lo, S, N, rank, nranks);
+        } else {
+            cl_combine<1>(cl, cs, par, ksum);
+            bnorm = cs.bcast[0];
+        }
         par ^= 1;
         int branch = 0;
         if (t == 0.0) branch = 1;                                  // expact.cpp:108
@@ -261,8 +353,13 @@ __global__ void __launch_bounds__(kCT, 1) cluster_run_kernel(const __grid_consta
             }
             block_to_mbox<1>(cs, par, cs1, ks);
             cl.sync();
-            cl_combine<1>(cl, cs, par, ksum);
-            const double coln = cs.bcast[0];
+            double coln;  // sparse.cpp:36-38 on the bordered operator: sequential, or tree (A/B)
+            if (p.seq_exact) {
+                coln = cl_exact_sum(cl, cs, csq, par, B, len, lo, S, N, rank, nranks);
+            } else {
+                cl_combine<1>(cl, cs, par, ksum);
+                coln = cs.bcast[0];
+            }
             par ^= 1;
             const double norm_tA = __dmul_rn(fabs(t), nan_dropping_max(p.anorm, coln));
             int s_st = 1, m_deg = 1;
@@ -278,6 +375,7 @@ __global__ void __launch_bounds__(kCT, 1) cluster_run_kernel(const __grid_consta
                     ctrl->status = sel;
                     ctrl->detail = 1;
                 }
+                cl.sync();  // uniform branch: no CTA exits while another still reads its mailbox
                 return;
             }
             // ---- Taylor stages of single-term passes (expact.cpp:63-99) on [A b/gamma; 0 0]
@@ -331,6 +429,7 @@ __global__ void __launch_bounds__(kCT, 1) cluster_run_kernel(const __grid_consta
                             ctrl->status = GS_ENUMERIC;
                             ctrl->detail = 2;
                         }
+                        cl.sync();  // uniform branch: no CTA exits while another still reads its mailbox
                         return;
                     }
                     if (__dadd_rn(prev, cur) <= __dmul_rn(p.tol, fnorm)) {  // expact.cpp:93

@@ -150,6 +150,9 @@ struct Ctrl {
     unsigned int ticket;  // last-block-done counter (metrics)
     int ntrace;
     int step;             // current step of a graph-replayed run (kernels launched with step < 0)
+    // exact sequential sums (gs_seqsum.cuh): [0] ||b||_1, [1] the bordered column sum
+    double seq[2];
+    unsigned seq_ticket[2], seq_ticket2[2], seq_flags[2];
     int last_terms;       // Taylor terms of the last step (ensemble: longest members first)
 };
 
@@ -185,6 +188,13 @@ struct SolveParams {
     double* part_b;         // [grid] block partial sums of |b|
     double* part_c;         // [grid] block partial sums of |b/gamma|
     double* part_u;         // [grid] block partial sums of u (metrics)
+    // exact sequential sums (gs_seqsum.cuh): per-tile approximate sums / prefixes, per-CTA
+    // item lists (seq::Item[kSeqItemCap] each) and their {count, overflow} words
+    double* seq_tsum;
+    void* seq_items;
+    int* seq_counts;
+    int seq_tiles;
+    int seq_exact;          // 1: the two sums are the reference's sequential ones; 0: tree sums (A/B)
     unsigned long long* slots;   // [3][8] rotating max slots for per-term reductions
     unsigned long long* mslots;  // [2][4] metric max/min/r2 slots (step parity)
     Ctrl* ctrl;
@@ -214,11 +224,19 @@ __global__ void label_count_kernel(const uint8_t* labels, int64_t n, unsigned lo
 __global__ void metrics_kernel(const __grid_constant__ SolveParams p);
 __global__ void prep_kernel(const __grid_constant__ SolveParams p, int step);
 __global__ void border_kernel(const __grid_constant__ SolveParams p, int prep_blocks, int step);
+// The reference's sequential sums (gs_seqsum.cuh), which = 0 ||b||_1, 1 the bordered column sum:
+// tile pass, then item pass + composer (last CTA); result in ctrl->seq[which].
+__global__ void seqsum_tiles_kernel(const __grid_constant__ SolveParams p, int which);
+__global__ void seqsum_items_kernel(const __grid_constant__ SolveParams p, int which);
+constexpr int kSeqTileElems = kSolveThreads * 8;  // elements per tile (kSeqTile in gs_solve.cu)
+constexpr int kSeqItemBytes = 40;                 // sizeof(seq::Item)
+constexpr int kSeqItemsPerCta = 512;              // kSeqItemCap
 // Small grids: whole runs in one thread-block cluster (gs_cluster.cu).
 constexpr int kClusterCTAs = 16;  // non-portable cluster size (opt-in attribute)
 struct ClusterParams {
     StencilOp op;            // palette mode: pal + wtab
     int n_steps, want_metrics;
+    int seq_exact;           // 1: the reference's sequential sums (gs_seqsum.cuh); 0: rank-order tree sums
     int64_t slice, halo;     // voxels per CTA, halo width (one plane, or one row in 2-D)
     double rho, tau, tol, anorm;
     double rtab[kMaxDegree + 1];
@@ -253,6 +271,8 @@ __global__ void ens_metrics_kernel(const SolveParams* P, int cpm);
 __global__ void ens_prep_kernel(const SolveParams* P, int cpm, int step);
 __global__ void ens_border_kernel(const SolveParams* P, int cpm, int prep_blocks, int step);
 __global__ void ens_update_kernel(const SolveParams* P, int cpm, int step);
+__global__ void ens_seqsum_tiles_kernel(const SolveParams* P, int cpm, int which);
+__global__ void ens_seqsum_items_kernel(const SolveParams* P, int cpm, int which);
 __global__ void ens_order_kernel(const SolveParams* P, int n_members, unsigned* order);
 const void* ens_taylor_kernel_fn(int fuse);  // fuse 2 or 4 (args: P, n_members, group, border_blocks, step, ctl, order)
 inline int ens_ctl_words(int groups) { return 4 * groups + 1; }

@@ -114,6 +114,178 @@ __device__ double grid_sum(const double* part, int nb, S& sm) {
     return r;
 }
 
+#include "gs_seqsum.cuh"
+
+// ------------------------------------------------------------------------------------------
+// Exact sequential sums (gs_seqsum.cuh): which = 0 ||b||_1 of G (before the border pass),
+// which = 1 the bordered column sum of G = b/gamma (after it).
+// ------------------------------------------------------------------------------------------
+static_assert(kSeqTile == kSeqTileElems && sizeof(seq::Item) == kSeqItemBytes && kSeqItemCap == kSeqItemsPerCta,
+              "gs_kernels.cuh mirrors the seqsum layout");
+constexpr int kSeqMaxLists = 1024;  // CTA lists the composer can index (virtual grids <= 2 x SMs)
+
+__device__ __forceinline__ bool seq_skip(const SolveParams& p, int which) {
+    if (__ldcg(&p.ctrl->status)) return true;
+    return which == 1 && __ldcg(&p.ctrl->branch) != 0;
+}
+
+// Pass 1: approximate per-tile sums (any order) and non-finite flags; the last CTA turns the
+// tile sums into approximate exclusive prefixes (in place).
+__device__ __forceinline__ void seqsum_tiles_body(const SolveParams& p, int which) {
+    __shared__ SeqSmem sm;
+    if (seq_skip(p, which)) return;
+    Ctrl* ctrl = p.ctrl;
+    const double* X = p.buf[kBufG];
+    const int64_t n = p.op.n;
+    const int tiles = p.seq_tiles;
+    unsigned flags = 0;
+    for (int t = vcta(); t < tiles; t += vncta()) {
+        const int64_t base = static_cast<int64_t>(t) * kSeqTile + threadIdx.x;
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < kSeqEPT; ++j) {
+            const int64_t i = base + static_cast<int64_t>(j) * kSolveThreads;
+            if (i < n) {
+                const double x = fabs(X[i]);
+                flags |= isnan(x) ? seq::kHasNaN : (isinf(x) ? seq::kHasInf : 0u);
+                s = __dadd_rn(s, x);
+            }
+        }
+        double tot;
+        seq_block_excl_sum(s, sm, &tot);
+        if (threadIdx.x == 0) p.seq_tsum[t] = tot;
+    }
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if ((threadIdx.x & 31) == 0 && flags) atomicOr(&ctrl->seq_flags[which], flags);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        sm.last = atomicAdd(&ctrl->seq_ticket[which], 1u) == static_cast<unsigned>(vncta()) - 1;
+    }
+    __syncthreads();
+    if (!sm.last) return;
+    __threadfence();
+    double carry = 0.0;
+    for (int t0 = 0; t0 < tiles; t0 += kSolveThreads) {
+        const int t = t0 + threadIdx.x;
+        const double v = t < tiles ? __ldcg(p.seq_tsum + t) : 0.0;
+        double tot;
+        const double ex = seq_block_excl_sum(v, sm, &tot);
+        if (t < tiles) p.seq_tsum[t] = __dadd_rn(carry, ex);
+        carry = __dadd_rn(carry, tot);
+    }
+    if (threadIdx.x == 0) ctrl->seq_ticket[which] = 0u;
+}
+
+// s <- fl(s + |X[i]|) for i in [lo, hi): the reference's loop itself (fallback of the walk)
+__device__ __noinline__ double seq_walk(double s, const double* X, int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) s = __dadd_rn(s, fabs(__ldcg(X + i)));
+    return s;
+}
+
+// Pass 2: per CTA, a contiguous range of tiles -> its list of run / raw items; the last CTA
+// composes all lists in order into the exact sequential sum.
+__device__ __forceinline__ void seqsum_items_body(const SolveParams& p, int which) {
+    __shared__ SeqSmem sm;
+    __shared__ seq::Item s_items[kSolveThreads];
+    __shared__ int s_pref[kSeqMaxLists + 1];
+    if (seq_skip(p, which)) return;
+    Ctrl* ctrl = p.ctrl;
+    const double* X = p.buf[kBufG];
+    const int64_t n = p.op.n;
+    const int tiles = p.seq_tiles;
+    const int nc = vncta(), c = vcta();
+    const int tpc = (tiles + nc - 1) / nc;
+    const int t_lo = min(tiles, c * tpc), t_hi = min(tiles, t_lo + tpc);
+    seq::Item* items = static_cast<seq::Item*>(p.seq_items) + static_cast<size_t>(c) * kSeqItemCap;
+    const unsigned fl = __ldcg(&ctrl->seq_flags[which]);
+    if (threadIdx.x == 0) seq_open_reset(sm);
+    __syncthreads();
+    for (int t = t_lo; t < t_hi && fl == 0; ++t) {
+        const int64_t base = static_cast<int64_t>(t) * kSeqTile;
+        const int cnt = static_cast<int>(min(static_cast<int64_t>(kSeqTile), n - base));
+        const double* Xt = X + base;
+        seq_tile_items<kSeqEPT>(sm, [&](int e) { return Xt[e]; }, base, cnt, __ldcg(p.seq_tsum + t), items,
+                                kSeqItemCap);
+    }
+    if (threadIdx.x == 0) {
+        int k = sm.items;
+        if (fl == 0 && t_lo < t_hi) k = seq_close(sm, min(n, static_cast<int64_t>(t_hi) * kSeqTile), items, kSeqItemCap);
+        p.seq_counts[2 * c] = min(k, kSeqItemCap);
+        p.seq_counts[2 * c + 1] = k > kSeqItemCap;
+        __threadfence();
+        sm.last = atomicAdd(&ctrl->seq_ticket2[which], 1u) == static_cast<unsigned>(nc) - 1;
+    }
+    __syncthreads();
+    if (!sm.last) return;
+    __threadfence();
+    // ---- composer (last CTA): walk the lists in order from s = 0
+    double s = 0.0;
+    if (fl & seq::kHasNaN) {
+        s = __longlong_as_double(0x7ff8000000000000ll);
+    } else if (fl & seq::kHasInf) {
+        s = __longlong_as_double(0x7ff0000000000000ll);
+    } else {
+        // items per list (an overflowed list counts as one pseudo-item: its whole range)
+        int tot = 0;
+        for (int c0 = 0; c0 < nc; c0 += kSolveThreads) {
+            const int cc = c0 + threadIdx.x;
+            int cnt = 0;
+            if (cc < nc) cnt = __ldcg(p.seq_counts + 2 * cc + 1) ? 1 : __ldcg(p.seq_counts + 2 * cc);
+            int t2;
+            const int ex = seq_block_excl_int(cnt, sm, &t2);
+            if (cc < nc && cc < kSeqMaxLists) s_pref[cc] = tot + ex;
+            tot += t2;
+        }
+        if (threadIdx.x == 0) s_pref[min(nc, kSeqMaxLists)] = tot;
+        __syncthreads();
+        const seq::Item* all = static_cast<const seq::Item*>(p.seq_items);
+        for (int g0 = 0; g0 < tot; g0 += kSolveThreads) {
+            const int g = g0 + threadIdx.x;
+            if (g < tot) {
+                int lo = 0, hi = min(nc, kSeqMaxLists) - 1;  // list of item g: last pref <= g
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_pref[mid] <= g) lo = mid;
+                    else hi = mid - 1;
+                }
+                if (__ldcg(p.seq_counts + 2 * lo + 1)) {
+                    const int64_t b0 = static_cast<int64_t>(lo) * tpc * kSeqTile;
+                    const int64_t e0 = min(n, static_cast<int64_t>(min(tiles, (lo + 1) * tpc)) * kSeqTile);
+                    s_items[threadIdx.x] = seq::Item{seq::kMixed, 0, 0, 0, b0, e0 - b0};
+                } else {
+                    const seq::Item* it = all + static_cast<size_t>(lo) * kSeqItemCap + (g - s_pref[lo]);
+                    seq::Item r;
+                    r.kind = __ldcg(&it->kind);
+                    r.B = __ldcg(&it->B);
+                    r.d0 = __ldcg(&it->d0);
+                    r.d1 = __ldcg(&it->d1);
+                    r.start = __ldcg(&it->start);
+                    r.len = __ldcg(&it->len);
+                    s_items[threadIdx.x] = r;
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double acc = sm.bcast;
+                if (g0 == 0) acc = 0.0;
+                const int m = min(kSolveThreads, tot - g0);
+                for (int q = 0; q < m && !isinf(acc); ++q)
+                    seq_apply_item(acc, s_items[q], [&](double a, int64_t lo, int64_t hi) { return seq_walk(a, X, lo, hi); });
+                sm.bcast = acc;
+            }
+            __syncthreads();
+        }
+        s = tot > 0 ? sm.bcast : 0.0;
+    }
+    if (threadIdx.x == 0) {
+        ctrl->seq[which] = s;
+        ctrl->seq_flags[which] = 0u;
+        ctrl->seq_ticket2[which] = 0u;
+        __threadfence();
+    }
+}
+
 __device__ __forceinline__ double slot_read(const unsigned long long* s) {
     return __longlong_as_double(static_cast<long long>(__ldcg(s)));
 }
@@ -1327,7 +1499,8 @@ __device__ __forceinline__ void border_body(const SolveParams& p, int prep_block
         }
         return;
     }
-    const double bnorm = grid_sum(p.part_b, prep_blocks, sm);  // expact.cpp:110 (tree order)
+    // expact.cpp:110: the reference's sequential sum (seqsum kernels) or, for A/B, a tree sum
+    const double bnorm = p.seq_exact ? __ldcg(&ctrl->seq[0]) : grid_sum(p.part_b, prep_blocks, sm);
     int branch = 0;
     if (t == 0.0) branch = 1;                                  // expact.cpp:108
     else if (bnorm == 0.0) branch = 2;                         // expact.cpp:111
@@ -1448,7 +1621,7 @@ __device__ __forceinline__ void taylor_body(const SolveParams& p, int border_blo
     const double gamma = __ldcg(&ctrl->gamma);
     double norm_tA;
     if (bordered) {
-        const double coln = grid_sum(p.part_c, border_blocks, sm);
+        const double coln = p.seq_exact ? __ldcg(&ctrl->seq[1]) : grid_sum(p.part_c, border_blocks, sm);
         // bordered ||.||_1 = max over columns: A's columns, then column n (sparse.cpp:39-40)
         norm_tA = __dmul_rn(fabs(t), nan_dropping_max(p.anorm, coln));
         if (info) info->coln = coln;
@@ -2009,6 +2182,24 @@ __global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_cons
                                                                int step) {
     vgrid_set(blockIdx.x, gridDim.x);
     border_body(p, prep_blocks, step);
+}
+__global__ void __launch_bounds__(kSolveThreads) seqsum_tiles_kernel(const __grid_constant__ SolveParams p, int which) {
+    vgrid_set(blockIdx.x, gridDim.x);
+    seqsum_tiles_body(p, which);
+}
+__global__ void __launch_bounds__(kSolveThreads) seqsum_items_kernel(const __grid_constant__ SolveParams p, int which) {
+    vgrid_set(blockIdx.x, gridDim.x);
+    seqsum_items_body(p, which);
+}
+__global__ void __launch_bounds__(kSolveThreads) ens_seqsum_tiles_kernel(const SolveParams* __restrict__ P, int cpm,
+                                                                         int which) {
+    vgrid_set(blockIdx.x % cpm, cpm);
+    seqsum_tiles_body(P[blockIdx.x / cpm], which);
+}
+__global__ void __launch_bounds__(kSolveThreads) ens_seqsum_items_kernel(const SolveParams* __restrict__ P, int cpm,
+                                                                         int which) {
+    vgrid_set(blockIdx.x % cpm, cpm);
+    seqsum_items_body(P[blockIdx.x / cpm], which);
 }
 __global__ void __launch_bounds__(kSolveThreads) update_kernel(const __grid_constant__ SolveParams p, int step) {
     vgrid_set(blockIdx.x, gridDim.x);
