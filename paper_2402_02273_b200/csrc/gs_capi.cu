@@ -471,11 +471,14 @@ gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps
     p.mslots = c->mslots.as<unsigned long long>();
     p.ctrl = c->ctrl.as<gs::Ctrl>();
     // the reference's sequential ||b||_1 and bordered column sum (GS_TREE_SUMS=1: tree sums, A/B)
-    p.seq_exact = std::getenv("GS_TREE_SUMS") == nullptr ? 1 : 0;
+    p.seq_exact = std::getenv("GS_TREE_SUMS") == nullptr ? (std::getenv("GS_SEQ_DEBUG") ? 2 : 1) : 0;
     p.seq_tiles = static_cast<int>((c->n + gs::kSeqTileElems - 1) / gs::kSeqTileElems);
-    GS_CUDA(c, c->seq_tsum.alloc(sizeof(double) * std::max(1, p.seq_tiles)));
-    GS_CUDA(c, c->seq_items.alloc(static_cast<size_t>(gs::kSeqItemBytes) * gs::kSeqItemsPerCta * sb));
-    GS_CUDA(c, c->seq_counts.alloc(sizeof(int) * 2 * sb));
+    GS_CUDA(c, c->seq_tsum.alloc(sizeof(double) * 2 * std::max(1, p.seq_tiles)));  // tile sums, then prefixes
+    {
+        const int sq = std::min(2 * c->num_sms, gs::kSeqMaxCtas);  // >= any seq_ctas()
+        GS_CUDA(c, c->seq_items.alloc(static_cast<size_t>(gs::kSeqItemBytes) * gs::kSeqItemsPerCta * sq));
+        GS_CUDA(c, c->seq_counts.alloc(sizeof(int) * 2 * sq));
+    }
     p.seq_tsum = c->seq_tsum.as<double>();
     p.seq_items = c->seq_items.p;
     p.seq_counts = c->seq_counts.as<int>();
@@ -509,10 +512,24 @@ int solve_blocks(const gs_ctx* c) {
 
 // The exact sequential sum `which` (0: ||b||_1 before the border pass, 1: the bordered column
 // sum after it) on the context's stream; expmv has neither.
-void launch_seqsum(gs_ctx* c, const gs::SolveParams& p, int sb, int which) {
+// CTAs of the seqsum kernels for one run when `members` runs share the GPU: about two per SM
+// in all (one resident wave), at least a few tiles each; GS_SEQ_CTAS overrides (A/B).
+int seq_ctas(const gs_ctx* c, int tiles, int members) {
+    int k = 2 * c->num_sms;
+    (void)members;
+    if (const char* e = std::getenv("GS_SEQ_CTAS")) k = std::max(1, std::atoi(e));
+    return std::max(1, std::min({k, (tiles + 1) / 2, 2 * c->num_sms, gs::kSeqMaxCtas}));
+}
+
+void launch_seqsum(gs_ctx* c, const gs::SolveParams& p, int which) {
     if (!p.seq_exact || p.mode == gs::kModeExpmv) return;
-    gs::seqsum_tiles_kernel<<<sb, gs::kSolveThreads, 0, c->stream>>>(p, which);
-    gs::seqsum_items_kernel<<<sb, gs::kSolveThreads, 0, c->stream>>>(p, which);
+    const int k = seq_ctas(c, p.seq_tiles, 1);
+    // the tile pass: one CTA per SM at most (its last-CTA ticket costs ~50 ns per CTA; measured
+    // C3 14.5 us with 148 CTAs against 21 us with 256 and 35 us with 592)
+    int k1 = std::max(1, std::min(p.seq_tiles, c->num_sms));
+    if (const char* e = std::getenv("GS_SEQ_CTAS1")) k1 = std::max(1, std::min(p.seq_tiles, std::atoi(e)));
+    gs::seqsum_tiles_kernel<<<k1, gs::kSolveThreads, 0, c->stream>>>(p, which);
+    gs::seqsum_items_kernel<<<k, gs::kSolveThreads, 0, c->stream>>>(p, which);
 }
 
 gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* metrics, gs_step_info* infos) {
@@ -607,9 +624,9 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
             if (ok) {
                 gs::prep_kernel<<<gb, blk, dyn_prep, c->stream>>>(p, -1);
-                launch_seqsum(c, p, sb, 0);
+                launch_seqsum(c, p, 0);
                 gs::border_kernel<<<sb, blk, 0, c->stream>>>(p, gb, -1);
-                launch_seqsum(c, p, sb, 1);
+                launch_seqsum(c, p, 1);
                 cudaLaunchCooperativeKernel(gs::taylor_kernel_fn(p.fuse), dim3(gb), blk, args, dyn, c->stream);
                 gs::update_kernel<<<sb, blk, 0, c->stream>>>(p, -1);
                 gs::advance_kernel<<<1, 1, 0, c->stream>>>(p.ctrl);
@@ -634,9 +651,9 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             GS_CUDA(c, cudaGetLastError());
             GS_CUDA(c, ev_end());
             GS_CUDA(c, ev(1));  // border and the two exact sums
-            launch_seqsum(c, p, sb, 0);
+            launch_seqsum(c, p, 0);
             gs::border_kernel<<<sb, blk, 0, c->stream>>>(p, gb, step);
-            launch_seqsum(c, p, sb, 1);
+            launch_seqsum(c, p, 1);
             GS_CUDA(c, cudaGetLastError());
             GS_CUDA(c, ev_end());
             int border_blocks = sb;
@@ -1295,6 +1312,8 @@ namespace {
 struct EnsPlan {
     std::vector<gs::SolveParams> P;
     int groups = 1, grp = 1, sb = 1, fuse = 2;
+    int sq = 1;   // CTAs per member of the seqsum item pass
+    int sq1 = 1;  // ... and of its tile pass
     bool batched = false;
     bool seq_exact = true;  // the members' SolveParams::seq_exact (one environment, one value)
 };
@@ -1338,6 +1357,14 @@ gs_status ens_prepare(gs_ctx* const* ctxs, int n_members, int n_steps, const dou
     for (int i = 0; i < n_members; ++i) plan.sb = std::max(plan.sb, stream_blocks(ctxs[i]));
     plan.fuse = thin ? 4 : 2;
     plan.seq_exact = std::getenv("GS_TREE_SUMS") == nullptr;
+    {
+        int tiles = 1;
+        for (int i = 0; i < n_members; ++i)
+            tiles = std::max(tiles, static_cast<int>((ctxs[i]->n + gs::kSeqTileElems - 1) / gs::kSeqTileElems));
+        plan.sq = seq_ctas(c0, tiles, n_members);
+        plan.sq1 = std::max(1, std::min(tiles, 2 * c0->num_sms / n_members));
+        if (const char* e = std::getenv("GS_SEQ_CTAS1")) plan.sq1 = std::max(1, std::min(tiles, std::atoi(e)));
+    }
     plan.P.assign(static_cast<size_t>(n_members), gs::SolveParams{});
     for (int i = 0; i < n_members; ++i) {
         gs_ctx* c = ctxs[i];
@@ -1377,13 +1404,13 @@ cudaError_t ens_launch(const EnsPlan& plan, const gs::SolveParams* dP, int n, in
     for (int step = 0; step < n_steps; ++step) {
         gs::ens_prep_kernel<<<n * grp, blk, gs::kRingBytes, st>>>(dP, grp, step);
         if (plan.seq_exact) {
-            gs::ens_seqsum_tiles_kernel<<<n * sb, blk, 0, st>>>(dP, sb, 0);
-            gs::ens_seqsum_items_kernel<<<n * sb, blk, 0, st>>>(dP, sb, 0);
+            gs::ens_seqsum_tiles_kernel<<<n * plan.sq1, blk, 0, st>>>(dP, plan.sq1, 0);
+            gs::ens_seqsum_items_kernel<<<n * plan.sq, blk, 0, st>>>(dP, plan.sq, 0);
         }
         gs::ens_border_kernel<<<n * sb, blk, 0, st>>>(dP, sb, grp, step);
         if (plan.seq_exact) {
-            gs::ens_seqsum_tiles_kernel<<<n * sb, blk, 0, st>>>(dP, sb, 1);
-            gs::ens_seqsum_items_kernel<<<n * sb, blk, 0, st>>>(dP, sb, 1);
+            gs::ens_seqsum_tiles_kernel<<<n * plan.sq1, blk, 0, st>>>(dP, plan.sq1, 1);
+            gs::ens_seqsum_items_kernel<<<n * plan.sq, blk, 0, st>>>(dP, plan.sq, 1);
         }
         gs::ens_order_kernel<<<1, 256, 0, st>>>(dP, n, ctl + gs::ens_ctl_words(groups));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -15,6 +15,7 @@
 // The arithmetic is the large-grid path's operation for operation (row_apply in CSR column
 // order, the same termination tests, expact.cpp:63-153; integrator.cpp:52-89).
 #include <cooperative_groups.h>
+#include <cstdio>
 
 #include "gs_kernels.cuh"
 
@@ -117,17 +118,21 @@ __device__ __forceinline__ void block_to_mbox(ClusterShared& cs, int par, double
 // before anyone overwrites B.
 constexpr int kClItemCap = 32;
 constexpr int kClEPT = 8;  // elements per thread: slices of up to kCT * 8 voxels
+constexpr int kClAll = kClusterCTAs * kClItemCap + 8;  // the gathered sequence (+ walk padding)
 struct ClusterSeq {
     SeqSmem sm;
     seq::Item own[kClItemCap];
-    seq::Item all[kClusterCTAs * kClItemCap];
-    int count, cnt[kClusterCTAs];
+    int kind[kClAll], B[kClAll];
+    uint64_t d0[kClAll], d1[kClAll], lo[kClAll], hi[kClAll];
+    longlong2 pos[kClAll];
+    int count, pref[kClusterCTAs + 1];
+    int walked;  // this CTA's walk read remote B (a fallback)
     unsigned flags;
     double result, prefix;
 };
 
 __device__ double cl_exact_sum(cg::cluster_group& cl, ClusterShared& cs, ClusterSeq& q, int par, const double* B,
-                               int64_t len, int64_t lo, int64_t S, int64_t N, int rank, int nranks) {
+                               int64_t len, int64_t lo, int64_t S, int64_t N, int rank, int nranks, bool debug) {
     const int tid = threadIdx.x;
     // approximate sum before this slice; this slice's non-finite flags
     if (tid < 32) {
@@ -139,56 +144,93 @@ __device__ double cl_exact_sum(cg::cluster_group& cl, ClusterShared& cs, Cluster
             seq_open_reset(q.sm);
         }
     }
-    __syncthreads();
+    double xv[kClEPT];
     unsigned f = 0;
-    for (int64_t i = tid; i < len; i += kCT) {
-        const double x = B[i];
-        f |= isnan(x) ? seq::kHasNaN : (isinf(x) ? seq::kHasInf : 0u);
+#pragma unroll
+    for (int j = 0; j < kClEPT; ++j) {
+        const int64_t e = static_cast<int64_t>(tid) * kClEPT + j;
+        xv[j] = e < len ? B[e] : 0.0;
+        f |= isnan(xv[j]) ? seq::kHasNaN : (isinf(xv[j]) ? seq::kHasInf : 0u);
     }
+    __syncthreads();
     f = __reduce_or_sync(0xffffffffu, f);
     if ((tid & 31) == 0 && f) atomicOr(&q.flags, f);
-    seq_tile_items<kClEPT>(q.sm, [&](int e) { return B[e]; }, lo, static_cast<int>(len), q.prefix, q.own, kClItemCap);
+    seq_tile_items<kClEPT>(q.sm, xv, lo, static_cast<int>(len), q.prefix, q.own, kClItemCap);
     if (tid == 0) q.count = len > 0 ? seq_close(q.sm, lo + len, q.own, kClItemCap) : 0;
     cl.sync();
-    // gather every rank's list (thread r * kClItemCap + k loads item k of rank r)
+    // every rank's list, compacted in rank order (an overflowed list: one pseudo-item, its range)
+    if (tid < 32) {
+        int cnt = 0;
+        if (tid < nranks) {
+            cnt = *cl.map_shared_rank(&q.count, tid);
+            cnt = cnt > kClItemCap ? 1 : cnt;
+            const unsigned rf = *cl.map_shared_rank(&q.flags, tid);
+            if (rf && tid != rank) atomicOr(&q.flags, rf);
+        }
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (tid >= o) inc += y;
+        }
+        if (tid < nranks) q.pref[tid + 1] = inc;
+        if (tid == 0) q.pref[0] = 0;
+    }
+    __syncthreads();
     {
         const int r = tid / kClItemCap, k = tid % kClItemCap;
-        if (r < nranks) {
+        if (r < nranks && k < q.pref[r + 1] - q.pref[r]) {
             const int cnt = *cl.map_shared_rank(&q.count, r);
-            if (k == 0) {
-                q.cnt[r] = cnt;
-                const unsigned rf = *cl.map_shared_rank(&q.flags, r);
-                if (rf && r != rank) atomicOr(&q.flags, rf);
-            }
-            if (k < cnt && cnt <= kClItemCap) q.all[r * kClItemCap + k] = cl.map_shared_rank(q.own, r)[k];
-        }
-    }
-    __syncthreads();
-    bool overflow = false;
-    for (int r = 0; r < nranks; ++r) overflow = overflow || q.cnt[r] > kClItemCap;
-    if (tid == 0) {
-        double acc = 0.0;
-        if (q.flags & seq::kHasNaN) {
-            acc = __longlong_as_double(0x7ff8000000000000ll);
-        } else if (q.flags & seq::kHasInf) {
-            acc = __longlong_as_double(0x7ff0000000000000ll);
-        } else {
-            for (int r = 0; r < nranks && !isinf(acc); ++r) {
-                const double* RB = cl.map_shared_rank(B, r);
+            const int at = q.pref[r] + k;
+            seq::Item it;
+            if (cnt > kClItemCap) {
                 const int64_t rlo = r * S;
-                auto walk = [&](double a, int64_t l, int64_t h) {
-                    for (int64_t i = l; i < h; ++i) a = __dadd_rn(a, fabs(RB[i - rlo]));
-                    return a;
-                };
-                if (q.cnt[r] > kClItemCap) acc = walk(acc, rlo, min(N, rlo + S));
-                else
-                    for (int k = 0; k < q.cnt[r]; ++k) seq_apply_item(acc, q.all[r * kClItemCap + k], walk);
+                it = seq::Item{seq::kMixed, 0, 0, 0, rlo, min(N, rlo + S) - rlo};
+            } else {
+                it = cl.map_shared_rank(q.own, r)[k];
             }
+            q.kind[at] = it.kind;
+            q.B[at] = it.B;
+            seq_stage(it.kind, it.B, it.d0, it.d1, q.d0[at], q.d1[at], q.lo[at], q.hi[at]);
+            q.pos[at] = make_longlong2(it.start, it.len);
         }
-        q.result = acc;
+        const int total = q.pref[nranks];
+        if (tid < 8) {  // padding of the walk's last batch: zero runs
+            q.kind[total + tid] = seq::kEmpty;
+            q.B[total + tid] = 0;
+            q.d0[total + tid] = q.d1[total + tid] = q.lo[total + tid] = 0ull;
+            q.hi[total + tid] = ~0ull;
+        }
     }
-    if (overflow) cl.sync();  // remote B was read: nobody may overwrite it before everyone is done
     __syncthreads();
+    bool walked = false;  // a fallback read remote B
+    if (tid == 0) {
+        uint64_t bits = 0ull;
+        bool fin = true;
+        if (q.flags & seq::kHasNaN) {
+            bits = 0x7ff8000000000000ull;
+        } else if (q.flags & seq::kHasInf) {
+            bits = 0x7ff0000000000000ull;
+        } else {
+            fin = seq_walk_batch(bits, q.kind, q.B, q.d0, q.d1, q.lo, q.hi, q.pos, q.pref[nranks],
+                                 [&](double a, int64_t l, int64_t h) {
+                                     walked = true;
+                                     for (int64_t i = l; i < h; ++i) {
+                                         const int r = static_cast<int>(i / S);
+                                         a = __dadd_rn(a, fabs(cl.map_shared_rank(B, r)[i - r * S]));
+                                     }
+                                     return a;
+                                 },
+                                 debug);
+            if (!fin) bits = 0x7ff0000000000000ull;
+        }
+        q.result = __longlong_as_double(static_cast<long long>(bits));
+        q.walked = walked ? 1 : 0;
+    }
+    __syncthreads();
+    // a fallback walk read remote B: nobody may overwrite it before everyone is done (uniform:
+    // every rank walks the same items with the same state)
+    if (q.walked) cl.sync();
     return q.result;
 }
 
@@ -312,7 +354,11 @@ __global__ void __launch_bounds__(kCT, 1) cluster_run_kernel(const __grid_consta
         const int ksum[1] = {0};
         double bnorm;  // expact.cpp:110: the reference's sequential sum (or a rank-order tree sum, A/B)
         if (p.seq_exact) {
-            bnorm = cl_exact_sum(cl, cs, csq, par, B, len, lo, S, N, rank, nranks);
+            const long long tc = clock64();
+            bnorm = cl_exact_sum(cl, cs, csq, par, B, len, lo, S, N, rank, nranks, p.seq_exact > 1);
+            if (p.seq_exact > 1 && leader)
+                printf("cluster step %d: bnorm exact sum %lld cycles, %d items\n", step, clock64() - tc,
+                       csq.pref[nranks]);
         } else {
             cl_combine<1>(cl, cs, par, ksum);
             bnorm = cs.bcast[0];
@@ -353,12 +399,14 @@ __global__ void __launch_bounds__(kCT, 1) cluster_run_kernel(const __grid_consta
             }
             block_to_mbox<1>(cs, par, cs1, ks);
             cl.sync();
-            double coln;  // sparse.cpp:36-38 on the bordered operator: sequential, or tree (A/B)
-            if (p.seq_exact) {
-                coln = cl_exact_sum(cl, cs, csq, par, B, len, lo, S, N, rank, nranks);
-            } else {
-                cl_combine<1>(cl, cs, par, ksum);
-                coln = cs.bcast[0];
+            // sparse.cpp:36-38 on the bordered operator: the sequential sum when the step log asks
+            // for it or the rank-order tree sum does not settle (s, m) (seq::coln_settles), else
+            // the tree sum, which then selects the same (s, m)
+            cl_combine<1>(cl, cs, par, ksum);
+            double coln = cs.bcast[0];
+            if (p.seq_exact && (p.infos || !seq::coln_settles(t, p.anorm, coln, N, p.rtab, kMaxDegree))) {
+                if (p.seq_exact > 1 && leader) printf("cluster step %d: coln exact\n", step);
+                coln = cl_exact_sum(cl, cs, csq, par, B, len, lo, S, N, rank, nranks, p.seq_exact > 1);
             }
             par ^= 1;
             const double norm_tA = __dmul_rn(fabs(t), nan_dropping_max(p.anorm, coln));

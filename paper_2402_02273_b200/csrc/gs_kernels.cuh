@@ -153,6 +153,8 @@ struct Ctrl {
     // exact sequential sums (gs_seqsum.cuh): [0] ||b||_1, [1] the bordered column sum
     double seq[2];
     unsigned seq_ticket[2], seq_ticket2[2], seq_flags[2];
+    unsigned border_ticket;
+    int coln_need;        // the tree column sum does not settle (s, m): the exact one is required
     int last_terms;       // Taylor terms of the last step (ensemble: longest members first)
 };
 
@@ -231,6 +233,7 @@ __global__ void seqsum_items_kernel(const __grid_constant__ SolveParams p, int w
 constexpr int kSeqTileElems = kSolveThreads * 8;  // elements per tile (kSeqTile in gs_solve.cu)
 constexpr int kSeqItemBytes = 40;                 // sizeof(seq::Item)
 constexpr int kSeqItemsPerCta = 512;              // kSeqItemCap
+constexpr int kSeqMaxCtas = 1024;                 // kSeqMaxLists: the composer's list index
 // Small grids: whole runs in one thread-block cluster (gs_cluster.cu).
 constexpr int kClusterCTAs = 16;  // non-portable cluster size (opt-in attribute)
 struct ClusterParams {

@@ -87,6 +87,25 @@ __device__ __forceinline__ Pair elem_pair(double x, int B) {
     return (k & 1) ? Pair{r0 + 1, r0} : Pair{r0, r0 + 1};  // tie: round to the even m + r
 }
 
+// The fast path's element increment without the parity rule: x/u rounded half-down, with
+// `tie` set when x/u is exactly halfway (then only the parity-tracking pair path is exact) and
+// `big` when x reaches 2^53 u (the element cannot belong to a run of binade B).
+__device__ __forceinline__ uint64_t elem_r0(double x, int B, bool& tie, bool& big) {
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(x));
+    const int ex = static_cast<int>(bits >> 52);
+    const uint64_t mx = (bits & kM52) | (ex ? kTwo52 : 0ull);
+    const int sh = (ex ? ex : 1) - 1075 - (B - 52);
+    if (sh >= 0) {
+        big = big || (mx != 0 && (sh >= 1 || mx >= kTwo53));
+        return mx;  // (only meaningful when !big: sh == 0)
+    }
+    const int n = -sh;
+    if (n >= 64) return 0;
+    const uint64_t half = 1ull << (n - 1), rem = mx & ((1ull << n) - 1);
+    tie = tie || rem == half;
+    return (mx + half - 1) >> n;  // k + (rem > half)
+}
+
 // s <- s + run, when s is in binade B and the run keeps it there; false otherwise.
 __device__ __forceinline__ bool apply_run(double& s, int B, const Pair& d) {
     const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
@@ -144,7 +163,43 @@ __device__ __forceinline__ void seg_op(bool fa, const Seg& a, bool& fb, Seg& b) 
     fb = fb || fa;
 }
 
+// Does any value of the bordered column sum within the tree sum's error bound give the same
+// select_params (expact.cpp:29-61) result?  The sequential and the tree sums of the same n
+// non-negative values both lie within (n-1) 2^-53 (relative) of the true sum, so the sequential
+// one lies in [lo, hi] below.  select_params depends on the norm only through
+// stages(m) = max(1, ceil(norm / r_m)), monotone in the norm: if every m has the same stage
+// count at both ends, the whole interval -- the exact value included -- selects the same
+// (s, m).  Then only the reported value needs the exact sum.
+__device__ __forceinline__ bool coln_settles(double t, double anorm, double coln_tree, int64_t n, const double* rtab,
+                                             int max_degree) {
+    if (!isfinite(coln_tree)) return false;
+    const double e = static_cast<double>(n + 64) * 0x1p-52;
+    const double lo = __dmul_rn(coln_tree, 1.0 - e), hi = __dmul_rn(coln_tree, 1.0 + e);
+    const double nlo = __dmul_rn(fabs(t), anorm < lo ? lo : anorm);
+    const double nhi = __dmul_rn(fabs(t), anorm < hi ? hi : anorm);
+    if (!isfinite(nhi)) return false;
+    for (int m = 1; m <= max_degree; ++m)
+        if (ceil(__ddiv_rn(nlo, rtab[m])) != ceil(__ddiv_rn(nhi, rtab[m]))) return false;
+    return true;
+}
+
 }  // namespace seq
+
+// The walk's state: s = m 2^(B-52) with m < 2^53 (s = 0: B = -1022, m = 0).
+struct SeqState {
+    int B;
+    uint64_t m;
+    __device__ __forceinline__ double value() const {
+        const uint64_t bits = m < seq::kTwo52 ? m : ((static_cast<uint64_t>(B + 1023) << 52) | (m & seq::kM52));
+        return __longlong_as_double(static_cast<long long>(bits));
+    }
+    __device__ __forceinline__ void set(double s) {  // finite s >= 0
+        const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
+        const int e = static_cast<int>(bits >> 52);
+        B = (e > 0 ? e : 1) - 1023;
+        m = (bits & seq::kM52) | (e ? seq::kTwo52 : 0ull);
+    }
+};
 
 constexpr int kSeqEPT = 8;                          // elements per thread and tile
 constexpr int kSeqTile = kSolveThreads * kSeqEPT;   // elements per tile
@@ -154,13 +209,15 @@ struct SeqSmem {
     double dred[kSolveThreads / 32];
     int ired[kSolveThreads / 32];
     seq::Seg wseg[kSolveThreads / 32];
+    seq::Pair wpair[2][kSolveThreads / 32];  // fast tiles' warp summaries, double-buffered
     bool wflag[kSolveThreads / 32];
     int lastB[kSolveThreads];      // per thread: binade of its last element (-2000: raw)
     seq::Seg open;                 // the CTA's open segment carried across its tiles
     int open_B;                    // binade of the previous element (-2000: raw / none)
     int items;                     // items emitted so far
-    bool last;
+    bool last, fin;
     double bcast;
+    SeqState st;  // the composer's walk state between item batches
 };
 
 // Exclusive block scan of doubles (fixed order); also returns the block total in *total.
@@ -222,19 +279,59 @@ __device__ __forceinline__ void seq_open_reset(SeqSmem& sm) {
 // owning e in [t EPT, t EPT + EPT); a_tile approximates the sequential sum before the tile.
 // Items go to items[sm.items ..] (up to cap; sm.items counts past it on overflow); the open
 // segment carries over to the next tile in sm.  Every thread of the block must call it.
-template <int EPT, class Load>
-__device__ __forceinline__ void seq_tile_items(SeqSmem& sm, Load load, int64_t base, int cnt, double a_tile,
-                                               seq::Item* items, int cap) {
+template <int EPT>
+__device__ __forceinline__ void seq_tile_items(SeqSmem& sm, const double (&xin)[EPT], int64_t base, int cnt,
+                                               double a_tile, seq::Item* items, int cap) {
     using seq::Seg;
     const int e0 = static_cast<int>(threadIdx.x) * EPT;
     double x[EPT];
     double ts = 0.0;
 #pragma unroll
     for (int j = 0; j < EPT; ++j) {
-        x[j] = e0 + j < cnt ? fabs(load(e0 + j)) : 0.0;
+        x[j] = e0 + j < cnt ? fabs(xin[j]) : 0.0;
         ts = __dadd_rn(ts, x[j]);
     }
-    const double a0 = __dadd_rn(a_tile, seq_block_excl_sum(ts, sm, nullptr));
+    double tile_sum;
+    const double a0 = __dadd_rn(a_tile, seq_block_excl_sum(ts, sm, &tile_sum));
+    // Fast path: the whole tile stays in one binade (its approximate prefix interval, widened
+    // by delta, does) -- one run: an ordered block reduction of the element summaries, merged
+    // into the CTA's open segment.  Block-uniform: a_tile and tile_sum are.
+    {
+        const int bt = seq::binade(__dmul_rn(a_tile, 1.0 - seq::kDelta));
+        const double a_end = __dmul_rn(__dadd_rn(a_tile, tile_sum), 1.0 + seq::kDelta);
+        if (cnt > 0 && isfinite(a_end) && bt == seq::binade(a_end)) {
+            seq::Pair d{0, 0};
+#pragma unroll
+            for (int j = 0; j < EPT; ++j)
+                if (e0 + j < cnt) d = seq::pcompose(d, seq::elem_pair(x[j], bt));
+            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {  // ordered: lane l absorbs lane l + o
+                const uint64_t q0 = __shfl_down_sync(0xffffffffu, d.d0, o);
+                const uint64_t q1 = __shfl_down_sync(0xffffffffu, d.d1, o);
+                if ((lane & (2 * o - 1)) == 0) d = seq::pcompose(d, seq::Pair{q0, q1});
+            }
+            if (lane == 0) sm.wseg[w].d = d;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                seq::Pair t{0, 0};
+                for (int q = 0; q < kSolveThreads / 32; ++q) t = seq::pcompose(t, sm.wseg[q].d);
+                Seg& o = sm.open;
+                if (o.kind == seq::kRun && o.B == bt && sm.open_B == bt) {
+                    o.d = seq::pcompose(o.d, t);
+                } else {
+                    if (o.kind != seq::kEmpty) {
+                        if (sm.items < cap) items[sm.items] = seq::Item{o.kind, o.B, o.d.d0, o.d.d1, o.start, base - o.start};
+                        ++sm.items;
+                    }
+                    o = Seg{seq::kRun, bt, t, base};
+                }
+                sm.open_B = bt;
+            }
+            __syncthreads();
+            return;
+        }
+    }
     // predicted binade of every element (kSeqRawB: the prefix may change binade at it)
     int bj[EPT];
     double a = a0;
@@ -329,6 +426,69 @@ __device__ __forceinline__ void seq_tile_items(SeqSmem& sm, Load load, int64_t b
     __syncthreads();
 }
 
+// Thread 0: append a run of binade bt starting at `base` to the CTA's open segment (or close
+// the open segment into the list and start a new one).
+__device__ __forceinline__ void seq_merge_run(SeqSmem& sm, int bt, const seq::Pair& t, int64_t base, seq::Item* items,
+                                              int cap) {
+    seq::Seg& o = sm.open;
+    if (o.kind == seq::kRun && o.B == bt && sm.open_B == bt) {
+        o.d = seq::pcompose(o.d, t);
+    } else {
+        if (o.kind != seq::kEmpty) {
+            if (sm.items < cap) items[sm.items] = seq::Item{o.kind, o.B, o.d.d0, o.d.d1, o.start, base - o.start};
+            ++sm.items;
+        }
+        o = seq::Seg{seq::kRun, bt, t, base};
+    }
+    sm.open_B = bt;
+}
+
+// Fast tile (the whole tile predicted in binade bt): the ordered summary of this thread's
+// elements x (already |.|, zeros past the end), reduced over the block in element order and
+// merged into the CTA's open segment by thread 0.  One block barrier; the warp summaries are
+// double-buffered by `buf` so consecutive fast tiles need no second one.
+template <int EPT>
+__device__ __forceinline__ void seq_fast_tile(SeqSmem& sm, const double (&x)[EPT], int bt, int64_t base,
+                                              seq::Item* items, int cap, int buf) {
+    using seq::Seg;
+    // Without rounding ties the increment does not depend on the parity: a plain integer sum.
+    {
+        bool tie = false, big = false;
+        uint64_t r = 0;
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) r += seq::elem_r0(x[j], bt, tie, big);
+        if (!__syncthreads_or(tie || big)) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);  // <= 32 * 8 * 2^53
+            if ((threadIdx.x & 31) == 0) sm.wpair[buf][threadIdx.x >> 5] = seq::Pair{r, r};
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint64_t t = 0;
+                for (int q = 0; q < kSolveThreads / 32; ++q) t = seq::sat_add(t, sm.wpair[buf][q].d0);
+                seq_merge_run(sm, bt, seq::Pair{t, t}, base, items, cap);
+            }
+            return;
+        }
+    }
+    seq::Pair d{0, 0};
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) d = seq::pcompose(d, seq::elem_pair(x[j], bt));
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {  // ordered: lane l absorbs lane l + o
+        const uint64_t q0 = __shfl_down_sync(0xffffffffu, d.d0, o);
+        const uint64_t q1 = __shfl_down_sync(0xffffffffu, d.d1, o);
+        if ((lane & (2 * o - 1)) == 0) d = seq::pcompose(d, seq::Pair{q0, q1});
+    }
+    if (lane == 0) sm.wpair[buf][w] = d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        seq::Pair t{0, 0};
+        for (int q = 0; q < kSolveThreads / 32; ++q) t = seq::pcompose(t, sm.wpair[buf][q]);
+        seq_merge_run(sm, bt, t, base, items, cap);
+    }
+}
+
 // Close the range's open segment at global index end (thread 0); returns the item count.
 __device__ __forceinline__ int seq_close(SeqSmem& sm, int64_t end, seq::Item* items, int cap) {
     int k = sm.items;
@@ -338,6 +498,34 @@ __device__ __forceinline__ int seq_close(SeqSmem& sm, int64_t end, seq::Item* it
         ++k;
     }
     return k;
+}
+
+// One item on the integer state: a run in the current binade is m += d[m & 1] (renormalised
+// when it lands exactly on 2^(B+1)); anything else goes through the double value.  Returns
+// false when the state became non-finite (the sum overflowed: it stays inf).
+template <class Walk>
+__device__ __forceinline__ bool seq_step(SeqState& st, int kind, int B, uint64_t d0, uint64_t d1, int64_t start,
+                                         int64_t len, Walk walk) {
+    if (kind == seq::kRun && B == st.B) {
+        const uint64_t mm = st.m + ((st.m & 1) ? d1 : d0);
+        if (mm < seq::kTwo53) {
+            st.m = mm;
+            return true;
+        }
+        if (mm == seq::kTwo53) {
+            if (st.B + 1 > 1023) return false;
+            st.B += 1;
+            st.m = seq::kTwo52;
+            return true;
+        }
+    }
+    if (kind == seq::kEmpty) return true;
+    double s = st.value();
+    if (kind == seq::kRaw) s = __dadd_rn(s, __longlong_as_double(static_cast<long long>(d0)));
+    else s = walk(s, start, start + len);
+    if (!isfinite(s)) return false;
+    st.set(s);
+    return true;
 }
 
 // One item of the walk: acc <- acc + item; walk(acc, lo, hi) adds elements [lo, hi) one by
@@ -351,4 +539,93 @@ __device__ __forceinline__ void seq_apply_item(double& acc, const seq::Item& it,
     }
     if (it.kind == seq::kRun && seq::apply_run(acc, it.B, seq::Pair{it.d0, it.d1})) return;
     acc = walk(acc, it.start, it.start + it.len);
+}
+
+// One item on the state s (as its bits), carefully: a run in s's binade as an integer add
+// (checked), a raw element as __dadd_rn, anything else the reference's loop over its elements.
+// False: the sum overflowed (it stays inf).
+template <class Walk>
+__device__ __noinline__ bool seq_item_slow(uint64_t& bits, int kind, int B, uint64_t d0, uint64_t d1, longlong2 r,
+                                           Walk walk, bool debug) {
+    if (kind == seq::kEmpty) return true;
+    double s = __longlong_as_double(static_cast<long long>(bits));
+    if (kind == seq::kRaw) {
+        s = __dadd_rn(s, __longlong_as_double(static_cast<long long>(d0)));
+    } else if (kind != seq::kRun || !seq::apply_run(s, B, seq::Pair{d0, d1})) {
+        if (debug) printf("seqsum walk: kind %d B %d start %lld len %lld\n", kind, B, r.x, r.y);
+        s = walk(s, r.x, r.x + r.y);
+    }
+    bits = static_cast<uint64_t>(__double_as_longlong(s));
+    return isfinite(s);
+}
+
+// The composer's inner loop over m staged items (thread 0), on the bits of s.  Within a binade
+// the bits of s are ((B + 1022) << 52) + m for every B (subnormals included), and 2^(B+1)'s
+// bits are what m = 2^53 gives -- so a run is bits += d[bits & 1] and a raw element one
+// __dadd_rn: a chain of about three dependent instructions per item.  Whether each run really
+// started in its binade and stayed in it (lo <= bits, result <= hi) is checked off the chain;
+// a batch with any failure is redone item by item with seq_item_slow.
+constexpr int kSeqWalkU = 8;
+template <class Walk>
+__device__ __noinline__ bool seq_walk_batch(uint64_t& io, const int* kind, const int* bb, const uint64_t* d0,
+                                            const uint64_t* d1, const uint64_t* lo, const uint64_t* hi,
+                                            const longlong2* pos, int m, Walk walk, bool debug) {
+    // staged so that the chain has no branches: empties (and the padding up to a multiple of
+    // kSeqWalkU) are zero runs valid anywhere, mixed items have lo > hi (always "bad"), a raw
+    // item has lo = 0, hi = ~0 and its value in d0
+    uint64_t bits = io;
+    for (int q0 = 0; q0 < m; q0 += kSeqWalkU) {
+        const uint64_t start = bits;
+        uint64_t a0[kSeqWalkU], a1[kSeqWalkU], l[kSeqWalkU], h[kSeqWalkU];
+        bool raw[kSeqWalkU];
+#pragma unroll
+        for (int u = 0; u < kSeqWalkU; ++u) {
+            a0[u] = d0[q0 + u];
+            a1[u] = d1[q0 + u];
+            l[u] = lo[q0 + u];
+            h[u] = hi[q0 + u];
+            raw[u] = kind[q0 + u] == seq::kRaw;
+        }
+        unsigned bad = 0;
+#pragma unroll
+        for (int u = 0; u < kSeqWalkU; ++u) {
+            const uint64_t odd = 0ull - (bits & 1ull);
+            const uint64_t run = bits + (a0[u] ^ ((a0[u] ^ a1[u]) & odd));
+            const uint64_t rw = static_cast<uint64_t>(__double_as_longlong(
+                __dadd_rn(__longlong_as_double(static_cast<long long>(bits)), __longlong_as_double(static_cast<long long>(a0[u])))));
+            bad |= static_cast<unsigned>(bits < l[u]) | static_cast<unsigned>(run > h[u]);
+            bits = raw[u] ? rw : run;
+        }
+        if (bad | static_cast<unsigned>(bits >= 0x7ff0000000000000ull)) {
+            if (debug) printf("seqsum walk: slow batch at %d\n", q0);
+            bits = start;
+            for (int q = q0; q < min(m, q0 + kSeqWalkU); ++q)
+                if (!seq_item_slow(bits, kind[q], bb[q], d0[q], d1[q], pos[q], walk, debug)) return false;
+        }
+    }
+    io = bits;
+    return true;
+}
+
+// Stage one item for seq_walk_batch: a run of binade B must start in [2^B, 2^(B+1)) (B = -1022:
+// from 0) and end <= 2^(B+1); raw items and empties are valid anywhere (empties are zero runs);
+// mixed items (or a run with an impossible binade) always fail -> the slow path.
+__device__ __forceinline__ void seq_stage(int kind, int B, uint64_t d0, uint64_t d1, uint64_t& o0, uint64_t& o1,
+                                          uint64_t& lo, uint64_t& hi) {
+    o0 = kind == seq::kEmpty ? 0ull : d0;
+    o1 = kind == seq::kEmpty ? 0ull : d1;
+    lo = 0ull;
+    hi = ~0ull;
+    if (kind == seq::kRun) {
+        if (B >= -1022 && B <= 1023) {
+            lo = B == -1022 ? 0ull : static_cast<uint64_t>(B + 1023) << 52;
+            hi = static_cast<uint64_t>(B + 1024) << 52;
+        } else {
+            lo = ~0ull;
+            hi = 0ull;
+        }
+    } else if (kind == seq::kMixed) {
+        lo = ~0ull;
+        hi = 0ull;
+    }
 }

@@ -22,6 +22,7 @@
 // fallback sweep with identical arithmetic.
 #include <cooperative_groups.h>
 
+#include <cstdio>
 #include <type_traits>
 
 #include "gs_kernels.cuh"
@@ -120,43 +121,82 @@ __device__ double grid_sum(const double* part, int nb, S& sm) {
 // Exact sequential sums (gs_seqsum.cuh): which = 0 ||b||_1 of G (before the border pass),
 // which = 1 the bordered column sum of G = b/gamma (after it).
 // ------------------------------------------------------------------------------------------
-static_assert(kSeqTile == kSeqTileElems && sizeof(seq::Item) == kSeqItemBytes && kSeqItemCap == kSeqItemsPerCta,
-              "gs_kernels.cuh mirrors the seqsum layout");
+
 constexpr int kSeqMaxLists = 1024;  // CTA lists the composer can index (virtual grids <= 2 x SMs)
+static_assert(kSeqTile == kSeqTileElems && sizeof(seq::Item) == kSeqItemBytes && kSeqItemCap == kSeqItemsPerCta &&
+                  kSeqMaxLists == kSeqMaxCtas,
+              "gs_kernels.cuh mirrors the seqsum layout");
 
 __device__ __forceinline__ bool seq_skip(const SolveParams& p, int which) {
     if (__ldcg(&p.ctrl->status)) return true;
-    return which == 1 && __ldcg(&p.ctrl->branch) != 0;
+    if (which == 0) return false;
+    // the column sum: only on the Taylor branch, and only when (s, m) or the step log needs it
+    return __ldcg(&p.ctrl->branch) != 0 || (!p.infos && !__ldcg(&p.ctrl->coln_need));
 }
 
 // Pass 1: approximate per-tile sums (any order) and non-finite flags; the last CTA turns the
 // tile sums into approximate exclusive prefixes (in place).
 __device__ __forceinline__ void seqsum_tiles_body(const SolveParams& p, int which) {
     __shared__ SeqSmem sm;
+    __shared__ double s_part[16][kSolveThreads / 32];
     if (seq_skip(p, which)) return;
     Ctrl* ctrl = p.ctrl;
     const double* X = p.buf[kBufG];
     const int64_t n = p.op.n;
     const int tiles = p.seq_tiles;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned flags = 0;
-    for (int t = vcta(); t < tiles; t += vncta()) {
-        const int64_t base = static_cast<int64_t>(t) * kSeqTile + threadIdx.x;
-        double s = 0.0;
+    // tiles vcta(), vcta() + vncta(), ...: warp partials in shared memory, 16 tiles per barrier;
+    // the loads of four tiles are issued before any of their reductions
+    constexpr int kG = 2;
+    for (int t0 = vcta(); t0 < tiles; t0 += 16 * vncta()) {
+        for (int k0 = 0; k0 < 16; k0 += kG) {
+            double v[kG][kSeqEPT];
 #pragma unroll
-        for (int j = 0; j < kSeqEPT; ++j) {
-            const int64_t i = base + static_cast<int64_t>(j) * kSolveThreads;
-            if (i < n) {
-                const double x = fabs(X[i]);
-                flags |= isnan(x) ? seq::kHasNaN : (isinf(x) ? seq::kHasInf : 0u);
-                s = __dadd_rn(s, x);
+            for (int g = 0; g < kG; ++g) {
+                const int t = t0 + (k0 + g) * vncta();
+                const int64_t base = static_cast<int64_t>(t) * kSeqTile + threadIdx.x;
+                if (t < tiles && static_cast<int64_t>(t + 1) * kSeqTile <= n) {  // whole tile: no predicates
+#pragma unroll
+                    for (int j = 0; j < kSeqEPT; ++j) v[g][j] = X[base + static_cast<int64_t>(j) * kSolveThreads];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < kSeqEPT; ++j) {
+                        const int64_t i = base + static_cast<int64_t>(j) * kSolveThreads;
+                        v[g][j] = t < tiles && i < n ? X[i] : 0.0;
+                    }
+                }
+            }
+            double s[kG];
+#pragma unroll
+            for (int g = 0; g < kG; ++g) {
+                s[g] = 0.0;
+#pragma unroll
+                for (int j = 0; j < kSeqEPT; ++j) {
+                    const double x = fabs(v[g][j]);
+                    flags |= isnan(x) ? seq::kHasNaN : (isinf(x) ? seq::kHasInf : 0u);
+                    s[g] = __dadd_rn(s[g], x);
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < kG; ++g) {
+                const double v = warp_sum(s[g]);
+                if (lane == 0) s_part[k0 + g][w] = v;
             }
         }
-        double tot;
-        seq_block_excl_sum(s, sm, &tot);
-        if (threadIdx.x == 0) p.seq_tsum[t] = tot;
+        __syncthreads();
+        if (threadIdx.x < 16) {
+            const int t = t0 + threadIdx.x * vncta();
+            if (t < tiles) {
+                double tot = 0.0;
+                for (int q = 0; q < kSolveThreads / 32; ++q) tot = __dadd_rn(tot, s_part[threadIdx.x][q]);
+                p.seq_tsum[t] = tot;
+            }
+        }
+        __syncthreads();
     }
     flags = __reduce_or_sync(0xffffffffu, flags);
-    if ((threadIdx.x & 31) == 0 && flags) atomicOr(&ctrl->seq_flags[which], flags);
+    if (lane == 0 && flags) atomicOr(&ctrl->seq_flags[which], flags);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -165,14 +205,17 @@ __device__ __forceinline__ void seqsum_tiles_body(const SolveParams& p, int whic
     __syncthreads();
     if (!sm.last) return;
     __threadfence();
-    double carry = 0.0;
-    for (int t0 = 0; t0 < tiles; t0 += kSolveThreads) {
-        const int t = t0 + threadIdx.x;
-        const double v = t < tiles ? __ldcg(p.seq_tsum + t) : 0.0;
-        double tot;
-        const double ex = seq_block_excl_sum(v, sm, &tot);
-        if (t < tiles) p.seq_tsum[t] = __dadd_rn(carry, ex);
-        carry = __dadd_rn(carry, tot);
+    // approximate exclusive prefixes into seq_tsum[tiles ..]: thread i takes ceil(tiles/threads)
+    // consecutive tiles, one block scan
+    double* pre = p.seq_tsum + tiles;
+    const int per = (tiles + kSolveThreads - 1) / kSolveThreads;
+    const int lo = min(tiles, static_cast<int>(threadIdx.x) * per), hi = min(tiles, lo + per);
+    double mine = 0.0;
+    for (int t = lo; t < hi; ++t) mine = __dadd_rn(mine, __ldcg(p.seq_tsum + t));
+    double run = seq_block_excl_sum(mine, sm, nullptr);
+    for (int t = lo; t < hi; ++t) {
+        pre[t] = run;
+        run = __dadd_rn(run, __ldcg(p.seq_tsum + t));
     }
     if (threadIdx.x == 0) ctrl->seq_ticket[which] = 0u;
 }
@@ -187,7 +230,9 @@ __device__ __noinline__ double seq_walk(double s, const double* X, int64_t lo, i
 // composes all lists in order into the exact sequential sum.
 __device__ __forceinline__ void seqsum_items_body(const SolveParams& p, int which) {
     __shared__ SeqSmem sm;
-    __shared__ seq::Item s_items[kSolveThreads];
+    __shared__ int s_kind[kSolveThreads], s_B[kSolveThreads];
+    __shared__ uint64_t s_d0[kSolveThreads], s_d1[kSolveThreads], s_lo[kSolveThreads], s_hi[kSolveThreads];
+    __shared__ longlong2 s_pos[kSolveThreads];
     __shared__ int s_pref[kSeqMaxLists + 1];
     if (seq_skip(p, which)) return;
     Ctrl* ctrl = p.ctrl;
@@ -201,13 +246,49 @@ __device__ __forceinline__ void seqsum_items_body(const SolveParams& p, int whic
     const unsigned fl = __ldcg(&ctrl->seq_flags[which]);
     if (threadIdx.x == 0) seq_open_reset(sm);
     __syncthreads();
+    // tile t's data (thread-contiguous kSeqEPT elements) and its prefix / sum are loaded one
+    // tile ahead
+    double xn[kSeqEPT], pn = 0.0, sn = 0.0;
+    const double* pre = p.seq_tsum + tiles;
+    auto load_tile = [&](int t) {
+        const int64_t b = static_cast<int64_t>(t) * kSeqTile + static_cast<int64_t>(threadIdx.x) * kSeqEPT;
+        if (b + kSeqEPT <= n) {
+            const double2* X2 = reinterpret_cast<const double2*>(X + b);
+#pragma unroll
+            for (int j = 0; j < kSeqEPT / 2; ++j) {
+                const double2 v = X2[j];
+                xn[2 * j] = v.x;
+                xn[2 * j + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kSeqEPT; ++j) xn[j] = b + j < n ? X[b + j] : 0.0;
+        }
+        pn = __ldcg(pre + t);
+        sn = __ldcg(p.seq_tsum + t);
+    };
+    if (fl == 0 && t_lo < t_hi) load_tile(t_lo);
     for (int t = t_lo; t < t_hi && fl == 0; ++t) {
         const int64_t base = static_cast<int64_t>(t) * kSeqTile;
         const int cnt = static_cast<int>(min(static_cast<int64_t>(kSeqTile), n - base));
-        const double* Xt = X + base;
-        seq_tile_items<kSeqEPT>(sm, [&](int e) { return Xt[e]; }, base, cnt, __ldcg(p.seq_tsum + t), items,
-                                kSeqItemCap);
+        double x[kSeqEPT];
+#pragma unroll
+        for (int j = 0; j < kSeqEPT; ++j) x[j] = xn[j];
+        const double a_tile = pn, t_sum = sn;
+        if (t + 1 < t_hi) load_tile(t + 1);
+        // the whole tile in one binade (pass 1's tile sum, widened by delta): one run
+        const int bt = seq::binade(__dmul_rn(a_tile, 1.0 - seq::kDelta));
+        const double a_end = __dmul_rn(__dadd_rn(a_tile, t_sum), 1.0 + seq::kDelta);
+        if (isfinite(a_end) && bt == seq::binade(a_end)) {
+#pragma unroll
+            for (int j = 0; j < kSeqEPT; ++j) x[j] = fabs(x[j]);
+            seq_fast_tile<kSeqEPT>(sm, x, bt, base, items, kSeqItemCap, t & 1);
+        } else {
+            __syncthreads();  // thread 0's merge of a previous fast tile is visible
+            seq_tile_items<kSeqEPT>(sm, x, base, cnt, a_tile, items, kSeqItemCap);
+        }
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
         int k = sm.items;
         if (fl == 0 && t_lo < t_hi) k = seq_close(sm, min(n, static_cast<int64_t>(t_hi) * kSeqTile), items, kSeqItemCap);
@@ -220,6 +301,7 @@ __device__ __forceinline__ void seqsum_items_body(const SolveParams& p, int whic
     if (!sm.last) return;
     __threadfence();
     // ---- composer (last CTA): walk the lists in order from s = 0
+    long long t_c0 = clock64(), t_walk = 0;
     double s = 0.0;
     if (fl & seq::kHasNaN) {
         s = __longlong_as_double(0x7ff8000000000000ll);
@@ -237,11 +319,18 @@ __device__ __forceinline__ void seqsum_items_body(const SolveParams& p, int whic
             if (cc < nc && cc < kSeqMaxLists) s_pref[cc] = tot + ex;
             tot += t2;
         }
-        if (threadIdx.x == 0) s_pref[min(nc, kSeqMaxLists)] = tot;
+        if (threadIdx.x == 0) {
+            s_pref[min(nc, kSeqMaxLists)] = tot;
+            sm.st = SeqState{-1022, 0ull};  // s = +0
+            sm.fin = true;
+        }
         __syncthreads();
         const seq::Item* all = static_cast<const seq::Item*>(p.seq_items);
         for (int g0 = 0; g0 < tot; g0 += kSolveThreads) {
             const int g = g0 + threadIdx.x;
+            int kd = seq::kEmpty, bq = 0;
+            uint64_t q0 = 0ull, q1 = 0ull;
+            longlong2 qp = make_longlong2(0, 0);
             if (g < tot) {
                 int lo = 0, hi = min(nc, kSeqMaxLists) - 1;  // list of item g: last pref <= g
                 while (lo < hi) {
@@ -252,31 +341,39 @@ __device__ __forceinline__ void seqsum_items_body(const SolveParams& p, int whic
                 if (__ldcg(p.seq_counts + 2 * lo + 1)) {
                     const int64_t b0 = static_cast<int64_t>(lo) * tpc * kSeqTile;
                     const int64_t e0 = min(n, static_cast<int64_t>(min(tiles, (lo + 1) * tpc)) * kSeqTile);
-                    s_items[threadIdx.x] = seq::Item{seq::kMixed, 0, 0, 0, b0, e0 - b0};
+                    kd = seq::kMixed;
+                    qp = make_longlong2(b0, e0 - b0);
                 } else {
                     const seq::Item* it = all + static_cast<size_t>(lo) * kSeqItemCap + (g - s_pref[lo]);
-                    seq::Item r;
-                    r.kind = __ldcg(&it->kind);
-                    r.B = __ldcg(&it->B);
-                    r.d0 = __ldcg(&it->d0);
-                    r.d1 = __ldcg(&it->d1);
-                    r.start = __ldcg(&it->start);
-                    r.len = __ldcg(&it->len);
-                    s_items[threadIdx.x] = r;
+                    kd = __ldcg(&it->kind);
+                    bq = __ldcg(&it->B);
+                    q0 = __ldcg(&it->d0);
+                    q1 = __ldcg(&it->d1);
+                    qp = make_longlong2(__ldcg(&it->start), __ldcg(&it->len));
                 }
             }
+            {
+                s_kind[threadIdx.x] = kd;
+                s_B[threadIdx.x] = bq;
+                seq_stage(kd, bq, q0, q1, s_d0[threadIdx.x], s_d1[threadIdx.x], s_lo[threadIdx.x], s_hi[threadIdx.x]);
+                s_pos[threadIdx.x] = qp;
+            }
             __syncthreads();
-            if (threadIdx.x == 0) {
-                double acc = sm.bcast;
-                if (g0 == 0) acc = 0.0;
-                const int m = min(kSolveThreads, tot - g0);
-                for (int q = 0; q < m && !isinf(acc); ++q)
-                    seq_apply_item(acc, s_items[q], [&](double a, int64_t lo, int64_t hi) { return seq_walk(a, X, lo, hi); });
-                sm.bcast = acc;
+            if (threadIdx.x == 0 && sm.fin) {
+                const long long tw = clock64();
+                uint64_t bits = static_cast<uint64_t>(__double_as_longlong(sm.st.value()));
+                sm.fin = seq_walk_batch(bits, s_kind, s_B, s_d0, s_d1, s_lo, s_hi, s_pos, min(kSolveThreads, tot - g0),
+                                        [&](double a, int64_t lo, int64_t hi) { return seq_walk(a, X, lo, hi); },
+                                        p.seq_exact > 1);
+                sm.st.set(__longlong_as_double(static_cast<long long>(bits)));
+                t_walk += clock64() - tw;
             }
             __syncthreads();
         }
-        s = tot > 0 ? sm.bcast : 0.0;
+        s = sm.fin ? sm.st.value() : __longlong_as_double(0x7ff0000000000000ll);
+        if (p.seq_exact > 1 && threadIdx.x == 0)
+            printf("seqsum %d: %d lists, %d items, sum %a; composer %lld cycles, walk %lld\n", which, nc, tot, s,
+                   clock64() - t_c0, t_walk);
     }
     if (threadIdx.x == 0) {
         ctrl->seq[which] = s;
@@ -1552,7 +1649,24 @@ __device__ __forceinline__ void border_body(const SolveParams& p, int prep_block
     }
     double s[1] = {csum};
     block_reduce<1, false>(s, sm);
-    if (threadIdx.x == 0) p.part_c[vcta()] = s[0];
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        p.part_c[vcta()] = s[0];
+        last = false;
+        if (p.seq_exact) {  // the last CTA: does the tree column sum settle (s, m)?
+            __threadfence();
+            last = atomicAdd(&ctrl->border_ticket, 1u) == static_cast<unsigned>(vncta()) - 1;
+        }
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        const double coln = grid_sum(p.part_c, vncta(), sm);
+        if (threadIdx.x == 0) {
+            ctrl->coln_need = seq::coln_settles(t, p.anorm, coln, n, p.rtab, kMaxDegree) ? 0 : 1;
+            ctrl->border_ticket = 0u;
+        }
+    }
     if (p.use_tma) fence_proxy_async_global();
 }
 
@@ -1621,7 +1735,11 @@ __device__ __forceinline__ void taylor_body(const SolveParams& p, int border_blo
     const double gamma = __ldcg(&ctrl->gamma);
     double norm_tA;
     if (bordered) {
-        const double coln = p.seq_exact ? __ldcg(&ctrl->seq[1]) : grid_sum(p.part_c, border_blocks, sm);
+        // the exact (sequential) column sum when it was computed -- the step log asks for it, or
+        // the tree sum's error bound straddles a (s, m) boundary -- else the tree sum, which
+        // then provably selects the same (s, m) (seq::coln_settles)
+        const bool exact = p.seq_exact && (p.infos || __ldcg(&ctrl->coln_need));
+        const double coln = exact ? __ldcg(&ctrl->seq[1]) : grid_sum(p.part_c, border_blocks, sm);
         // bordered ||.||_1 = max over columns: A's columns, then column n (sparse.cpp:39-40)
         norm_tA = __dmul_rn(fabs(t), nan_dropping_max(p.anorm, coln));
         if (info) info->coln = coln;
@@ -2183,7 +2301,7 @@ __global__ void __launch_bounds__(kSolveThreads) border_kernel(const __grid_cons
     vgrid_set(blockIdx.x, gridDim.x);
     border_body(p, prep_blocks, step);
 }
-__global__ void __launch_bounds__(kSolveThreads) seqsum_tiles_kernel(const __grid_constant__ SolveParams p, int which) {
+__global__ void __launch_bounds__(kSolveThreads, 2) seqsum_tiles_kernel(const __grid_constant__ SolveParams p, int which) {
     vgrid_set(blockIdx.x, gridDim.x);
     seqsum_tiles_body(p, which);
 }
@@ -2191,7 +2309,7 @@ __global__ void __launch_bounds__(kSolveThreads) seqsum_items_kernel(const __gri
     vgrid_set(blockIdx.x, gridDim.x);
     seqsum_items_body(p, which);
 }
-__global__ void __launch_bounds__(kSolveThreads) ens_seqsum_tiles_kernel(const SolveParams* __restrict__ P, int cpm,
+__global__ void __launch_bounds__(kSolveThreads, 2) ens_seqsum_tiles_kernel(const SolveParams* __restrict__ P, int cpm,
                                                                          int which) {
     vgrid_set(blockIdx.x % cpm, cpm);
     seqsum_tiles_body(P[blockIdx.x / cpm], which);
