@@ -10,7 +10,9 @@ only").  ``e2e`` is the same metric through the drop-in step() call with host bu
 (pinned H2D of u, the step, D2H of the new u every step).  ``roofline`` covers the
 persistent solve kernel (the only kernel in the timed region) against the measured HBM
 copy peak; ``cpu_baseline`` is the UNMODIFIED reference (oracle/_ref) timed on this
-host on a bounded slab sample.  ``--impl reference`` times that reference alone.
+host on full-grid steps of the same workload (one step with all host cores, one with one).
+``--impl reference`` times that reference alone: full-grid gliosim::run steps on all host
+cores, as many of the requested steps as fit in --ref-budget seconds.
 
 Working set at C4: u, b, f x2, T x2 = 6 x 128 MiB fp64 (+ 16 MiB labels) >> 126 MB L2,
 so no L2 flush is needed between steps ("inputs larger than L2").
@@ -59,7 +61,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work for the baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=30.0,
+                    help="CPU time budget of the cpu_baseline sample (at least one full-grid reference step)")
+    ap.add_argument("--ref-budget", type=float, default=600.0,
+                    help="--impl reference: timed seconds after which no further full-grid step starts")
     return ap.parse_args()
 
 
@@ -226,23 +231,16 @@ def initial_state(w, op, labels):
 
 
 # ------------------------------------------------------------------------------------------
-# CPU side: the unmodified reference on a bounded slab sample
+# CPU side: the unmodified reference on the full grid of the workload
 # ------------------------------------------------------------------------------------------
 
-def slab_of(w, labels, u0, depth):
-    """A z-slab of `depth` planes centred on the seed plane (same phantom, same physics)."""
-    nxy = w.nx * w.ny
-    kz = int(np.argmax(u0.reshape(w.nz, nxy).max(axis=1)))
-    z0 = max(0, min(w.nz - depth, kz - depth // 2))
-    sl = slice(z0 * nxy, (z0 + depth) * nxy)
-    return labels[sl].copy(), u0[sl].copy()
-
-
-def cpu_reference_sample(w, labels, u0, target_s, steps=None, warmup=0, gpu_terms_of=None, rho=None, cores=None):
+def cpu_reference_sample(w, labels, u0, steps, warmup=0, rho=None, cores=None, budget_s=None):
     """Time the reference's own run() loop (RunTimings::step_seconds, integrator.cpp:123-125)
-    on a slab with workers = all host cores; the C port stands in only if oracle/_ref is
-    absent.  `steps` fixed -> exactly that many timed steps after `warmup` untimed ones;
-    otherwise as many as fit in ~target_s seconds."""
+    on the FULL grid of the workload with workers = all host cores (or `cores`): `warmup`
+    untimed steps, then `steps` timed steps, one run() call per step so every step is its own
+    sample (the operator assembly of each call is outside step_seconds).  budget_s caps the
+    timed steps when the first one shows they would not fit.  The C port stands in only where
+    oracle/_ref is absent."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import Port
     try:
@@ -253,44 +251,42 @@ def cpu_reference_sample(w, labels, u0, target_s, steps=None, warmup=0, gpu_term
         ref = None
         kind = "port"
     from paper_2402_02273_b200 import workloads as W
-    cores = cores or os.cpu_count() or 1
-    depth = w.nz if w.n <= 128 ** 3 else 16
-    lab_s, u_s = slab_of(w, labels, u0, depth)
-    shape = (w.nx, w.ny, depth)
-    d_s = np.array([0.0, W.D_WHITE, W.D_GRAY, 0.0])[lab_s]
+    cores = cores or host_cores()
+    shape = (w.nx, w.ny, w.nz)
+    d = np.array([0.0, W.D_WHITE, W.D_GRAY, 0.0])[labels]
     center = (0.0, 0.0, 0.0)
     port = Port()
-    op_p = port.stencil(shape, w.h, d_s)
+    op_p = port.stencil(shape, w.h, d)
     rho = w.rho if rho is None else rho
 
-    def timed(u, k):
-        if k <= 0:
-            return u, 0.0
+    def one(u):
         if ref:
-            u2, _, secs = ref.run(shape, w.h, d_s, u, k, rho, W.T0, W.T0 + k * W.TAU, W.TOL, center,
-                                  workers=cores)
+            u2, _, secs = ref.run(shape, w.h, d, u, 1, rho, W.T0, W.T0 + W.TAU, W.TOL, center, workers=cores)
             return u2, secs
         t0 = time.perf_counter()
-        u2, _, _ = port.run(op_p, u, k, rho, W.TAU, W.TOL, center)
+        u2, _, _ = port.run(op_p, u, 1, rho, W.TAU, W.TOL, center)
         return u2, time.perf_counter() - t0
 
-    u, _ = timed(u_s, warmup)
-    if steps is None:
-        _, t1 = timed(u, 1)
-        steps = max(1, min(50, int(target_s / max(t1, 1e-6))))
-    u_end, secs = timed(u, steps)
-    terms = gpu_terms_of(shape, lab_s, u_s, steps + warmup) if gpu_terms_of else None
-    return {"kind": kind, "cores": cores if kind == "reference" else 1, "n_slab": lab_s.size,
-            "slab_shape": shape, "step_times": [secs / steps] * steps, "steps": steps, "terms_slab": terms}
+    u = u0
+    for _ in range(warmup):
+        u, _ = one(u)
+    times = []
+    for k in range(max(1, steps)):
+        u, secs = one(u)
+        times.append(secs)
+        if budget_s is not None and k == 0:
+            steps = max(1, min(steps, int(budget_s / max(secs, 1e-9))))
+        if len(times) >= steps:
+            break
+    return {"kind": kind, "cores": cores if kind == "reference" else 1, "shape": shape, "step_times": times,
+            "steps": len(times), "warmup": warmup}
 
 
-def extrapolate(sample, n_full):
-    """Full-grid steps/s from slab timings, scaled by voxel count (the reference's step
-    cost is linear in voxels x Taylor terms; the slab has the same (s, m) -- ||A||_1 is
-    set by interior white matter -- and its terms per step are reported alongside)."""
-    t = float(np.mean(sample["step_times"]))
-    full = t * n_full / sample["n_slab"]
-    return 1.0 / full, full
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 # ------------------------------------------------------------------------------------------
@@ -395,31 +391,21 @@ def run_ours(args, w, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        def gpu_terms_of(shape, lab_s, u_s, k):
-            g = G.Grid(*shape, h=w.h)
-            with G.StencilOperator.from_labels(g, lab_s) as ops:
-                ops.set_state(u_s)
-                _, inf = ops.run_resident(k, w.rho, w.tau, W.TOL, metrics=False, infos=True)
-                return [inf[q].total_terms for q in range(k)]
         try:
-            sample = cpu_reference_sample(w, labels, u0, args.cpu_seconds, gpu_terms_of=gpu_terms_of)
-            v, full_s = extrapolate(sample, w.n)
-            cpu = {"value": v, "unit": "steps/s", "cores": sample["cores"], "kind": sample["kind"],
-                   "sample": (f"{len(sample['step_times'])} gliosim::step calls (workers={sample['cores']}) on a "
-                              f"{sample['slab_shape'][0]}x{sample['slab_shape'][1]}x{sample['slab_shape'][2]} z-slab "
-                              f"of the same phantom through the seed; mean {np.mean(sample['step_times']):.3f} s/step, "
-                              f"extrapolated by voxel count to {full_s:.1f} s per {w.nx}x{w.ny}x{w.nz} step; slab Taylor "
-                              f"terms/step {np.mean(sample['terms_slab']) if sample['terms_slab'] else float('nan'):.1f} "
-                              f"vs full grid {np.mean(terms):.1f}")}
-            # the reference with workers = 1 as well (one timed step of the slab)
+            # one full-grid step of the reference on all host cores (~15 s at 256^3 on 16 cores),
+            # then one with workers = 1; no extrapolation
+            sample = cpu_reference_sample(w, labels, u0, 1, budget_s=args.cpu_seconds)
+            t = float(np.mean(sample["step_times"]))
+            cpu = {"value": 1.0 / t, "unit": "steps/s", "cores": sample["cores"], "kind": sample["kind"],
+                   "sample": (f"{sample['steps']} gliosim::run step(s) of the full {w.nx}x{w.ny}x{w.nz} grid from the "
+                              f"same u0 (workers={sample['cores']}), {t:.2f} s/step (RunTimings::step_seconds)")}
             if sample["kind"] == "reference" and sample["cores"] > 1:
-                one = cpu_reference_sample(w, labels, u0, args.cpu_seconds, steps=1, cores=1)
-                v1, full1 = extrapolate(one, w.n)
-                cpu.update({"value_1core": v1,
-                            "sample_1core": (f"1 gliosim::step (workers=1) on the same slab, {one['step_times'][0]:.2f} s, "
-                                             f"extrapolated to {full1:.1f} s per full step")})
+                one = cpu_reference_sample(w, labels, u0, 1, cores=1)
+                t1 = float(one["step_times"][0])
+                cpu.update({"value_1core": 1.0 / t1,
+                            "sample_1core": f"1 gliosim::run step of the full grid with workers=1, {t1:.2f} s"})
         except Exception as e:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "unavailable",
+            cpu = {"value": None, "unit": "steps/s", "cores": host_cores(), "kind": "unavailable",
                    "sample": f"failed: {e}"}
 
     traffic = None
@@ -553,8 +539,8 @@ def run_ensemble(args, w, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            sample = cpu_reference_sample(w, runner.ops[0].labels(), runner.u0[0], args.cpu_seconds,
-                                          rho=runner.rhos[0])
+            sample = cpu_reference_sample(w, runner.ops[0].labels(), runner.u0[0], 50, rho=runner.rhos[0],
+                                          budget_s=args.cpu_seconds)
             cpu = {"value": 1.0 / float(np.mean(sample["step_times"])), "unit": "member-steps/s",
                    "cores": sample["cores"], "kind": sample["kind"],
                    "sample": (f"{sample['steps']} gliosim::run steps (workers={sample['cores']}) of member 0 "
@@ -607,24 +593,29 @@ def run_reference(args, w, rank, world, local):
         ui = port.seed_initial((w.nx, w.ny, w.nz), w.h, 1.0, W.seed_width(w), c, d)
         u0 = ui if u0 is None else np.maximum(u0, ui)
     rho = W.member_rho(w, member)
-    sample = cpu_reference_sample(w, labels, u0, args.cpu_seconds, steps=args.steps, warmup=args.warmup, rho=rho)
+    # the reference has no warm-up effects (no JIT, no caches across run() calls): one untimed
+    # step at most; the timed steps are capped by --ref-budget seconds (the first step's time
+    # decides how many fit), and the line reports the number actually timed
+    warm = min(args.warmup, 1)
+    sample = cpu_reference_sample(w, labels, u0, args.steps, warmup=warm, rho=rho, budget_s=args.ref_budget)
+    t = float(np.mean(sample["step_times"]))
     if w.members > 1:
-        v = 1.0 / float(np.mean(sample["step_times"]))
+        v = 1.0 / t
         metric, unit = "ensemble member-steps/s (64 x 128^3 fp64)", "member-steps/s"
-        ms_step = 1e3 * w.members / v
-        desc = (f"{args.steps} timed gliosim::run steps (+{args.warmup} warm-up) of member 0 "
-                f"(rho={rho:.4f}); member-steps/s")
+        ms_step = 1e3 * w.members * t
+        desc = (f"{sample['steps']} timed gliosim::run steps (+{warm} untimed) of member 0 on its full "
+                f"{w.nx}x{w.ny}x{w.nz} grid (rho={rho:.4f}, workers={sample['cores']}); member-steps/s")
     else:
-        v, full_s = extrapolate(sample, w.n)
+        v = 1.0 / t
         metric = "expEuler steps/s at 256^3 fp64" if w.name.startswith("C4") else f"expEuler steps/s ({w.name})"
         unit = "steps/s"
-        ms_step = 1e3 * full_s
-        desc = (f"{args.steps} timed gliosim::run steps (+{args.warmup} warm-up) on a "
-                f"{sample['slab_shape'][0]}x{sample['slab_shape'][1]}x{sample['slab_shape'][2]} z-slab, "
-                f"extrapolated by voxel count to {w.nx}x{w.ny}x{w.nz}")
+        ms_step = 1e3 * t
+        desc = (f"{sample['steps']} timed gliosim::run steps (+{warm} untimed) of the full {w.nx}x{w.ny}x{w.nz} grid "
+                f"(workers={sample['cores']}), {t:.2f} s/step, RunTimings::step_seconds")
     line = {
-        "impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": world, "steps": sample["steps"],
+        "steps_requested": args.steps, "step_seconds": sample["step_times"],
+        "warmup": warm, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong" if w.members > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded shell phantom, BASELINE.json config)",
         "config": {"workload": f"{w.name}: {w.note}", "grid": [w.nx, w.ny, w.nz], "parallelism": "CPU threads"},

@@ -4,9 +4,13 @@
  * Drop-in boundary for the reference gliosim library (/root/reference/proj).  Every
  * entry point names the reference interface it replaces (file:line, paths relative to
  * /root/reference/proj).  Plain pointers and sizes only; host buffers are
- * caller-owned, device memory belongs to the context.  One context = one grid
- * operator + one CUDA stream; a context is not thread-safe (use one per thread),
- * matching the reference's caller-single-threaded API (sparse.hpp:27-29).
+ * caller-owned, device memory belongs to the context.  One context = one grid operator + one
+ * CUDA stream.  Calls on one context from several threads are serialised by a per-context lock
+ * (the reference's operators are immutable and shareable read-only, SPEC.md), and
+ * gs_last_error() returns the message of the calling thread's own last failure on that
+ * context; independent contexts run concurrently.  The value-semantics calls (gs_step_host,
+ * gs_phi1v, gs_expmv, gs_apply, gs_step_ensemble_host) never touch the resident state that
+ * gs_set_state / gs_run / gs_get_state work on.
  *
  * Errors: every call returns a gs_status.  The codes map 1:1 onto the reference's
  * exception types (errors.hpp:10-17, std::invalid_argument); gs_last_error() returns
@@ -114,7 +118,8 @@ gs_status gs_expmv(gs_ctx* ctx, double t, const double* b, double tol, double* o
 gs_status gs_phi1v(gs_ctx* ctx, double t, const double* b, double tol, double* out, gs_step_info* info);
 /* step (integrator.hpp:59-60, integrator.cpp:52-63) on the RESIDENT state: u <- step(A, u). */
 gs_status gs_step(gs_ctx* ctx, double rho, double tau, double tol, gs_step_info* info);
-/* step with host vectors, value semantics as the reference (u in, out returned). */
+/* step with host vectors, value semantics as the reference (u in, out returned); runs on a
+ * staging buffer, leaving the resident state untouched. */
 gs_status gs_step_host(gs_ctx* ctx, const double* u, double rho, double tau, double tol, double* out,
                        gs_step_info* info);
 /* The time loop of run (integrator.cpp:91-138) on the resident state: n_steps steps,

@@ -178,11 +178,15 @@ inline std::vector<double> phi1v(double t, const StencilOperator& a, const std::
     return out;
 }
 
-// step (integrator.cpp:52-63).  Overwrites the operator's resident state.
+// step (integrator.cpp:52-63).  Value semantics: the step runs on the context's staging
+// buffer, the operator's resident state (run) is untouched, and concurrent calls on one
+// operator are serialised by the context.  A length mismatch throws what the reference's
+// first use of u throws: SparseOperator::apply's message (sparse.cpp:44-46).
 inline std::vector<double> step(const StencilOperator& a, const std::vector<double>& u, double rho, double tau,
                                 double tol, int = 1) {
     if (static_cast<int64_t>(u.size()) != a.dim())
-        throw std::invalid_argument("phi1v: vector length does not match operator dimension");
+        throw std::invalid_argument("SparseOperator::apply: vector length " + std::to_string(u.size()) + " != dim " +
+                                    std::to_string(a.dim()));
     std::vector<double> out(u.size());
     check(gs_step_host(a.ctx(), u.data(), rho, tau, tol, out.data(), nullptr), a.ctx());
     return out;
@@ -202,8 +206,8 @@ RunResult run_impl(const SimConfigT& cfg, const DiffusionFieldT& d, std::vector<
                    const SnapshotSink& snapshot, const RangeWarning& on_range, const StepWatcher& on_step,
                    const VtkSink* vtk, bool seed_from_cfg = false) {
     const int64_t n = static_cast<int64_t>(d.grid.nx) * d.grid.ny * d.grid.nz;
-    const double origin[3] = {cfg.origin[0], cfg.origin[1], cfg.origin[2]};
     const double center[3] = {cfg.seed_center[0], cfg.seed_center[1], cfg.seed_center[2]};
+    // compute_metrics places points with the DiffusionField's grid (integrator.cpp:65-89)
     const double gorigin[3] = {d.grid.origin[0], d.grid.origin[1], d.grid.origin[2]};
     if (!seed_from_cfg) cfg.validate();
     if (!seed_from_cfg && static_cast<int64_t>(u0.size()) != n)
@@ -244,9 +248,14 @@ RunResult run_impl(const SimConfigT& cfg, const DiffusionFieldT& d, std::vector<
     emit(0, &u0);
     int done = 0;
     std::vector<gs_metrics> m;
+    // segment ends: the snapshot nodes; every step when a StepWatcher / RangeWarning is given,
+    // so they fire live after each step as in the reference's loop (integrator.cpp:128-131)
+    const bool live = static_cast<bool>(on_step) || static_cast<bool>(on_range);
     while (done < cfg.num_steps) {
         int cut = cfg.num_steps;
-        if (sinks)
+        if (live)
+            cut = done + 1;
+        else if (sinks)
             for (int k = done + 1; k <= cfg.num_steps; ++k)
                 if (k % cfg.snapshot_every == 0 || k == cfg.num_steps) {
                     cut = k;
@@ -255,7 +264,7 @@ RunResult run_impl(const SimConfigT& cfg, const DiffusionFieldT& d, std::vector<
         const int k = cut - done;
         m.assign(static_cast<size_t>(k) + 1, gs_metrics{});
         const auto tic = std::chrono::steady_clock::now();
-        check(gs_run(a.ctx(), k, cfg.rho, tau, cfg.exp_tol, origin, center, cfg.front_threshold, m.data(), nullptr),
+        check(gs_run(a.ctx(), k, cfg.rho, tau, cfg.exp_tol, gorigin, center, cfg.front_threshold, m.data(), nullptr),
               a.ctx());
         res.timings.step_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - tic).count();
         for (int q = done == 0 ? 0 : 1; q <= k; ++q) {
@@ -268,7 +277,7 @@ RunResult run_impl(const SimConfigT& cfg, const DiffusionFieldT& d, std::vector<
                 on_range(sm.step, sm.min_density, sm.max_density);
         }
         done = cut;
-        if (sinks) emit(cut, nullptr);
+        if (sinks && (cut % cfg.snapshot_every == 0 || cut == cfg.num_steps)) emit(cut, nullptr);
     }
     if (vtk) {
         const auto tic = std::chrono::steady_clock::now();

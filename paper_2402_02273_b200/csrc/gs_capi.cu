@@ -30,6 +30,10 @@
 namespace {
 
 thread_local std::string g_create_error;
+// the last failure on this thread and its context: gs_last_error(ctx) reads it first, so another
+// thread's later failure on the same context cannot overwrite the message a caller is reading
+thread_local std::string t_err;
+thread_local const void* t_err_ctx = nullptr;
 
 struct DevBuf {
     void* p = nullptr;
@@ -127,6 +131,11 @@ struct gs_ctx {
     // gs_step_host: the state's H2D / D2H ride in the launch sequence (one synchronisation)
     const double* stage_in = nullptr;
     double* stage_out = nullptr;
+    // value-semantics calls (gs_step_host, gs_step_ensemble_host): the step's state lives in the
+    // `out` buffer (free in run mode) instead of the resident u, which stays untouched
+    bool stage_swap = false;
+    // one caller at a time per context (recursive: entry points call each other)
+    std::recursive_mutex call_mu;
     // small-grid path (gs_cluster.cu): one 16-CTA cluster runs whole gs_run calls
     int64_t cl_slice = 0, cl_halo = 0;
     size_t cl_smem = 0;
@@ -167,10 +176,34 @@ struct gs_ctx {
 namespace {
 
 gs_status fail(gs_ctx* c, gs_status code, const std::string& msg) {
-    if (c) c->err = msg;
-    else g_create_error = msg;
+    if (c) {
+        c->err = msg;
+        t_err = msg;
+        t_err_ctx = c;
+    } else {
+        g_create_error = msg;
+    }
     return code;
 }
+
+// Serialise the calls on one context (the reference's operators are safe to share read-only
+// across threads, SPEC.md: a context serialises instead of racing on its scratch buffers).
+#define GS_LOCK(c)                                     \
+    std::unique_lock<std::recursive_mutex> gs_lock_;   \
+    if (c) gs_lock_ = std::unique_lock<std::recursive_mutex>((c)->call_mu)
+
+// All members' locks, in address order (no lock-order inversion between two ensemble calls).
+struct MultiLock {
+    std::vector<std::unique_lock<std::recursive_mutex>> locks;
+    MultiLock(gs_ctx* const* ctxs, int n) {
+        std::vector<gs_ctx*> v;
+        for (int i = 0; ctxs && i < n; ++i)
+            if (ctxs[i]) v.push_back(ctxs[i]);
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        for (gs_ctx* c : v) locks.emplace_back(c->call_mu);
+    }
+};
 
 gs_status cuda_fail(gs_ctx* c, cudaError_t e, const char* where) {
     return fail(c, GS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -429,7 +462,7 @@ gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps
     GS_CUDA(c, cudaMemsetAsync(c->ctrl.p, 0, fresh_ctrl ? sizeof(gs::Ctrl) : offsetof(gs::Ctrl, last_terms),
                                c->stream));
     if (c->stage_in)
-        GS_CUDA(c, cudaMemcpyAsync(c->u.p, c->stage_in, sizeof(double) * static_cast<size_t>(c->n),
+        GS_CUDA(c, cudaMemcpyAsync(c->stage_swap ? c->out.p : c->u.p, c->stage_in, sizeof(double) * static_cast<size_t>(c->n),
                                    cudaMemcpyHostToDevice, c->stream));
     if (metrics) GS_CUDA(c, c->metrics.alloc(sizeof(double) * 4 * (n_steps + 1)));
     if (infos) {
@@ -484,6 +517,15 @@ gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps
     p.seq_counts = c->seq_counts.as<int>();
     DevBuf* bufs[gs::kNumBufs] = {&c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out};
     for (int b = 0; b < gs::kNumBufs; ++b) p.buf[b] = bufs[b]->as<double>();
+    if (c->stage_swap) {  // the state is the staging (`out`) buffer: pointer and TMA maps
+        p.buf[gs::kBufU] = c->out.as<double>();
+        if (p.use_tma) {
+            p.xmap[gs::kBufU] = c->xmap[gs::kBufOut];
+            p.omap[gs::kBufU] = c->omap[gs::kBufOut];
+            p.x2map[gs::kBufU] = c->x2map[gs::kBufOut];
+            p.x3map[gs::kBufU] = c->x3map[gs::kBufOut];
+        }
+    }
     p.trace = nullptr;
     p.trace_cap = 0;
     if (c->trace_cap > 0) {
@@ -575,7 +617,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
         cp.tol = p.tol;
         cp.anorm = c->anorm;
         std::copy(p.rtab, p.rtab + gs::kMaxDegree + 1, cp.rtab);
-        cp.u = c->u.as<double>();
+        cp.u = p.buf[gs::kBufU];
         cp.metrics = p.metrics;
         cp.infos = p.infos;
         cp.ctrl = p.ctrl;
@@ -669,7 +711,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
         }
     }
     if (c->stage_out)
-        GS_CUDA(c, cudaMemcpyAsync(c->stage_out, c->u.p, sizeof(double) * static_cast<size_t>(c->n),
+        GS_CUDA(c, cudaMemcpyAsync(c->stage_out, p.buf[gs::kBufU], sizeof(double) * static_cast<size_t>(c->n),
                                    cudaMemcpyDeviceToHost, c->stream));
     gs::Ctrl ctrl{};
     GS_CUDA(c, cudaMemcpyAsync(&ctrl, c->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, c->stream));
@@ -1054,7 +1096,10 @@ void gs_destroy(gs_ctx* c) {
     delete c;
 }
 
-const char* gs_last_error(const gs_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+const char* gs_last_error(const gs_ctx* c) {
+    if (!c) return g_create_error.c_str();
+    return c == t_err_ctx ? t_err.c_str() : c->err.c_str();
+}
 
 int64_t gs_num_points(const gs_ctx* c) { return c ? c->n : 0; }
 
@@ -1062,6 +1107,7 @@ void* gs_stream(gs_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr;
 
 gs_status gs_set_intensity(gs_ctx* c, const uint8_t* stack, int w, int hgt, int slices, int t_air, int t_white,
                            int t_gray, double d_white, double d_gray) {
+    GS_LOCK(c);
     if (c && c->is_csr) return fail(c, GS_EINVAL, "operator is a generic CSR matrix (gs_create_csr)");
     if (!c || !stack) return fail(c, GS_EINVAL, "gs_set_intensity: null argument");
     if (slices < 1 || w < 1 || hgt < 1) return fail(c, GS_EDATA, "resample: degenerate stack");  // imaging.cpp:126-127
@@ -1085,6 +1131,7 @@ gs_status gs_set_intensity(gs_ctx* c, const uint8_t* stack, int w, int hgt, int 
 }
 
 gs_status gs_set_labels(gs_ctx* c, const uint8_t* labels, double d_white, double d_gray) {
+    GS_LOCK(c);
     if (c && c->is_csr) return fail(c, GS_EINVAL, "operator is a generic CSR matrix (gs_create_csr)");
     if (!c || !labels) return fail(c, GS_EINVAL, "gs_set_labels: null argument");
     for (int64_t v = 0; v < c->n; ++v)
@@ -1100,6 +1147,7 @@ gs_status gs_set_labels(gs_ctx* c, const uint8_t* labels, double d_white, double
 }
 
 gs_status gs_set_diffusion(gs_ctx* c, const double* d) {
+    GS_LOCK(c);
     if (c && c->is_csr) return fail(c, GS_EINVAL, "operator is a generic CSR matrix (gs_create_csr)");
     if (!c || !d) return fail(c, GS_EINVAL, "gs_set_diffusion: null argument");
     cudaSetDevice(c->device);
@@ -1135,6 +1183,7 @@ gs_status gs_set_diffusion(gs_ctx* c, const double* d) {
 }
 
 gs_status gs_get_labels(gs_ctx* c, uint8_t* labels) {
+    GS_LOCK(c);
     if (!c || !labels) return fail(c, GS_EINVAL, "gs_get_labels: null argument");
     if (!c->has_labels) return fail(c, GS_EINVAL, "gs_get_labels: operator was not built from material labels");
     cudaSetDevice(c->device);
@@ -1144,6 +1193,7 @@ gs_status gs_get_labels(gs_ctx* c, uint8_t* labels) {
 }
 
 gs_status gs_get_diffusion(gs_ctx* c, double* d) {
+    GS_LOCK(c);
     if (!c || !d) return fail(c, GS_EINVAL, "gs_get_diffusion: null argument");
     gs_status st = ensure_operator(c);
     if (st != GS_OK) return st;
@@ -1163,6 +1213,7 @@ gs_status gs_get_diffusion(gs_ctx* c, double* d) {
 }
 
 gs_status gs_one_norm(gs_ctx* c, double* out) {
+    GS_LOCK(c);
     if (!c || !out) return fail(c, GS_EINVAL, "gs_one_norm: null argument");
     gs_status st = ensure_operator(c);
     if (st != GS_OK) return st;
@@ -1171,6 +1222,7 @@ gs_status gs_one_norm(gs_ctx* c, double* out) {
 }
 
 gs_status gs_apply(gs_ctx* c, const double* x, double* y) {
+    GS_LOCK(c);
     if (!c || !x || !y) return fail(c, GS_EINVAL, "gs_apply: null argument");
     gs_status st = ensure_operator(c);
     if (st != GS_OK) return st;
@@ -1188,6 +1240,7 @@ gs_status gs_apply(gs_ctx* c, const double* x, double* y) {
 }
 
 gs_status gs_set_state(gs_ctx* c, const double* u) {
+    GS_LOCK(c);
     if (!c || !u) return fail(c, GS_EINVAL, "gs_set_state: null argument");
     cudaSetDevice(c->device);
     GS_CUDA(c, cudaMemcpyAsync(c->u.p, u, sizeof(double) * static_cast<size_t>(c->n), cudaMemcpyHostToDevice,
@@ -1197,6 +1250,7 @@ gs_status gs_set_state(gs_ctx* c, const double* u) {
 }
 
 gs_status gs_get_state(gs_ctx* c, double* u) {
+    GS_LOCK(c);
     if (!c || !u) return fail(c, GS_EINVAL, "gs_get_state: null argument");
     cudaSetDevice(c->device);
     GS_CUDA(c, cudaMemcpyAsync(u, c->u.p, sizeof(double) * static_cast<size_t>(c->n), cudaMemcpyDeviceToHost,
@@ -1243,6 +1297,7 @@ gs_status gs_select_params(double norm_tA, double tol, int* s, int* m) {
 
 static gs_status action(gs_ctx* c, int mode, double t, const double* b, double tol, double* out,
                         gs_step_info* info) {
+    GS_LOCK(c);
     const char* who = mode == gs::kModeExpmv ? "expmv" : "phi1v";
     if (!c || !b || !out) return fail(c, GS_EINVAL, std::string(who) + ": null argument");
     if (!tol_ok(tol)) return fail(c, GS_EINVAL, std::string(who) + ": tolerance must lie in (0, 1)");
@@ -1283,6 +1338,7 @@ gs_status gs_phi1v(gs_ctx* c, double t, const double* b, double tol, double* out
 
 gs_status gs_run(gs_ctx* c, int n_steps, double rho, double tau, double tol, const double origin[3],
                  const double seed_center[3], double front_threshold, gs_metrics* metrics, gs_step_info* infos) {
+    GS_LOCK(c);
     if (!c) return fail(c, GS_EINVAL, "run: null context");
     if (n_steps < 0) return fail(c, GS_EINVAL, "run: negative step count");
     if (!tol_ok(tol)) return fail(c, GS_EINVAL, "phi1v: tolerance must lie in (0, 1)");
@@ -1445,6 +1501,7 @@ gs_status ens_status(gs_ctx* const* ctxs, int n_members, const std::vector<gs::C
 gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const double* rhos, double tau, double tol,
                           const double* origins, const double* centers, double front_threshold, gs_metrics* metrics,
                           gs_step_info* infos, int groups) {
+    MultiLock lk(ctxs, n_members);
     EnsPlan plan;
     gs_status st0 = ens_prepare(ctxs, n_members, n_steps, rhos, tau, tol, origins, centers, front_threshold, metrics,
                                 infos, groups, plan);
@@ -1486,11 +1543,17 @@ gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const
 gs_status gs_step_ensemble_host(gs_ctx* const* ctxs, int n_members, const double* const* u_in, double* const* u_out,
                                 const double* rhos, double tau, double tol, gs_step_info* infos, int groups,
                                 int chunks) {
+    MultiLock lk(ctxs, n_members);
     if (!u_in || !u_out) return fail(ctxs ? ctxs[0] : nullptr, GS_EINVAL, "step_ensemble: null argument");
     for (int i = 0; ctxs && i < n_members; ++i)
         if (!u_in[i] || !u_out[i]) return fail(ctxs[0], GS_EINVAL, "step_ensemble: null member vector");
     EnsPlan plan;
+    // value semantics: every member steps its staging (`out`) buffer, its resident u untouched
+    for (int i = 0; ctxs && i < n_members; ++i)
+        if (ctxs[i]) ctxs[i]->stage_swap = true;
     gs_status st0 = ens_prepare(ctxs, n_members, 1, rhos, tau, tol, nullptr, nullptr, 0.1, nullptr, infos, groups, plan);
+    for (int i = 0; ctxs && i < n_members; ++i)
+        if (ctxs[i]) ctxs[i]->stage_swap = false;
     if (st0 != GS_OK) return st0;
     if (!plan.batched) {
         for (int i = 0; i < n_members; ++i) {
@@ -1520,7 +1583,7 @@ gs_status gs_step_ensemble_host(gs_ctx* const* ctxs, int n_members, const double
     for (int k = 0; k < chunks; ++k) {
         const int lo = k * n_members / chunks, hi = (k + 1) * n_members / chunks;
         for (int i = lo; i < hi; ++i)
-            GS_CUDA(c0, cudaMemcpyAsync(ctxs[i]->u.p, u_in[i], bytes * static_cast<size_t>(ctxs[i]->n),
+            GS_CUDA(c0, cudaMemcpyAsync(ctxs[i]->out.p, u_in[i], bytes * static_cast<size_t>(ctxs[i]->n),
                                         cudaMemcpyHostToDevice, c0->ens_h2d));
         GS_CUDA(c0, cudaEventRecord(c0->ens_events[2 * k], c0->ens_h2d));
         GS_CUDA(c0, cudaStreamWaitEvent(c0->stream, c0->ens_events[2 * k], 0));
@@ -1528,7 +1591,7 @@ gs_status gs_step_ensemble_host(gs_ctx* const* ctxs, int n_members, const double
         GS_CUDA(c0, cudaEventRecord(c0->ens_events[2 * k + 1], c0->stream));
         GS_CUDA(c0, cudaStreamWaitEvent(c0->ens_d2h, c0->ens_events[2 * k + 1], 0));
         for (int i = lo; i < hi; ++i)
-            GS_CUDA(c0, cudaMemcpyAsync(u_out[i], ctxs[i]->u.p, bytes * static_cast<size_t>(ctxs[i]->n),
+            GS_CUDA(c0, cudaMemcpyAsync(u_out[i], ctxs[i]->out.p, bytes * static_cast<size_t>(ctxs[i]->n),
                                         cudaMemcpyDeviceToHost, c0->ens_d2h));
     }
     std::vector<gs::Ctrl> ctrl(static_cast<size_t>(n_members));
@@ -1551,16 +1614,20 @@ gs_status gs_step_host(gs_ctx* c, const double* u, double rho, double tau, doubl
                        gs_step_info* info) {
     if (!c || !u || !out) return fail(c, GS_EINVAL, "gs_step_host: null argument");
     // u in, one step, u' out on the context's stream with a single synchronisation
+    GS_LOCK(c);
     c->stage_in = u;
     c->stage_out = out;
+    c->stage_swap = true;
     const gs_status st = gs_step(c, rho, tau, tol, info);
     c->stage_in = nullptr;
     c->stage_out = nullptr;
+    c->stage_swap = false;
     return st;
 }
 
 gs_status gs_seed_initial(gs_ctx* c, const double origin[3], double amplitude, double width, const double center[3],
                           int mask, double* u) {
+    GS_LOCK(c);
     if (!c || !u || !center) return fail(c, GS_EINVAL, "seed_initial: null argument");
     const double o[3] = {origin ? origin[0] : 0.0, origin ? origin[1] : 0.0, origin ? origin[2] : 0.0};
     // Grid::contains (grid.hpp:43-50)
@@ -1621,12 +1688,14 @@ gs_status gs_seed_initial(gs_ctx* c, const double origin[3], double amplitude, d
 }
 
 gs_status gs_set_kernel_timing(gs_ctx* c, int enable) {
+    GS_LOCK(c);
     if (!c) return fail(c, GS_EINVAL, "gs_set_kernel_timing: null context");
     c->ktime = enable != 0;
     return GS_OK;
 }
 
 gs_status gs_get_kernel_times(gs_ctx* c, double ms[4], int launches[4]) {
+    GS_LOCK(c);
     if (!c || !ms || !launches) return fail(c, GS_EINVAL, "gs_get_kernel_times: null argument");
     for (int k = 0; k < 4; ++k) {
         ms[k] = c->kms[k];
@@ -1636,12 +1705,14 @@ gs_status gs_get_kernel_times(gs_ctx* c, double ms[4], int launches[4]) {
 }
 
 gs_status gs_set_trace(gs_ctx* c, int capacity) {
+    GS_LOCK(c);
     if (!c || capacity < 0) return fail(c, GS_EINVAL, "gs_set_trace: bad argument");
     c->trace_cap = capacity;
     return GS_OK;
 }
 
 gs_status gs_get_trace(gs_ctx* c, uint64_t* pairs, int capacity, int* count) {
+    GS_LOCK(c);
     if (!c || !pairs || !count) return fail(c, GS_EINVAL, "gs_get_trace: null argument");
     int n = 0;
     const int have = static_cast<int>(c->trace_host.size() / 2);
@@ -1655,6 +1726,7 @@ gs_status gs_get_trace(gs_ctx* c, uint64_t* pairs, int capacity, int* count) {
 }
 
 gs_status gs_snapshot_vtk(gs_ctx* c, const char* path, const double origin[3], const uint8_t* labels) {
+    GS_LOCK(c);
     if (!c || !path || !origin) return fail(c, GS_EINVAL, "gs_snapshot_vtk: null argument");
     cudaSetDevice(c->device);
     // open now so an unwritable path fails at this snapshot, as write_vtk does (vtk.cpp:66-68)
@@ -1736,6 +1808,7 @@ gs_status gs_snapshot_flush(gs_ctx* c) {
 }
 
 gs_status gs_matter_fractions(gs_ctx* c, double* white, double* gray) {
+    GS_LOCK(c);
     if (!c || !white || !gray) return fail(c, GS_EINVAL, "gs_matter_fractions: null argument");
     if (!c->has_labels) return fail(c, GS_EINVAL, "gs_matter_fractions: operator was not built from material labels");
     cudaSetDevice(c->device);

@@ -116,24 +116,40 @@ __device__ __forceinline__ void block_to_mbox(ClusterShared& cs, int par, double
 // way, so all CTAs hold the same value.  A list longer than kClItemCap is walked element by
 // element over DSMEM, followed by one more barrier (uniform: every CTA sees the same counts)
 // before anyone overwrites B.
-constexpr int kClItemCap = 32;
 constexpr int kClEPT = 8;  // elements per thread: slices of up to kCT * 8 voxels
-constexpr int kClAll = kClusterCTAs * kClItemCap + 8;  // the gathered sequence (+ walk padding)
-struct ClusterSeq {
+struct ClusterSeq {        // static shared memory
     SeqSmem sm;
     seq::Item own[kClItemCap];
-    int kind[kClAll], B[kClAll];
-    uint64_t d0[kClAll], d1[kClAll], lo[kClAll], hi[kClAll];
-    longlong2 pos[kClAll];
     int count, pref[kClusterCTAs + 1];
     int walked;  // this CTA's walk read remote B (a fallback)
     unsigned flags;
     double result, prefix;
 };
+// The gathered sequence, staged for seq_walk_batch, in dynamic shared memory over F0..T1
+// (cluster_b_offset keeps kClGatherDoubles there).
+struct ClusterGather {
+    int* kind;
+    int* B;
+    uint64_t *d0, *d1, *lo, *hi;
+    longlong2* pos;
+    __device__ explicit ClusterGather(void* base) {
+        unsigned char* b = static_cast<unsigned char*>(base);
+        pos = reinterpret_cast<longlong2*>(b);
+        d0 = reinterpret_cast<uint64_t*>(b + 16 * kClAll);
+        d1 = d0 + kClAll;
+        lo = d1 + kClAll;
+        hi = lo + kClAll;
+        kind = reinterpret_cast<int*>(hi + kClAll);
+        B = kind + kClAll;
+    }
+};
+static_assert(56 * kClAll <= 8 * kClGatherDoubles, "gather layout");
 
-__device__ double cl_exact_sum(cg::cluster_group& cl, ClusterShared& cs, ClusterSeq& q, int par, const double* B,
-                               int64_t len, int64_t lo, int64_t S, int64_t N, int rank, int nranks, bool debug) {
+__device__ double cl_exact_sum(cg::cluster_group& cl, ClusterShared& cs, ClusterSeq& q, void* gather, int par,
+                               const double* B, int64_t len, int64_t lo, int64_t S, int64_t N, int rank, int nranks,
+                               bool debug) {
     const int tid = threadIdx.x;
+    const ClusterGather g(gather);
     // approximate sum before this slice; this slice's non-finite flags
     if (tid < 32) {
         double v = tid < rank ? *cl.map_shared_rank(&cs.mbox[par][0], tid) : 0.0;
@@ -189,17 +205,17 @@ __device__ double cl_exact_sum(cg::cluster_group& cl, ClusterShared& cs, Cluster
             } else {
                 it = cl.map_shared_rank(q.own, r)[k];
             }
-            q.kind[at] = it.kind;
-            q.B[at] = it.B;
-            seq_stage(it.kind, it.B, it.d0, it.d1, q.d0[at], q.d1[at], q.lo[at], q.hi[at]);
-            q.pos[at] = make_longlong2(it.start, it.len);
+            g.kind[at] = it.kind;
+            g.B[at] = it.B;
+            seq_stage(it.kind, it.B, it.d0, it.d1, g.d0[at], g.d1[at], g.lo[at], g.hi[at]);
+            g.pos[at] = make_longlong2(it.start, it.len);
         }
         const int total = q.pref[nranks];
         if (tid < 8) {  // padding of the walk's last batch: zero runs
-            q.kind[total + tid] = seq::kEmpty;
-            q.B[total + tid] = 0;
-            q.d0[total + tid] = q.d1[total + tid] = q.lo[total + tid] = 0ull;
-            q.hi[total + tid] = ~0ull;
+            g.kind[total + tid] = seq::kEmpty;
+            g.B[total + tid] = 0;
+            g.d0[total + tid] = g.d1[total + tid] = g.lo[total + tid] = 0ull;
+            g.hi[total + tid] = ~0ull;
         }
     }
     __syncthreads();
@@ -212,7 +228,7 @@ __device__ double cl_exact_sum(cg::cluster_group& cl, ClusterShared& cs, Cluster
         } else if (q.flags & seq::kHasInf) {
             bits = 0x7ff0000000000000ull;
         } else {
-            fin = seq_walk_batch(bits, q.kind, q.B, q.d0, q.d1, q.lo, q.hi, q.pos, q.pref[nranks],
+            fin = seq_walk_batch(bits, g.kind, g.B, g.d0, g.d1, g.lo, g.hi, g.pos, q.pref[nranks],
                                  [&](double a, int64_t l, int64_t h) {
                                      walked = true;
                                      for (int64_t i = l; i < h; ++i) {
@@ -252,7 +268,7 @@ __global__ void __launch_bounds__(kCT, 1) cluster_run_kernel(const __grid_consta
     // shared layout: U, F0, F1, T0, T1 haloed, then B, then labels
     double* HV[5];
     for (int k = 0; k < 5; ++k) HV[k] = reinterpret_cast<double*>(dyn) + k * HS;
-    double* const B = reinterpret_cast<double*>(dyn) + 5 * HS;
+    double* const B = reinterpret_cast<double*>(dyn) + cluster_b_offset(S, H);
     uint8_t* const L = reinterpret_cast<uint8_t*>(B + S);
     uint8_t* const M = L + (S + 15) / 16 * 16;
     enum { kU = 0, kF0 = 1, kF1 = 2, kT0 = 3, kT1 = 4 };
@@ -355,7 +371,7 @@ __global__ void __launch_bounds__(kCT, 1) cluster_run_kernel(const __grid_consta
         double bnorm;  // expact.cpp:110: the reference's sequential sum (or a rank-order tree sum, A/B)
         if (p.seq_exact) {
             const long long tc = clock64();
-            bnorm = cl_exact_sum(cl, cs, csq, par, B, len, lo, S, N, rank, nranks, p.seq_exact > 1);
+            bnorm = cl_exact_sum(cl, cs, csq, HV[kF0], par, B, len, lo, S, N, rank, nranks, p.seq_exact > 1);
             if (p.seq_exact > 1 && leader)
                 printf("cluster step %d: bnorm exact sum %lld cycles, %d items\n", step, clock64() - tc,
                        csq.pref[nranks]);
@@ -406,7 +422,7 @@ __global__ void __launch_bounds__(kCT, 1) cluster_run_kernel(const __grid_consta
             double coln = cs.bcast[0];
             if (p.seq_exact && (p.infos || !seq::coln_settles(t, p.anorm, coln, N, p.rtab, kMaxDegree))) {
                 if (p.seq_exact > 1 && leader) printf("cluster step %d: coln exact\n", step);
-                coln = cl_exact_sum(cl, cs, csq, par, B, len, lo, S, N, rank, nranks, p.seq_exact > 1);
+                coln = cl_exact_sum(cl, cs, csq, HV[kF0], par, B, len, lo, S, N, rank, nranks, p.seq_exact > 1);
             }
             par ^= 1;
             const double norm_tA = __dmul_rn(fabs(t), nan_dropping_max(p.anorm, coln));

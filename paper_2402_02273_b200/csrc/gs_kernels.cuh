@@ -249,10 +249,22 @@ struct ClusterParams {
     Ctrl* ctrl;
     double origin[3], center[3], h, front_threshold;
 };
+// The exact sums' gathered item lists (gs_cluster.cu) alias the four Taylor vectors F0..T1,
+// idle while ||b||_1 and the column sum are formed: 16 ranks x 32 items + 8 padding, 56 bytes
+// each (kind, B, d0, d1, lo, hi, start/len).
+constexpr int kClItemCap = 32;
+constexpr int kClAll = kClusterCTAs * kClItemCap + 8;
+constexpr int64_t kClGatherDoubles = (static_cast<int64_t>(kClAll) * 56 + 7) / 8;
+// Offset (doubles) of b/gamma: U, then F0, F1, T0, T1 -- padded to hold the gather.
+__host__ __device__ inline int64_t cluster_b_offset(int64_t slice, int64_t halo) {
+    const int64_t hs = slice + 2 * halo;
+    return hs + (4 * hs > kClGatherDoubles ? 4 * hs : kClGatherDoubles);
+}
 // Dynamic shared memory of cluster_run_kernel per CTA (5 haloed vectors, b/gamma, labels,
 // neighbour masks).
 inline size_t cluster_smem_bytes(int64_t slice, int64_t halo) {
-    return static_cast<size_t>(5 * (slice + 2 * halo) + slice) * 8 + 2 * ((static_cast<size_t>(slice) + 15) / 16) * 16;
+    return static_cast<size_t>(cluster_b_offset(slice, halo) + slice) * 8 +
+           2 * ((static_cast<size_t>(slice) + 15) / 16) * 16;
 }
 __global__ void cluster_run_kernel(const __grid_constant__ ClusterParams p);
 

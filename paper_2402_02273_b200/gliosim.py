@@ -432,8 +432,13 @@ def phi1v(t: float, a: StencilOperator, b, tol: float, info: bool = False):
 
 
 def step(a: StencilOperator, u, rho: float, tau: float, tol: float, info: bool = False):
-    """integrator.cpp:52-63 with value semantics (overwrites the operator's resident state)."""
-    u = _vec(a, u, "phi1v")
+    """integrator.cpp:52-63 with value semantics: the step runs on a staging buffer, so the
+    operator's resident state (run_resident / set_state) is left untouched.  A length mismatch
+    raises what the reference's first use of u raises, SparseOperator::apply's message
+    (sparse.cpp:44-46 via integrator.cpp:55)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    if u.size != a.dim():
+        raise ValueError(f"SparseOperator::apply: vector length {u.size} != dim {a.dim()}")
     out = np.empty_like(u)
     inf = N.GsStepInfo()
     a._check(a.lib.gs_step_host(a.ctx, u, rho, tau, tol, out, C.byref(inf)))
@@ -497,7 +502,18 @@ def step_ensemble_host(ops, us, rhos, tau: float, tol: float, outs=None, infos: 
     for op, u in zip(ops, ins):
         if u.size != op.grid.num_points():
             raise ValueError("step: state length does not match the grid")
-    outs = [np.empty_like(u) for u in ins] if outs is None else list(outs)
+    if outs is None:
+        outs = [np.empty_like(u) for u in ins]
+    else:
+        outs = list(outs)
+        if len(outs) != n:
+            raise ValueError("step_ensemble: one output vector per member")
+        for op, o in zip(ops, outs):
+            # the library writes n doubles through each pointer: exact dtype, size and layout
+            if (not isinstance(o, np.ndarray) or o.dtype != np.float64 or not o.flags.c_contiguous
+                    or not o.flags.writeable or o.size != op.grid.num_points()):
+                raise ValueError("step_ensemble: each output must be a writeable C-contiguous float64 array "
+                                 "with one value per grid point")
     pin = (C.c_void_p * n)(*[u.ctypes.data for u in ins])
     pout = (C.c_void_p * n)(*[o.ctypes.data for o in outs])
     ctxs = (C.c_void_p * n)(*[o.ctx for o in ops])
@@ -511,9 +527,10 @@ def step_ensemble_host(ops, us, rhos, tau: float, tol: float, outs=None, infos: 
 
 def run(cfg: SimConfig, a: StencilOperator, u0, snapshot=None, on_range=None, on_step=None,
         with_infos: bool = False, _vtk=None) -> RunResult:
-    """integrator.cpp:91-138: the time loop runs on the GPU as one launch per segment
-    between snapshots; metrics are computed on the device at every node, then the
-    hooks fire in order with the reference's arguments.
+    """integrator.cpp:91-138: the time loop runs on the GPU as one launch sequence per segment
+    between snapshots (per step when a StepWatcher or RangeWarning is given, so they fire
+    live); metrics are computed on the device at every node, then the hooks fire in order
+    with the reference's arguments.
 
     _vtk = (out_dir, labels or None) is run_to_directory's sink (pipeline.cpp:39-45):
     snapshot_NNNN.vtk files written asynchronously by the native library."""
@@ -525,10 +542,17 @@ def run(cfg: SimConfig, a: StencilOperator, u0, snapshot=None, on_range=None, on
     res = RunResult()
     a.set_state(u0)
     tau = cfg.tau()
-    # snapshot nodes: 0, every snapshot_every, and the last (integrator.cpp:112, :135-136)
     sinks = snapshot is not None or _vtk is not None
-    cuts = [n for n in range(1, cfg.num_steps + 1) if n % cfg.snapshot_every == 0 or n == cfg.num_steps] \
-        if sinks else [cfg.num_steps]
+    # segment ends: snapshot nodes (0, every snapshot_every, the last; integrator.cpp:112,
+    # :135-136); with a StepWatcher / RangeWarning every step, so the hooks fire live, after
+    # each step as in the reference's loop (integrator.cpp:128-131) -- a failing step then
+    # leaves the hooks of every completed step fired
+    if on_step or on_range:
+        cuts = list(range(1, cfg.num_steps + 1))
+    elif sinks:
+        cuts = [n for n in range(1, cfg.num_steps + 1) if n % cfg.snapshot_every == 0 or n == cfg.num_steps]
+    else:
+        cuts = [cfg.num_steps]
 
     def emit(n):
         tic = time.perf_counter()
@@ -544,7 +568,9 @@ def run(cfg: SimConfig, a: StencilOperator, u0, snapshot=None, on_range=None, on
     for cut in cuts:
         k = cut - done
         tic = time.perf_counter()
-        m, inf = a.run_resident(k, cfg.rho, tau, cfg.exp_tol, cfg.origin, cfg.seed_center, cfg.front_threshold,
+        # metrics on the operator's grid (compute_metrics uses grid.point of the DiffusionField's
+        # grid, integrator.cpp:65-89), as seeding and the snapshots do
+        m, inf = a.run_resident(k, cfg.rho, tau, cfg.exp_tol, grid.origin, cfg.seed_center, cfg.front_threshold,
                                 metrics=True, infos=with_infos)
         res.timings.step_seconds += time.perf_counter() - tic
         first = 0 if done == 0 else 1
@@ -563,7 +589,7 @@ def run(cfg: SimConfig, a: StencilOperator, u0, snapshot=None, on_range=None, on
         if with_infos:
             res.infos.extend(inf[q].as_dict() for q in range(k))
         done = cut
-        if sinks:
+        if sinks and (cut % cfg.snapshot_every == 0 or cut == cfg.num_steps):
             emit(cut)
     if _vtk is not None:
         tic = time.perf_counter()

@@ -6,12 +6,15 @@
 // Same SimConfig / DiffusionField / u0 objects go to gliosim::run (reference, CPU) and to
 // gliosim_b200::run (GPU); the final state must agree to a relative L2 of 1e-8 and the
 // order-free metrics (max, min, radius) to 1e-12; step() / phi1v() / expmv() / apply() too.
+// With the reference's sequential sums reproduced on the device (gs_seqsum.cuh) the states are
+// in fact bit-identical, and that is gated as well.
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
 #include <fstream>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gliosim/config.hpp"
@@ -75,6 +78,7 @@ int main() {
         cfg, d, u0, 1, [&](int n, double, const std::vector<double>&) { snaps_gpu.push_back(n); }, {},
         [&](const gliosim_b200::StepMetrics& m) { steps_gpu.push_back(m.step); });
     gate(rel_l2(gpu.u, ref.u) <= 1e-8, "run: final u rel L2", rel_l2(gpu.u, ref.u));
+    gate(gpu.u == ref.u, "run: final u bitwise", 0.0);
     gate(snaps_ref == snaps_gpu, "run: snapshot cadence", 0.0);
     gate(static_cast<int>(steps_gpu.size()) == cfg.num_steps, "run: step watcher calls", 0.0);
     double worst = 0.0;
@@ -93,9 +97,11 @@ int main() {
     const auto s_ref = gliosim::step(a, u0, cfg.rho, cfg.tau(), cfg.exp_tol);
     const auto s_gpu = gliosim_b200::step(ga, u0, cfg.rho, cfg.tau(), cfg.exp_tol);
     gate(rel_l2(s_gpu, s_ref) <= 1e-10, "step rel L2", rel_l2(s_gpu, s_ref));
+    gate(s_gpu == s_ref, "step bitwise", 0.0);
     const auto p_ref = gliosim::phi1v(40.0, a, u0, 1e-10);
     const auto p_gpu = gliosim_b200::phi1v(40.0, ga, u0, 1e-10);
     gate(rel_l2(p_gpu, p_ref) <= 1e-12, "phi1v rel L2", rel_l2(p_gpu, p_ref));
+    gate(p_gpu == p_ref, "phi1v bitwise", 0.0);
     const auto e_ref = gliosim::expmv(40.0, a, u0, 1e-10);
     const auto e_gpu = gliosim_b200::expmv(40.0, ga, u0, 1e-10);
     gate(e_gpu == e_ref, "expmv bitwise", rel_l2(e_gpu, e_ref));
@@ -110,6 +116,38 @@ int main() {
         threw = true;
     }
     gate(threw, "phi1v length mismatch -> std::invalid_argument", 0.0);
+    // step with a wrong length: the reference throws from SparseOperator::apply (sparse.cpp:44-46)
+    std::string msg_ref, msg_gpu;
+    try {
+        gliosim::step(a, std::vector<double>(5, 0.5), cfg.rho, cfg.tau(), cfg.exp_tol);
+    } catch (const std::invalid_argument& e) {
+        msg_ref = e.what();
+    }
+    try {
+        gliosim_b200::step(ga, std::vector<double>(5, 0.5), cfg.rho, cfg.tau(), cfg.exp_tol);
+    } catch (const std::invalid_argument& e) {
+        msg_gpu = e.what();
+    }
+    std::printf("  step length mismatch: reference \"%s\", drop-in \"%s\"\n", msg_ref.c_str(), msg_gpu.c_str());
+    gate(!msg_ref.empty() && msg_ref == msg_gpu, "step length mismatch: same exception and message", 0.0);
+    // the reference's operators are shareable read-only: step() from two threads on one operator
+    {
+        std::vector<std::vector<double>> ins, outs(6), serial;
+        for (int k = 0; k < 6; ++k) {
+            std::vector<double> v = u0;
+            for (size_t i = 0; i < v.size(); ++i) v[i] = std::fmod(v[i] + 0.37 * k + 1e-3 * static_cast<double>(i % 97), 1.0);
+            ins.push_back(v);
+            serial.push_back(gliosim::step(a, v, cfg.rho, cfg.tau(), cfg.exp_tol));
+        }
+        auto work = [&](int first) {
+            for (int r = 0; r < 3; ++r)
+                for (int k = first; k < 6; k += 2) outs[k] = gliosim_b200::step(ga, ins[k], cfg.rho, cfg.tau(), cfg.exp_tol);
+        };
+        std::thread t0(work, 0), t1(work, 1);
+        t0.join();
+        t1.join();
+        gate(outs == serial, "step from two threads on one operator == the reference's serial steps", 0.0);
+    }
 
     // run_to_directory (pipeline.hpp:18-24) with labels: the same files, read back by the
     // reference's own reader; the GPU's files re-written by the reference's writer are

@@ -18,6 +18,8 @@ def test_reference_arm_json_line(ref):
     assert line["metric"].startswith("expEuler steps/s")
     assert line["unit"] == "steps/s" and line["higher_is_better"] is True
     assert line["steps"] == 2 and line["warmup"] == 1 and line["n_gpus"] == 1
+    assert len(line["step_seconds"]) == 2 and abs(line["ms_per_step"] / 1e3 - sum(line["step_seconds"]) / 2) < 1e-9
+    assert "full 32x32x32 grid" in line["cpu_baseline"]["sample"]
     assert line["value"] > 0
     cb = line["cpu_baseline"]
     assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == line["value"]

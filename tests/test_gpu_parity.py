@@ -304,7 +304,7 @@ def test_multi_step_run_loose_tol_vs_oracle(G, port, path, tol, monkeypatch):
     max slots across the steps of one launch sequence: the Taylor kernel leaves its last
     round's maxima in one slot and the update kernel zeroes all three before the next step."""
     sweep_path_env(path, monkeypatch)
-    shape = (48, 32, 20) if path != "cluster" else (24, 16, 12)
+    shape = (48, 32, 20) if path != "cluster" else (24, 16, 16)
     rng = np.random.default_rng(17)
     n = int(np.prod(shape))
     d = np.array([0.0, 0.13, 0.013, 0.05])[rng.integers(0, 4, n)]
@@ -315,8 +315,7 @@ def test_multi_step_run_loose_tol_vs_oracle(G, port, path, tol, monkeypatch):
     u0[d == 0.0] = 0.0
     k = 4
     with G.assemble_diffusion(G.Grid(*shape, h=h), d) as op:
-        if path == "cluster" and not op.uses_cluster():
-            pytest.skip("grid too large (or too thin) for the single-cluster path")
+        assert op.uses_cluster() == (path == "cluster")
         op.set_state(u0)
         _, inf = op.run_resident(k, 0.1, 33.5, tol, metrics=False, infos=True)
         got = op.get_state()
@@ -354,8 +353,15 @@ def sweep_path_env(path, monkeypatch):
         monkeypatch.setenv("GS_EXACT_MAX", "2")
 
 
-@pytest.mark.parametrize("shape", TMA_SHAPES)
-@pytest.mark.parametrize("path", SWEEP_PATHS)
+# Shapes the single-cluster path takes (<= 40 K voxels, a slice of N/16 voxels at least one
+# plane -- one row in 2-D): awkward x extents (not a multiple of 16), 2-D, partial planes.
+CLUSTER_SHAPES = [(32, 32, 32), (16, 16, 16), (64, 48, 1), (24, 17, 16), (33, 7, 18), (20, 12, 40), (80, 16, 24),
+                  (40, 30, 24), (200, 190, 1)]
+SWEEP_CASES = [("cluster", s) for s in CLUSTER_SHAPES] + [(p, s) for p in SWEEP_PATHS if p != "cluster"
+                                                           for s in TMA_SHAPES]
+
+
+@pytest.mark.parametrize("path,shape", SWEEP_CASES)
 def test_sweep_paths_vs_oracle(G, port, shape, path, monkeypatch):
     """Every sweep implementation (sweep_path_env) -- bitwise against the oracle."""
     sweep_path_env(path, monkeypatch)
@@ -368,8 +374,7 @@ def test_sweep_paths_vs_oracle(G, port, shape, path, monkeypatch):
     x = rng.uniform(-1, 1, n)
     u = rng.uniform(0, 1, n)
     with G.assemble_diffusion(G.Grid(*shape, h=h), d) as op:
-        if path == "cluster" and not op.uses_cluster():
-            pytest.skip("grid too large (or too thin) for the single-cluster path")
+        assert op.uses_cluster() == (path == "cluster"), "shape does not take the path under test"
         assert np.array_equal(op.apply(x), port.apply(op_o, x))
         got, info = G.step(op, u, 0.1, 33.5, 1e-9, info=True)
         want, log = port.step(op_o, u, 0.1, 33.5, 1e-9, bnorm=info.bnorm, coln=info.coln)
@@ -388,7 +393,7 @@ def test_non_finite_inputs_vs_oracle(G, port, path, monkeypatch):
     norm infinite: numeric_error in both (expact.cpp:90-91).  On the two-term TMA path both
     cases go through the exact-maxima fallback (a non-finite key leaves the bounds open)."""
     sweep_path_env(path, monkeypatch)
-    shape = (48, 32, 12) if path != "cluster" else (24, 16, 12)
+    shape = (48, 32, 12) if path != "cluster" else (24, 16, 16)
     rng = np.random.default_rng(5)
     n = int(np.prod(shape))
     d = np.array([0.0, 0.13, 0.013, 0.05])[rng.integers(0, 4, n)]
@@ -396,8 +401,7 @@ def test_non_finite_inputs_vs_oracle(G, port, path, monkeypatch):
     x = rng.uniform(-1, 1, n)
     x[n // 2 + 7] = np.nan
     with G.assemble_diffusion(G.Grid(*shape, h=2.0), d) as op:
-        if path == "cluster" and not op.uses_cluster():
-            pytest.skip("grid too large (or too thin) for the single-cluster path")
+        assert op.uses_cluster() == (path == "cluster")
         got = G.expmv(2.0, op, x, 1e-10)
         want, _ = port.expmv(2.0, op_o, x, 1e-10)
         assert np.isnan(got).any() and np.isnan(got).sum() < n
