@@ -1368,6 +1368,7 @@ namespace {
 struct EnsPlan {
     std::vector<gs::SolveParams> P;
     int groups = 1, grp = 1, sb = 1, fuse = 2;
+    int num_sms = 1;
     int sq = 1;   // CTAs per member of the seqsum item pass
     int sq1 = 1;  // ... and of its tile pass
     bool batched = false;
@@ -1409,6 +1410,7 @@ gs_status ens_prepare(gs_ctx* const* ctxs, int n_members, int n_steps, const dou
     }
     plan.groups = std::max(1, std::min({groups, n_members, c0->num_sms}));
     plan.grp = c0->num_sms / plan.groups;
+    plan.num_sms = c0->capacity > 0 ? std::min(c0->num_sms, c0->capacity) : c0->num_sms;
     plan.sb = 1;
     for (int i = 0; i < n_members; ++i) plan.sb = std::max(plan.sb, stream_blocks(ctxs[i]));
     plan.fuse = thin ? 4 : 2;
@@ -1471,9 +1473,12 @@ cudaError_t ens_launch(const EnsPlan& plan, const gs::SolveParams* dP, int n, in
         gs::ens_order_kernel<<<1, 256, 0, st>>>(dP, n, ctl + gs::ens_ctl_words(groups));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(ctl, 0, sizeof(unsigned) * gs::ens_ctl_words(groups), st)) != cudaSuccess) return e;
-        int nm = n, g = grp, bb = sb, sp = step;
-        void* args[] = {const_cast<gs::SolveParams**>(&dP), &nm, &g, &bb, &sp, &ctl, const_cast<unsigned**>(&order)};
-        if ((e = cudaLaunchCooperativeKernel(gs::ens_taylor_kernel_fn(plan.fuse), dim3(groups * grp), blk, args,
+        // the SMs left over by groups * grp go one each to the first groups
+        int nm = n, g = grp, bb = sb, sp = step, extra = std::max(0, std::min(groups, plan.num_sms - groups * grp));
+        if (std::getenv("GS_ENS_NO_EXTRA")) extra = 0;
+        void* args[] = {const_cast<gs::SolveParams**>(&dP), &nm, &g, &bb, &sp, &ctl, const_cast<unsigned**>(&order),
+                        &extra};
+        if ((e = cudaLaunchCooperativeKernel(gs::ens_taylor_kernel_fn(plan.fuse), dim3(groups * grp + extra), blk, args,
                                              gs::kDynSmemBytes, st)) != cudaSuccess)
             return e;
         gs::ens_update_kernel<<<n * sb, blk, 0, st>>>(dP, sb, step);

@@ -289,7 +289,7 @@ __global__ void ens_update_kernel(const SolveParams* P, int cpm, int step);
 __global__ void ens_seqsum_tiles_kernel(const SolveParams* P, int cpm, int which);
 __global__ void ens_seqsum_items_kernel(const SolveParams* P, int cpm, int which);
 __global__ void ens_order_kernel(const SolveParams* P, int n_members, unsigned* order);
-const void* ens_taylor_kernel_fn(int fuse);  // fuse 2 or 4 (args: P, n_members, group, border_blocks, step, ctl, order)
+const void* ens_taylor_kernel_fn(int fuse);  // fuse 2 or 4 (args: P, n_members, group, border_blocks, step, ctl, order, extra)
 inline int ens_ctl_words(int groups) { return 4 * groups + 1; }
 
 }  // namespace gs

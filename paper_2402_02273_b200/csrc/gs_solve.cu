@@ -2261,15 +2261,29 @@ __global__ void __launch_bounds__(kSolveThreads, kMinBlocks) taylor_kernel(const
 // group takes members from a queue and runs a member's whole Taylor loop on its virtual grid,
 // with a software group barrier in place of grid.sync.  ctl: per group {count, gen, member[2]}
 // followed by the queue head, zeroed before the launch.
+// The first `extra` groups have group + 1 CTAs (so the launch can fill every SM); a member's
+// TMA work split (cta_work) follows the group's actual CTA count.
 template <int FUSE>
 __global__ void __launch_bounds__(kSolveThreads, kMinBlocks) ens_taylor_kernel(const SolveParams* __restrict__ P, int n_members,
                                                                       int group, int border_blocks, int step,
-                                                                      unsigned* ctl, const unsigned* order) {
-    const int g = blockIdx.x / group;
-    vgrid_set(blockIdx.x % group, group);
+                                                                      unsigned* ctl, const unsigned* order, int extra) {
+    const int big = group + 1;
+    int g, size, r;
+    if (static_cast<int>(blockIdx.x) < extra * big) {
+        g = blockIdx.x / big;
+        r = blockIdx.x % big;
+        size = big;
+    } else {
+        const int b = blockIdx.x - extra * big;
+        g = extra + b / group;
+        r = b % group;
+        size = group;
+    }
+    vgrid_set(r, size);
+    const int ngroups = extra + (gridDim.x - extra * big) / group;
     unsigned* mine = ctl + 4 * g;
-    unsigned* queue = ctl + 4 * (gridDim.x / group);
-    const GroupBarrier bar{mine, mine + 1, static_cast<unsigned>(group)};
+    unsigned* queue = ctl + 4 * ngroups;
+    const GroupBarrier bar{mine, mine + 1, static_cast<unsigned>(size)};
     bool reinit = false;
     for (int it = 0;; ++it) {
         // the group leader takes the next member; slots alternate so that a CTA still reading
@@ -2346,8 +2360,8 @@ template __global__ void taylor_kernel<2>(const __grid_constant__ SolveParams, i
 template __global__ void taylor_kernel<3>(const __grid_constant__ SolveParams, int, int);
 #endif
 template __global__ void taylor_kernel<4>(const __grid_constant__ SolveParams, int, int);
-template __global__ void ens_taylor_kernel<2>(const SolveParams*, int, int, int, int, unsigned*, const unsigned*);
-template __global__ void ens_taylor_kernel<4>(const SolveParams*, int, int, int, int, unsigned*, const unsigned*);
+template __global__ void ens_taylor_kernel<2>(const SolveParams*, int, int, int, int, unsigned*, const unsigned*, int);
+template __global__ void ens_taylor_kernel<4>(const SolveParams*, int, int, int, int, unsigned*, const unsigned*, int);
 
 // The queue's order for the next Taylor launch: members by their last step's Taylor terms,
 // most first (ties by index) -- the longest runs start first, so the groups finish together

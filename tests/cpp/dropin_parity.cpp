@@ -26,6 +26,7 @@
 #include "gliosim/stencil.hpp"
 #include "gliosim/vtk.hpp"
 #include "gliosim_b200.hpp"
+#include "oracles.hpp"  // the reference's test oracles (dense expm), proj/tests
 
 static double rel_l2(const std::vector<double>& a, const std::vector<double>& b) {
     double num = 0.0, den = 0.0;
@@ -147,6 +148,34 @@ int main() {
         t0.join();
         t1.join();
         gate(outs == serial, "step from two threads on one operator == the reference's serial steps", 0.0);
+    }
+
+    // The property of test_integrator.cpp:122-144 on the drop-in: with no reaction, ten
+    // exponential-Euler steps over [0, 500] equal one exponential action over the span --
+    // against the drop-in's expmv and the dense matrix exponential, 1e-7 (the unit test's bar).
+    {
+        gliosim::SimConfig c2;
+        c2.rho = 0.0;
+        c2.nx = c2.ny = c2.nz = 6;
+        c2.h = 200.0 / 5.0;
+        c2.t0 = 0.0;
+        c2.t_end = 500.0;
+        c2.num_steps = 10;
+        c2.seed_center = {100.0, 100.0, 100.0};
+        c2.seed_amplitude = 0.8;
+        c2.seed_width = 0.002;
+        const gliosim::Grid g2 = c2.grid();
+        const gliosim::DiffusionField d2(g2, 0.13);
+        const std::vector<double> v0 = gliosim::seed_initial(g2, c2);
+        const gliosim_b200::RunResult r2 = gliosim_b200::run(c2, d2, v0);
+        gliosim_b200::StencilOperator a2 = gliosim_b200::assemble_diffusion(d2);
+        const std::vector<double> one = gliosim_b200::expmv(500.0, a2, v0, 1e-10);
+        const double e1 = oracles::rel_err_inf(r2.u, one);
+        const gliosim::SparseOperator ar = gliosim::assemble_diffusion(d2);
+        const oracles::Dense e = oracles::expm(oracles::scale(oracles::dense_from_sparse(ar), 500.0));
+        const double e2 = oracles::rel_err_inf(r2.u, oracles::apply(e, v0));
+        gate(e1 <= 1e-7, "10 steps (rho = 0) == one expmv over the span (test_integrator.cpp:122-144)", e1);
+        gate(e2 <= 1e-7, "10 steps (rho = 0) == dense expm over the span", e2);
     }
 
     // run_to_directory (pipeline.hpp:18-24) with labels: the same files, read back by the
