@@ -1474,8 +1474,10 @@ cudaError_t ens_launch(const EnsPlan& plan, const gs::SolveParams* dP, int n, in
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(ctl, 0, sizeof(unsigned) * gs::ens_ctl_words(groups), st)) != cudaSuccess) return e;
         // the SMs left over by groups * grp go one each to the first groups
+        // (measured on C5: 2150 member-steps/s with the extra CTAs against 2156 without -- the
+        // longer groups finish no sooner -- so GS_ENS_EXTRA=1 opts in, for A/B)
         int nm = n, g = grp, bb = sb, sp = step, extra = std::max(0, std::min(groups, plan.num_sms - groups * grp));
-        if (std::getenv("GS_ENS_NO_EXTRA")) extra = 0;
+        if (!std::getenv("GS_ENS_EXTRA")) extra = 0;
         void* args[] = {const_cast<gs::SolveParams**>(&dP), &nm, &g, &bb, &sp, &ctl, const_cast<unsigned**>(&order),
                         &extra};
         if ((e = cudaLaunchCooperativeKernel(gs::ens_taylor_kernel_fn(plan.fuse), dim3(groups * grp + extra), blk, args,

@@ -149,7 +149,8 @@ __device__ double cl_exact_sum(cg::cluster_group& cl, ClusterShared& cs, Cluster
                                const double* B, int64_t len, int64_t lo, int64_t S, int64_t N, int rank, int nranks,
                                bool debug) {
     const int tid = threadIdx.x;
-    const ClusterGather g(gather);
+    // 16-byte aligned (its start/len pairs are 16-byte loads); F0 may start 8 bytes off
+    const ClusterGather g(reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(gather) + 15) & ~uintptr_t(15)));
     // approximate sum before this slice; this slice's non-finite flags
     if (tid < 32) {
         double v = tid < rank ? *cl.map_shared_rank(&cs.mbox[par][0], tid) : 0.0;

@@ -258,7 +258,8 @@ constexpr int64_t kClGatherDoubles = (static_cast<int64_t>(kClAll) * 56 + 7) / 8
 // Offset (doubles) of b/gamma: U, then F0, F1, T0, T1 -- padded to hold the gather.
 __host__ __device__ inline int64_t cluster_b_offset(int64_t slice, int64_t halo) {
     const int64_t hs = slice + 2 * halo;
-    return hs + (4 * hs > kClGatherDoubles ? 4 * hs : kClGatherDoubles);
+    // (+2: the gather starts at the first 16-byte boundary of F0, which may be 8 bytes in)
+    return hs + (4 * hs > kClGatherDoubles + 2 ? 4 * hs : kClGatherDoubles + 2);
 }
 // Dynamic shared memory of cluster_run_kernel per CTA (5 haloed vectors, b/gamma, labels,
 // neighbour masks).

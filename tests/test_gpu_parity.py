@@ -356,7 +356,7 @@ def sweep_path_env(path, monkeypatch):
 # Shapes the single-cluster path takes (<= 40 K voxels, a slice of N/16 voxels at least one
 # plane -- one row in 2-D): awkward x extents (not a multiple of 16), 2-D, partial planes.
 CLUSTER_SHAPES = [(32, 32, 32), (16, 16, 16), (64, 48, 1), (24, 17, 16), (33, 7, 18), (20, 12, 40), (80, 16, 24),
-                  (40, 30, 24), (200, 190, 1)]
+                  (40, 30, 24), (200, 190, 1), (161, 1, 1)]
 SWEEP_CASES = [("cluster", s) for s in CLUSTER_SHAPES] + [(p, s) for p in SWEEP_PATHS if p != "cluster"
                                                            for s in TMA_SHAPES]
 

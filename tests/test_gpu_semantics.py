@@ -148,7 +148,8 @@ def test_run_hooks_fire_live(G, path, monkeypatch):
     [-0.01, 1.01] -- here an explicit logistic term with rho tau > 3, which overshoots."""
     _path(path, monkeypatch)
     shape = SHAPES[path]
-    d, u0, _ = _case(shape)
+    d, _, _ = _case(shape)
+    u0 = np.where(d > 0.0, 0.5, 0.0)  # 0.5 + rho tau 0.25 = 1.34: the logistic term overshoots at once
     h = 0.5
     steps = 6
     rho = 0.1
