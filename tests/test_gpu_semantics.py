@@ -149,7 +149,8 @@ def test_run_hooks_fire_live(G, path, monkeypatch):
     _path(path, monkeypatch)
     shape = SHAPES[path]
     d, _, _ = _case(shape)
-    u0 = np.where(d > 0.0, 0.5, 0.0)  # 0.5 + rho tau 0.25 = 1.34: the logistic term overshoots at once
+    d = np.where(d > 0.0, d, 0.05)  # no dead voxels: a uniform u has A u = 0 (row-constant D)
+    u0 = np.full(d.size, 0.5)       # 0.5 + tau rho 0.25 = 1.34: the explicit logistic term overshoots
     h = 0.5
     steps = 6
     rho = 0.1
