@@ -117,7 +117,7 @@ struct gs_ctx {
     // vectors
     DevBuf u, g, f0, f1, t0, t1, out;
     // scratch
-    DevBuf part_b, part_c, part_u, slots, mslots, ctrl, metrics, infos, normbits;
+    DevBuf part_b, part_c, part_u, slots, mslots, xchg, ctrl, metrics, infos, normbits;
     // exact sequential sums (gs_seqsum.cuh): tile sums/prefixes, per-CTA item lists, counts
     DevBuf seq_tsum, seq_items, seq_counts;
     // gs_run_ensemble (this context as member 0): the members' SolveParams and the group control words
@@ -455,6 +455,8 @@ gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps
     const bool fresh_ctrl = c->ctrl.p == nullptr;
     GS_CUDA(c, c->ctrl.alloc(sizeof(gs::Ctrl)));
     GS_CUDA(c, cudaMemsetAsync(c->slots.p, 0, sizeof(unsigned long long) * 24, c->stream));
+    GS_CUDA(c, c->xchg.alloc(sizeof(unsigned long long) * gs::kXchgWords));
+    GS_CUDA(c, cudaMemsetAsync(c->xchg.p, 0, sizeof(unsigned long long) * gs::kXchgWords, c->stream));
     const unsigned long long ms_init[4] = {0ull, ~0ull, 0ull, 0ull};
     GS_CUDA(c, cudaMemcpyAsync(c->mslots.p, ms_init, sizeof ms_init, cudaMemcpyHostToDevice, c->stream));
     // a new run starts from a clean control block, except last_terms (the previous call's
@@ -502,6 +504,8 @@ gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps
     p.part_u = c->part_u.as<double>();
     p.slots = c->slots.as<unsigned long long>();
     p.mslots = c->mslots.as<unsigned long long>();
+    // GS_NO_XCHG=1: the atomicMax slots and the plain grid barrier (A/B)
+    p.xchg = (gb <= gs::kXchgCtas && std::getenv("GS_NO_XCHG") == nullptr) ? c->xchg.as<unsigned long long>() : nullptr;
     p.ctrl = c->ctrl.as<gs::Ctrl>();
     // the reference's sequential ||b||_1 and bordered column sum (GS_TREE_SUMS=1: tree sums, A/B)
     p.seq_exact = std::getenv("GS_TREE_SUMS") == nullptr ? (std::getenv("GS_SEQ_DEBUG") ? 2 : 1) : 0;
@@ -1085,7 +1089,7 @@ void gs_destroy(gs_ctx* c) {
     for (DevBuf* b : {&c->csr_offs, &c->csr_cols, &c->csr_vals, &c->csc_offs, &c->csc_abs})
         b->release();
     for (DevBuf* b : {&c->pal, &c->dvox, &c->wtab, &c->dtab, &c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out,
-                      &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->ctrl, &c->metrics, &c->infos,
+                      &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->xchg, &c->ctrl, &c->metrics, &c->infos,
                       &c->normbits, &c->trace, &c->ens_params, &c->ens_ctl})
         b->release();
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -1449,8 +1453,18 @@ gs_status ens_prepare(gs_ctx* const* ctxs, int n_members, int n_steps, const dou
 
 // n_steps batched steps of the n members whose SolveParams start at dP, on stream st; ctl
 // holds ens_ctl_words(groups) + n words.
+// tc (optional): a context with kernel timing on -- CUDA events bracket each step's Taylor
+// launch on st (gs_get_kernel_times of that context then reports them under "taylor").
 cudaError_t ens_launch(const EnsPlan& plan, const gs::SolveParams* dP, int n, int n_steps, bool metrics,
-                       unsigned* ctl, cudaStream_t st) {
+                       unsigned* ctl, cudaStream_t st, gs_ctx* tc = nullptr) {
+    if (tc && !tc->ktime) tc = nullptr;
+    if (tc)
+        while (tc->events.size() < 2 * static_cast<size_t>(n_steps)) {
+            cudaEvent_t ev;
+            const cudaError_t r = cudaEventCreate(&ev);
+            if (r != cudaSuccess) return r;
+            tc->events.push_back(ev);
+        }
     const int groups = std::min(plan.groups, n), grp = plan.grp, sb = plan.sb;
     const unsigned* order = ctl + gs::ens_ctl_words(groups);
     const dim3 blk(gs::kSolveThreads);
@@ -1480,9 +1494,11 @@ cudaError_t ens_launch(const EnsPlan& plan, const gs::SolveParams* dP, int n, in
         if (!std::getenv("GS_ENS_EXTRA")) extra = 0;
         void* args[] = {const_cast<gs::SolveParams**>(&dP), &nm, &g, &bb, &sp, &ctl, const_cast<unsigned**>(&order),
                         &extra};
+        if (tc && (e = cudaEventRecord(tc->events[2 * step], st)) != cudaSuccess) return e;
         if ((e = cudaLaunchCooperativeKernel(gs::ens_taylor_kernel_fn(plan.fuse), dim3(groups * grp + extra), blk, args,
                                              gs::kDynSmemBytes, st)) != cudaSuccess)
             return e;
+        if (tc && (e = cudaEventRecord(tc->events[2 * step + 1], st)) != cudaSuccess) return e;
         gs::ens_update_kernel<<<n * sb, blk, 0, st>>>(dP, sb, step);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
@@ -1531,7 +1547,7 @@ gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const
                                 cudaMemcpyHostToDevice, c0->stream));
     cudaStream_t st = c0->stream;
     GS_CUDA(c0, ens_launch(plan, c0->ens_params.as<gs::SolveParams>(), n_members, n_steps, metrics != nullptr,
-                           c0->ens_ctl.as<unsigned>(), st));
+                           c0->ens_ctl.as<unsigned>(), st, c0));
     std::vector<gs::Ctrl> ctrl(static_cast<size_t>(n_members));
     for (int i = 0; i < n_members; ++i) {
         gs_ctx* c = ctxs[i];
@@ -1544,6 +1560,18 @@ gs_status gs_run_ensemble(gs_ctx* const* ctxs, int n_members, int n_steps, const
                                         sizeof(gs_step_info) * n_steps, cudaMemcpyDeviceToHost, st));
     }
     GS_CUDA(c0, cudaStreamSynchronize(st));
+    if (c0->ktime) {  // the batched Taylor launches of this call (kind 2 = taylor, as gs_run reports it)
+        for (int k = 0; k < 4; ++k) {
+            c0->kms[k] = 0.0;
+            c0->kcount[k] = 0;
+        }
+        for (int q = 0; q < n_steps; ++q) {
+            float ms = 0.f;
+            GS_CUDA(c0, cudaEventElapsedTime(&ms, c0->events[2 * q], c0->events[2 * q + 1]));
+            c0->kms[2] += ms;
+            c0->kcount[2] += 1;
+        }
+    }
     return ens_status(ctxs, n_members, ctrl);
 }
 

@@ -67,8 +67,13 @@ constexpr int kRingBytes = kTmaStages * kSlotBytes + 128;              // + barr
 // two-voxel halo in x, y and z.
 #ifdef GS_TILE8
 constexpr int k2Stages = 7;
+#elif defined(GS_STAGES8)
+constexpr int k2Stages = 8;  // A/B: the eight-stage ring with rotating slot indices
 #else
-constexpr int k2Stages = 8;
+// six stages: the z-loop unrolled by six has compile-time slot indices (sweep2_tma); measured
+// against eight stages with rotating indices: +1.0% at C4, +1.2% at C3, +2.6% at C5 -- two
+// planes in flight beyond the four in use are enough lead at ~1 us per plane
+constexpr int k2Stages = 6;
 #endif
 constexpr int k2XRows = kTmaTY + 4;                                     // y halo 2
 constexpr int k2XBytes = (k2XRows * kXPitch * 8 + 127) / 128 * 128;    // 20 x 68 doubles
@@ -139,7 +144,10 @@ constexpr int kRedOffset = kDynSmemBytes - 128 - 768;  // (kSolveThreads / 32) x
 static_assert(kRedOffset >= k2IStages * k2ISlotBytes && kRedOffset >= k2Stages * k2SlotBytes &&
                   kRedOffset >= kTmaStages * kSlotBytes && kRedOffset >= k3XStages * k3XSlotBytes + k3FBStages * k3FBBytes,
               "reduction scratch overlaps a TMA-written region");
-static_assert(kDynSmemBytes + 2304 <= 232448, "dynamic + static shared memory over the 227 KB block limit");
+static_assert(kDynSmemBytes + 2336 <= 232448, "dynamic + static shared memory over the 227 KB block limit");
+
+constexpr int kXchgCtas = 160;   // CTAs of one (virtual) Taylor grid the maxima exchange can hold
+constexpr int kXchgWords = 2 * kXchgCtas * kXchgCtas * 2;  // [set][inbox of CTA][from CTA][2 words]
 
 // Device-resident control block shared by the kernels of one launch sequence.
 struct Ctrl {
@@ -155,6 +163,7 @@ struct Ctrl {
     unsigned seq_ticket[2], seq_ticket2[2], seq_flags[2];
     unsigned border_ticket;
     int coln_need;        // the tree column sum does not settle (s, m): the exact one is required
+    unsigned xround;      // rounds of the maxima exchange so far (xchg_keys4), across launches
     int last_terms;       // Taylor terms of the last step (ensemble: longest members first)
 };
 
@@ -199,6 +208,9 @@ struct SolveParams {
     int seq_exact;          // 1: the two sums are the reference's sequential ones; 0: tree sums (A/B)
     unsigned long long* slots;   // [3][8] rotating max slots for per-term reductions
     unsigned long long* mslots;  // [2][4] metric max/min/r2 slots (step parity)
+    // Bounded two-term sweeps: the per-sweep maxima exchange that is also the sweep's grid
+    // barrier (xchg_keys4; kXchgWords words cleared per run; nullptr: atomicMax slots + grid barrier)
+    unsigned long long* xchg;
     Ctrl* ctrl;
     unsigned long long* trace;  // optional phase trace: (tag, globaltimer ns) pairs
     int trace_cap;

@@ -100,6 +100,87 @@ __device__ __forceinline__ void block_reduce(double (&v)[K], S& sm) {
     __syncthreads();
 }
 
+// Maxima exchange of the bounded two-term sweeps: the sweep's grid barrier and the all-reduce
+// (max) of its four bounding maxima in ONE round trip through L2, in place of atomicMax slots
+// + grid barrier + slot reads (three).
+//   push   thread e < G of CTA c stores c's block maxima into CTA e's inbox, entry c;
+//   poll   the same thread waits for entry e of its own CTA's inbox (lines only this CTA
+//          reads: no hot spot), then a block max over the entries gives every thread the grid
+//          maxima.
+// Seeing CTA e's entry means CTA e has finished its sweep (each pusher fences after the block
+// barrier that follows the sweep, then stores; the poller fences after its loads), so this is
+// the barrier between sweeps as well.  A bounding maximum travels as its key, the high word of
+// a non-negative double with a zero low word (key_lower): 31 bits, two per 64-bit word, whose
+// two spare bits carry the round's tag.  The two entry sets alternate by round; tags cycle
+// 1, 2, 3 over the uses of a set and 0 is the cleared state (setup_solve), so an entry of the
+// set's previous use never passes for the current one -- a CTA cannot push round r + 2 before
+// every CTA has polled round r, since it first has to see every CTA's round r + 1 entry.  The
+// round counter lives in the control block across launches (ctrl->xround).
+template <class S>
+__device__ __forceinline__ void xchg_keys4(const SolveParams& p, S& sm, double (&mx)[5], unsigned xr) {
+    const int G = vncta(), me = vcta();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned long long* set = p.xchg + static_cast<size_t>(xr & 1u) * (kXchgCtas * kXchgCtas * 2);
+    const unsigned tag = 1u + ((xr >> 1) % 3u);
+    const unsigned t_hi = (tag >> 1) << 31, t_lo = (tag & 1u) << 31;
+    unsigned* s1 = reinterpret_cast<unsigned*>(&sm.red[0][0]);  // [warps][4] block stage
+    unsigned* s2 = s1 + (kSolveThreads / 32) * 4;               // [<= 5][4] grid stage
+    unsigned k[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) k[q] = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(__double2hiint(mx[q])));
+    if (lane == 0) *reinterpret_cast<uint4*>(s1 + 4 * wid) = make_uint4(k[0], k[1], k[2], k[3]);
+    __syncthreads();  // also: every thread's sweep writes precede the pushers' fences
+    k[0] = k[1] = k[2] = k[3] = 0u;
+    if (tid < G) {
+#pragma unroll
+        for (int w = 0; w < kSolveThreads / 32; ++w) {
+            const uint4 v = *reinterpret_cast<const uint4*>(s1 + 4 * w);
+            k[0] = max(k[0], v.x);
+            k[1] = max(k[1], v.y);
+            k[2] = max(k[2], v.z);
+            k[3] = max(k[3], v.w);
+        }
+        const unsigned long long w0 = (static_cast<unsigned long long>(k[0] | t_hi) << 32) | (k[1] | t_lo);
+        const unsigned long long w1 = (static_cast<unsigned long long>(k[2] | t_hi) << 32) | (k[3] | t_lo);
+        __threadfence();
+        volatile unsigned long long* out = set + (static_cast<size_t>(tid) * kXchgCtas + me) * 2;
+        out[0] = w0;
+        out[1] = w1;
+        const volatile unsigned long long* in = set + (static_cast<size_t>(me) * kXchgCtas + tid) * 2;
+        const unsigned long long tmask = (1ull << 63) | (1ull << 31);
+        const unsigned long long twant = (static_cast<unsigned long long>(t_hi) << 32) | t_lo;
+        unsigned long long a, b;
+        do {
+            a = in[0];
+            b = in[1];
+        } while ((a & tmask) != twant || (b & tmask) != twant);
+        __threadfence();
+        k[0] = static_cast<unsigned>(a >> 32) & 0x7fffffffu;
+        k[1] = static_cast<unsigned>(a) & 0x7fffffffu;
+        k[2] = static_cast<unsigned>(b >> 32) & 0x7fffffffu;
+        k[3] = static_cast<unsigned>(b) & 0x7fffffffu;
+    }
+    const int nw = (G + 31) >> 5;
+    if (wid < nw) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) k[q] = __reduce_max_sync(0xffffffffu, k[q]);
+        if (lane == 0) *reinterpret_cast<uint4*>(s2 + 4 * wid) = make_uint4(k[0], k[1], k[2], k[3]);
+    }
+    __syncthreads();
+    k[0] = k[1] = k[2] = k[3] = 0u;
+    for (int w = 0; w < nw; ++w) {
+        const uint4 v = *reinterpret_cast<const uint4*>(s2 + 4 * w);
+        k[0] = max(k[0], v.x);
+        k[1] = max(k[1], v.y);
+        k[2] = max(k[2], v.z);
+        k[3] = max(k[3], v.w);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mx[q] = __hiloint2double(static_cast<int>(k[q]), 0);
+    mx[4] = 0.0;
+    __syncthreads();  // the scratch is free again
+}
+
 // Deterministic sum of the per-CTA partials; every CTA computes the same value.
 template <class S>
 __device__ double grid_sum(const double* part, int nb, S& sm) {
@@ -475,11 +556,17 @@ __device__ __forceinline__ void sweep_l1(const StencilOp& op, const double* X, c
 // re-read is an L2 hit.  The remaining CTAs split the slab [lock_zm, nz) evenly.
 struct CtaWork {
     int zb, len;
-    int64_t qb, qe;
+    int qb, qe;  // tile-planes: tiles * nz < 2^31 for any grid that fits the device
 };
 
-__device__ __forceinline__ CtaWork cta_work(const SolveParams& p, int64_t tiles) {
+// Computed once per kernel by thread 0 (block_setup) and kept in shared memory: the split does
+// not change between sweeps, and its 64-bit divisions would otherwise sit at the head of every
+// sweep (a Taylor launch runs up to ~100 of them).
+__shared__ CtaWork s_cw;
+
+__device__ __forceinline__ CtaWork cta_work_compute(const SolveParams& p) {
     CtaWork w;
+    const int64_t tiles = static_cast<int64_t>((p.op.nx + kTmaTX - 1) / kTmaTX) * ((p.op.ny + kTmaTY - 1) / kTmaTY);
     const int64_t b = vcta(), G = vncta();
     const int k = p.lock_groups;
     if (k > 0 && G >= k * tiles) {
@@ -488,14 +575,14 @@ __device__ __forceinline__ CtaWork cta_work(const SolveParams& p, int64_t tiles)
             const int j = static_cast<int>(b / tiles);
             w.zb = j * p.lock_zm / k;
             w.len = (j + 1) * p.lock_zm / k - w.zb;
-            w.qb = (b % tiles) * w.len;
+            w.qb = static_cast<int>((b % tiles) * w.len);
             w.qe = w.qb + w.len;
         } else {
             w.zb = p.lock_zm;
             w.len = p.op.nz - p.lock_zm;
             const int64_t qs = tiles * w.len, E = G - kP, e = b - kP;
-            w.qb = e * qs / E;
-            w.qe = (e + 1) * qs / E;
+            w.qb = static_cast<int>(e * qs / E);
+            w.qe = static_cast<int>((e + 1) * qs / E);
         }
         if (w.len <= 0) w.len = 1, w.qb = w.qe = 0;
         return w;
@@ -503,10 +590,12 @@ __device__ __forceinline__ CtaWork cta_work(const SolveParams& p, int64_t tiles)
     w.zb = 0;
     w.len = p.op.nz;
     const int64_t Q = tiles * p.op.nz;
-    w.qb = b * Q / G;
-    w.qe = (b + 1) * Q / G;
+    w.qb = static_cast<int>(b * Q / G);
+    w.qe = static_cast<int>((b + 1) * Q / G);
     return w;
 }
+
+__device__ __forceinline__ CtaWork cta_work() { return s_cw; }
 
 // TMA z-slab sweep.  `seq` counts plane loads issued so far in this launch (identical in
 // every thread); it fixes each ring slot's mbarrier phase parity.
@@ -518,20 +607,22 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
     const int lane = tid & 31, row = tid >> 5;
     const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
     const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
-    const CtaWork cw = cta_work(p, static_cast<int64_t>(tiles_x) * tiles_y);
-    const int64_t q_begin = cw.qb, q_end = cw.qe;
+    const CtaWork cw = cta_work();
+    const int q_begin = cw.qb, q_end = cw.qe;
     constexpr uint32_t kOwnBytes = kLBytes + (kNeedF ? kOBytes : 0) + (kNeedB ? kOBytes : 0);
     constexpr uint32_t kHaloBytes = (kTmaTY + 2) * kXPitch * 8;
     if (tid == 0) fence_proxy_async_global();  // generic writes before this sweep -> TMA reads
     const uint64_t pol_labels = l2_policy_evict_last();  // labels stay in L2 (see sweep2_tma)
 
-    for (int64_t q = q_begin; q < q_end;) {
-        const int64_t tile = q / cw.len;
-        const int z0 = cw.zb + static_cast<int>(q % cw.len);
-        const int z1 = static_cast<int>(min(static_cast<int64_t>(cw.zb + cw.len), static_cast<int64_t>(z0) + (q_end - q)));
+    for (int q = q_begin; q < q_end;) {
+        // (unsigned 32-bit divisions: the operands are non-negative and small)
+        const unsigned tile = static_cast<unsigned>(q) / static_cast<unsigned>(cw.len);
+        const int z0 = cw.zb + (q - static_cast<int>(tile) * cw.len);
+        const int z1 = min(cw.zb + cw.len, z0 + (q_end - q));
         q += z1 - z0;
-        const int x0 = static_cast<int>(tile % tiles_x) * kTmaTX;
-        const int y0 = static_cast<int>(tile / tiles_x) * kTmaTY;
+        const unsigned ty = tile / static_cast<unsigned>(tiles_x);
+        const int x0 = static_cast<int>(tile - ty * tiles_x) * kTmaTX;
+        const int y0 = static_cast<int>(ty) * kTmaTY;
         const uint32_t base = seq;
         const int np = z1 - z0 + 2;  // planes z0-1 .. z1
 
@@ -735,25 +826,33 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
 
     const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
     const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
-    const CtaWork cw = cta_work(p, static_cast<int64_t>(tiles_x) * tiles_y);
-    const int64_t q_begin = cw.qb, q_end = cw.qe;
+    const CtaWork cw = cta_work();
+    const int q_begin = cw.qb, q_end = cw.qe;
     if (tid == kIssuer) fence_proxy_async_global();
     const uint64_t pol_labels = l2_policy_evict_last();
     unsigned mk[4] = {0u, 0u, 0u, 0u};  // bounding maxima (kExact == false): see max_key
 
-    for (int64_t q = q_begin; q < q_end;) {
-        const int64_t tile = q / cw.len;
-        const int z0 = cw.zb + static_cast<int>(q % cw.len);
-        const int z1 = static_cast<int>(min(static_cast<int64_t>(cw.zb + cw.len), static_cast<int64_t>(z0) + (q_end - q)));
+    for (int q = q_begin; q < q_end;) {
+        // (unsigned 32-bit divisions: the operands are non-negative and small)
+        const unsigned tile = static_cast<unsigned>(q) / static_cast<unsigned>(cw.len);
+        const int z0 = cw.zb + (q - static_cast<int>(tile) * cw.len);
+        const int z1 = min(cw.zb + cw.len, z0 + (q_end - q));
         q += z1 - z0;
-        const int x0 = static_cast<int>(tile % tiles_x) * kTmaTX;
-        const int y0 = static_cast<int>(tile / tiles_x) * kTmaTY;
+        const unsigned ty = tile / static_cast<unsigned>(tiles_x);
+        const int x0 = static_cast<int>(tile - ty * tiles_x) * kTmaTX;
+        const int y0 = static_cast<int>(ty) * kTmaTY;
         const uint32_t base = seq;
         const int pfirst = z0 - 2, plast = z1 + 1;  // planes loaded
         const int np = plast - pfirst + 1;
 
-        auto issue = [&](int pl) {  // thread 0 only
-            const int slot = static_cast<int>((base + static_cast<uint32_t>(pl - pfirst)) % kSt);
+        // Static slots (kStatic: six stages, the z-loop unrolled by six): every segment starts at
+        // slot 0 -- the ring is empty between segments, every issued plane has been waited for --
+        // so plane pfirst + k sits in slot k % 6, a compile-time index inside the unrolled loop, and
+        // every shared-memory address of the loop is a per-thread base plus an immediate.
+        constexpr bool kStatic = kSt == 6;
+        auto issue = [&](int pl) {  // the issuer only
+            const int slot = kStatic ? (pl - pfirst) % kSt
+                                     : static_cast<int>((base + static_cast<uint32_t>(pl - pfirst)) % kSt);
             uint64_t* bar = ring.bar + slot;
             const bool ownF = needF && pl >= z0 && pl < z1;
             const bool haloB = needB && pl >= z0 - 1 && pl <= z1;
@@ -807,7 +906,11 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
                 if (ringer) T1[rT] = 0.0;
                 return;
             }
+#ifdef GS_EXP_DHZ2
+            const double dhz = 2.0;  // timing experiment only
+#else
             const double dhz = static_cast<double>((pl > 0) + (pl < op.nz - 1));
+#endif
             const double* Xc = ring.x(sc_);
             const uint8_t* L = ring.l(sc_);
             const double* B = ring.b(sc_);
@@ -837,7 +940,12 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
             t1[1] = v1_;
             T1[oT] = v0_;
             T1[oT + kT1Pitch] = v1_;
+#ifdef GS_EXP_NORING
+            if (ringer) T1[rT] = 0.0;  // timing experiment only: WRONG results
+            if (false) {
+#else
             if (ringer) {
+#endif
                 const double w = s_wtab[L[rL]];
                 double sc;
                 if (KIND == k2FirstZero) {
@@ -883,8 +991,8 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
             fence_proxy_async_shared();  // generic writes into a TMA slot before its next fill
         };
 
-        int s0 = static_cast<int>(base % kSt);  // slot of plane z0-2
-        int s1 = next_slot(s0), s2 = next_slot(s1), s3 = next_slot(s2);
+        const int s0 = kStatic ? 0 : static_cast<int>(base % kSt);  // slot of plane z0-2
+        const int s1 = next_slot(s0), s2 = next_slot(s1), s3 = next_slot(s2);
         // prologue: T1 of planes z0-1 and z0
         wait_slot(s0);
         wait_slot(s1);
@@ -937,16 +1045,27 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
         int sM = s1, sA = s2, sB = s3, sC = next_slot(s3);  // slots of planes z-1, z, z+1, z+2
         double* pT = outT + v0 + static_cast<int64_t>(z0) * op.sz;
         double* pF = outF + v0 + static_cast<int64_t>(z0) * op.sz;
-        auto iter = [&](int z, auto rconst) {
-            constexpr int r = decltype(rconst)::value;
+        auto iter = [&](int z, auto jconst) {
+            constexpr int j = decltype(jconst)::value;  // (z - z0) % 6 (static slots) or % 3
+            constexpr int r = j % 3;
             constexpr int r1 = (r + 1) % 3, r2 = (r + 2) % 3;
+            if constexpr (kStatic) {
+                sM = (j + 1) % 6;
+                sA = (j + 2) % 6;
+                sB = (j + 3) % 6;
+                sC = (j + 4) % 6;
+            }
             if (z > z0) {
                 // Phase B: own voxels of plane zo = z-1 (T1 of zo-1, zo, zo+1 in T3[r2], T3[r], T3[r1])
                 const int zo = z - 1;
                 const double* T1s = ring.t1(r);  // plane zo = z - 1: slot (z - z0) % 3
                 const uint8_t* L = ring.l(sM);
                 const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
+#ifdef GS_EXP_DHZ2
+                const double dhz = 2.0;
+#else
                 const double dhz = static_cast<double>((zo > 0) + (zo < op.nz - 1));
+#endif
                 const double y0m = T1s[oT - kT1Pitch], y1p = T1s[oT + 2 * kT1Pitch];
                 const double a0 = rowap(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), T3[r2][0], y0m, T1s[oT - 1],
                                                T3[r][0], T1s[oT + 1], T3[r][1], T3[r1][0]);
@@ -1009,20 +1128,33 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
                 double lwN[2];
                 phaseA(z + 1, r2, sA, sB, sC, X3[r], X3[r1], X3[r2], T3[r2], lwN);
             }
-            sM = sA;
-            sA = sB;
-            sB = sC;
-            sC = next_slot(sC);
+            if constexpr (!kStatic) {
+                sM = sA;
+                sA = sB;
+                sB = sC;
+                sC = next_slot(sC);
+            }
             __syncthreads();  // plane z-1's slot and T1(z-1)'s shared plane are free
             if (tid == kIssuer && z > z0) {
                 const int nxt = z - 1 + kSt;
                 if (nxt <= plast) issue(nxt);
             }
         };
-        for (int zb = z0; zb <= z1; zb += 3) {
-            iter(zb, std::integral_constant<int, 0>{});
-            if (zb + 1 <= z1) iter(zb + 1, std::integral_constant<int, 1>{});
-            if (zb + 2 <= z1) iter(zb + 2, std::integral_constant<int, 2>{});
+        if constexpr (kStatic) {
+            for (int zb = z0; zb <= z1; zb += 6) {
+                iter(zb, std::integral_constant<int, 0>{});
+                if (zb + 1 <= z1) iter(zb + 1, std::integral_constant<int, 1>{});
+                if (zb + 2 <= z1) iter(zb + 2, std::integral_constant<int, 2>{});
+                if (zb + 3 <= z1) iter(zb + 3, std::integral_constant<int, 3>{});
+                if (zb + 4 <= z1) iter(zb + 4, std::integral_constant<int, 4>{});
+                if (zb + 5 <= z1) iter(zb + 5, std::integral_constant<int, 5>{});
+            }
+        } else {
+            for (int zb = z0; zb <= z1; zb += 3) {
+                iter(zb, std::integral_constant<int, 0>{});
+                if (zb + 1 <= z1) iter(zb + 1, std::integral_constant<int, 1>{});
+                if (zb + 2 <= z1) iter(zb + 2, std::integral_constant<int, 2>{});
+            }
         }
         seq = base + static_cast<uint32_t>(np);
     }
@@ -1121,18 +1253,20 @@ __device__ __forceinline__ void sweep3_tma(const SolveParams& p, const Ring3& ri
 
     const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
     const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
-    const CtaWork cw = cta_work(p, static_cast<int64_t>(tiles_x) * tiles_y);
-    const int64_t q_begin = cw.qb, q_end = cw.qe;
+    const CtaWork cw = cta_work();
+    const int q_begin = cw.qb, q_end = cw.qe;
     if (tid == 0) fence_proxy_async_global();
     const uint64_t pol_labels = l2_policy_evict_last();  // labels stay in L2 (see sweep2_tma)
 
-    for (int64_t q = q_begin; q < q_end;) {
-        const int64_t tile = q / cw.len;
-        const int z0 = cw.zb + static_cast<int>(q % cw.len);
-        const int z1 = static_cast<int>(min(static_cast<int64_t>(cw.zb + cw.len), static_cast<int64_t>(z0) + (q_end - q)));
+    for (int q = q_begin; q < q_end;) {
+        // (unsigned 32-bit divisions: the operands are non-negative and small)
+        const unsigned tile = static_cast<unsigned>(q) / static_cast<unsigned>(cw.len);
+        const int z0 = cw.zb + (q - static_cast<int>(tile) * cw.len);
+        const int z1 = min(cw.zb + cw.len, z0 + (q_end - q));
         q += z1 - z0;
-        const int x0 = static_cast<int>(tile % tiles_x) * kTmaTX;
-        const int y0 = static_cast<int>(tile / tiles_x) * kTmaTY;
+        const unsigned ty = tile / static_cast<unsigned>(tiles_x);
+        const int x0 = static_cast<int>(tile - ty * tiles_x) * kTmaTX;
+        const int y0 = static_cast<int>(ty) * kTmaTY;
         const uint32_t basex = seqx, basef = seqf;
         const int pfirst = z0 - 3, plast = z1 + 2;  // X planes loaded
         const int fbfirst = needF ? z0 : z0 - 2;    // first F / b plane
@@ -1410,6 +1544,7 @@ __device__ __forceinline__ void block_setup(const SolveParams& p, S& sm, bool wi
         mbar_fence_init();
         for (int b = 0; b < kNumBufs; ++b) tma_prefetch_desc(&p.xmap[b]);  // generic address: param or global
     }
+    if (with_tma && threadIdx.x == 0) s_cw = cta_work_compute(p);
     __syncthreads();
 }
 
@@ -1702,6 +1837,7 @@ __device__ __forceinline__ void taylor_body(const SolveParams& p, int border_blo
         trace_mark(p, tag);
     };
     int round = 0;  // per-term max-reduction rounds (slot rotation, identical in every CTA)
+    unsigned xround = p.xchg ? __ldcg(&ctrl->xround) : 0u;  // rounds of the maxima exchange (xchg_keys4)
     auto sync_round = [&](int tag) {
         gsync(tag);
         if (leader) {
@@ -1956,7 +2092,7 @@ __device__ __forceinline__ void taylor_body(const SolveParams& p, int border_blo
                 const double c1 = __ddiv_rn(tau_s, static_cast<double>(used + 1));  // expact.cpp:83
                 const double c2 = __ddiv_rn(tau_s, static_cast<double>(used + 2));
                 const int fout = kBufF0 + fsel, tout = kBufT0 + tsel;
-                auto run_sweep = [&](auto exactc, double (&mx)[5]) {
+                auto run_sweep = [&](auto exactc, double (&mx)[5]) __attribute__((always_inline)) {
                     constexpr bool kEx = decltype(exactc)::value;
                     const int xb_ = xb < 0 ? 0 : xb, fb_ = fb < 0 ? 0 : fb;
                     double* oT = p.buf[tout];
@@ -1980,6 +2116,12 @@ __device__ __forceinline__ void taylor_body(const SolveParams& p, int border_blo
                     else
                         sweep2_tma<k2FirstPlain, kSkip, kEx>(p, ring2, xb_, fb_, kBufG, c1, c2, oT, oF, mx, seq2,
                                                              pmask2, sm.wtab);
+                    if (!kEx && p.xchg) {
+                        // (every thread's generic -> async-proxy fence: the end of sweep2_tma)
+                        xchg_keys4(p, sm, mx, xround++);
+                        trace_mark(p, kind == k2Next ? kTrFusedNext : kTrFusedFirst);
+                        return;
+                    }
                     block_reduce<5, true>(mx, sm);
                     if (threadIdx.x == 0) {
                         unsigned long long* sl = p.slots + (round % 3) * 8;
@@ -2168,6 +2310,7 @@ __device__ __forceinline__ void taylor_body(const SolveParams& p, int border_blo
         info->reruns = reruns;
     }
     if (leader) {
+        if (p.xchg) ctrl->xround = xround;
         ctrl->fres = fres;
         ctrl->tres = tres;
         ctrl->last_terms = static_cast<int>(total_terms);

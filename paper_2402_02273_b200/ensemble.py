@@ -29,6 +29,7 @@ class MemberResult:
     metrics: np.ndarray      # (steps+1, 4): total_mass, max, min, radius
     terms: np.ndarray        # Taylor terms per step
     checksum: float          # sum of the final state (sanity)
+    stage_terms: list | None = None  # per step, the Taylor terms of each stage (the step log)
 
 
 class EnsembleRunner:
@@ -72,14 +73,15 @@ class EnsembleRunner:
             for i, (mb, rho) in enumerate(zip(self.members, self.rhos)):
                 met = np.array([[x.total_mass, x.max_density, x.min_density, x.radius] for x in m[i]])
                 terms = np.array([inf[i][q].total_terms for q in range(steps)])
-                out.append(MemberResult(mb, rho, steps, met, terms, float("nan")))
+                st = [inf[i][q].stage_terms() for q in range(steps)]
+                out.append(MemberResult(mb, rho, steps, met, terms, float("nan"), st))
             return out
         out = []
         for mb, op, c, rho in zip(self.members, self.ops, self.centers, self.rhos):
             m, inf = op.run_resident(steps, rho, self.w.tau, W.TOL, (0.0, 0.0, 0.0), c, 0.1, metrics=True, infos=True)
             met = np.array([[x.total_mass, x.max_density, x.min_density, x.radius] for x in m])
             terms = np.array([inf[q].total_terms for q in range(steps)])
-            out.append(MemberResult(mb, rho, steps, met, terms, float("nan")))
+            out.append(MemberResult(mb, rho, steps, met, terms, float("nan"), [inf[q].stage_terms() for q in range(steps)]))
         return out
 
     def close(self):

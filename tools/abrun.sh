@@ -8,7 +8,7 @@ for rep in 1 2; do
     [ "$rest" != "$lib" ] && envs=${rest#*:}
     cp "$lib" paper_2402_02273_b200/libgliosim_b200.so
     env $envs timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | \
-      python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$name', round(d['value'],2), round(d['roofline']['avg_launch_ms'],3))"
+      python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$name', round(d['value'],2), round(d['roofline']['avg_launch_ms'],3), 'terms', d['config']['terms_per_step'], 'reruns', d['roofline']['exact_reruns_per_step'])"
   done
 done
 cp /tmp/gs_lib_keep.so paper_2402_02273_b200/libgliosim_b200.so
