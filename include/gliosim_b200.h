@@ -176,6 +176,10 @@ gs_status gs_get_kernel_times(gs_ctx* ctx, double ms[4], int launches[4]);
  * every step with the state in distributed shared memory (grids up to 40 K voxels;
  * GS_NO_CLUSTER=1 disables it).  The kernel times then report it as the Taylor kernel. */
 int gs_uses_cluster(const gs_ctx* ctx);
+/* 1 when the Taylor loop of this context's steps (expact.cpp:63-153) takes the 2-D path: one
+ * resident CTA per 32 x 32 tile with the tile in shared memory (nz == 1, every tile on the
+ * device at once; GS_NO_2D=1 disables it).  In run mode gs_uses_cluster takes precedence. */
+int gs_uses_flat2d(const gs_ctx* ctx);
 
 /* ---- snapshot and metrics files (vtk.hpp:15-45, src/vtk.cpp:59-157) ------------------- */
 /* write_vtk (vtk.cpp:59-91): legacy ASCII VTK, header + one "%.17g" value per line, then,

@@ -56,7 +56,7 @@ EXPORTS = [
     "gs_set_trace", "gs_get_trace", "gs_set_kernel_timing", "gs_get_kernel_times",
     "gs_write_vtk", "gs_read_vtk", "gs_write_metrics_csv", "gs_snapshot_vtk", "gs_snapshot_flush",
     "gs_load_stack", "gs_load_raw_volume", "gs_write_label_volume", "gs_read_label_volume",
-    "gs_matter_fractions", "gs_uses_cluster",
+    "gs_matter_fractions", "gs_uses_cluster", "gs_uses_flat2d",
 ]
 
 
@@ -129,6 +129,8 @@ def load(path: str | None = None):
         L.gs_matter_fractions.argtypes = [vp, _d3, _d3]
     if hasattr(L, "gs_uses_cluster"):
         L.gs_uses_cluster.argtypes = [vp]
+    if hasattr(L, "gs_uses_flat2d"):
+        L.gs_uses_flat2d.argtypes = [vp]
     for name in EXPORTS:
         if name not in ("gs_destroy", "gs_last_error", "gs_num_points", "gs_stream", "gs_state_device_ptr") \
                 and hasattr(L, name):

@@ -117,7 +117,8 @@ struct gs_ctx {
     // vectors
     DevBuf u, g, f0, f1, t0, t1, out;
     // scratch
-    DevBuf part_b, part_c, part_u, slots, mslots, xchg, ctrl, metrics, infos, normbits;
+    DevBuf part_b, part_c, part_u, slots, mslots, xchg, x2d, ctrl, metrics, infos, normbits;
+    int cap2d = 0;  // CTAs of the resident 2-D Taylor kernel the device holds at once
     // exact sequential sums (gs_seqsum.cuh): tile sums/prefixes, per-CTA item lists, counts
     DevBuf seq_tsum, seq_items, seq_counts;
     // gs_run_ensemble (this context as member 0): the members' SolveParams and the group control words
@@ -442,6 +443,18 @@ void lockstep_split(const gs_ctx* c, int gb, gs::SolveParams& p) {
     p.lock_zm = static_cast<int>(zm);
 }
 
+int tiles_2d(const gs_ctx* c) { return ((c->nx + 31) / 32) * ((c->ny + 31) / 32); }
+
+// The cooperative Taylor launch of one step: the resident-tile kernel on 2-D grids, else the
+// TMA sweeps on gb CTAs.
+cudaError_t launch_taylor(gs_ctx* c, const gs::SolveParams& p, int gb, void** args) {
+    if (p.use_2d)
+        return cudaLaunchCooperativeKernel(gs::taylor2d_kernel_fn(), dim3(p.use_2d), dim3(gs::kSolveThreads), args,
+                                           gs::k2dSmemBytes, c->stream);
+    return cudaLaunchCooperativeKernel(gs::taylor_kernel_fn(p.fuse), dim3(gb), dim3(gs::kSolveThreads), args,
+                                       gs::kDynSmemBytes, c->stream);
+}
+
 // Scratch, state staging and the context-dependent SolveParams fields of one run on the
 // context's stream: gb CTAs for prep / taylor, sb for the streaming kernels.
 gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps, gs_metrics* metrics,
@@ -506,6 +519,18 @@ gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps
     p.mslots = c->mslots.as<unsigned long long>();
     // GS_NO_XCHG=1: the atomicMax slots and the plain grid barrier (A/B)
     p.xchg = (gb <= gs::kXchgCtas && std::getenv("GS_NO_XCHG") == nullptr) ? c->xchg.as<unsigned long long>() : nullptr;
+    // 2-D grids whose 32 x 32 tiles all fit the device at once: the resident-tile Taylor kernel
+    // (gs_flat2d.cuh); GS_NO_2D=1 keeps them on the TMA sweeps (A/B, tests)
+    p.use_2d = 0;
+    p.x2d = nullptr;
+    {
+        const int t2d = tiles_2d(c);
+        if (gs_uses_flat2d(c)) {
+            GS_CUDA(c, c->x2d.alloc(sizeof(double) * 2 * (gs::k2dK + 1) * static_cast<size_t>(c->n)));
+            p.use_2d = t2d;
+            p.x2d = c->x2d.as<double>();
+        }
+    }
     p.ctrl = c->ctrl.as<gs::Ctrl>();
     // the reference's sequential ||b||_1 and bordered column sum (GS_TREE_SUMS=1: tree sums, A/B)
     p.seq_exact = std::getenv("GS_TREE_SUMS") == nullptr ? (std::getenv("GS_SEQ_DEBUG") ? 2 : 1) : 0;
@@ -673,7 +698,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
                 launch_seqsum(c, p, 0);
                 gs::border_kernel<<<sb, blk, 0, c->stream>>>(p, gb, -1);
                 launch_seqsum(c, p, 1);
-                cudaLaunchCooperativeKernel(gs::taylor_kernel_fn(p.fuse), dim3(gb), blk, args, dyn, c->stream);
+                launch_taylor(c, p, gb, args);
                 gs::update_kernel<<<sb, blk, 0, c->stream>>>(p, -1);
                 gs::advance_kernel<<<1, 1, 0, c->stream>>>(p.ctrl);
                 ok = cudaStreamEndCapture(c->stream, &graph) == cudaSuccess && graph != nullptr;
@@ -705,8 +730,7 @@ gs_status launch_solve(gs_ctx* c, gs::SolveParams& p, int n_steps, gs_metrics* m
             int border_blocks = sb;
             void* args[] = {&p, &border_blocks, &step};
             GS_CUDA(c, ev(2));
-            GS_CUDA(c, cudaLaunchCooperativeKernel(gs::taylor_kernel_fn(p.fuse), dim3(gb), blk, args, dyn,
-                                                   c->stream));
+            GS_CUDA(c, launch_taylor(c, p, gb, args));
             GS_CUDA(c, ev_end());
             GS_CUDA(c, ev(3));
             gs::update_kernel<<<sb, blk, 0, c->stream>>>(p, step);
@@ -932,6 +956,15 @@ gs_status gs_create(gs_ctx** out, int nx, int ny, int nz, double h, int device) 
     for (const void* fn : {reinterpret_cast<const void*>(gs::prep_kernel), reinterpret_cast<const void*>(gs::ens_prep_kernel)})
         if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::kRingBytes)) != cudaSuccess)
             return bail(e, "cudaFuncSetAttribute(smem prep)");
+    if (const void* fn2 = gs::taylor2d_kernel_fn()) {
+        if ((e = cudaFuncSetAttribute(fn2, cudaFuncAttributeMaxDynamicSharedMemorySize, gs::k2dSmemBytes)) != cudaSuccess)
+            return bail(e, "cudaFuncSetAttribute(smem 2d)");
+        int per2 = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, fn2, gs::kSolveThreads, gs::k2dSmemBytes)) !=
+            cudaSuccess)
+            return bail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(2d)");
+        c->cap2d = per2 * c->num_sms;
+    }
     int per_sm = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::taylor_kernel_fn(2), gs::kSolveThreads,
                                                            gs::kDynSmemBytes)) != cudaSuccess)
@@ -1089,7 +1122,7 @@ void gs_destroy(gs_ctx* c) {
     for (DevBuf* b : {&c->csr_offs, &c->csr_cols, &c->csr_vals, &c->csc_offs, &c->csc_abs})
         b->release();
     for (DevBuf* b : {&c->pal, &c->dvox, &c->wtab, &c->dtab, &c->u, &c->g, &c->f0, &c->f1, &c->t0, &c->t1, &c->out,
-                      &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->xchg, &c->ctrl, &c->metrics, &c->infos,
+                      &c->part_b, &c->part_c, &c->part_u, &c->slots, &c->mslots, &c->xchg, &c->x2d, &c->ctrl, &c->metrics, &c->infos,
                       &c->normbits, &c->trace, &c->ens_params, &c->ens_ctl})
         b->release();
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -1822,6 +1855,12 @@ gs_status gs_snapshot_vtk(gs_ctx* c, const char* path, const double origin[3], c
 
 int gs_uses_cluster(const gs_ctx* c) {
     return (c && c->cluster_ok && c->palette_mode && !c->is_csr && std::getenv("GS_NO_CLUSTER") == nullptr) ? 1 : 0;
+}
+
+int gs_uses_flat2d(const gs_ctx* c) {
+    if (!c || c->nz != 1 || !c->palette_mode || c->is_csr || !gs::taylor2d_kernel_fn()) return 0;
+    const int t2d = tiles_2d(c);
+    return (t2d <= c->cap2d && std::getenv("GS_NO_2D") == nullptr) ? 1 : 0;
 }
 
 gs_status gs_snapshot_flush(gs_ctx* c) {

@@ -211,6 +211,9 @@ struct SolveParams {
     // Bounded two-term sweeps: the per-sweep maxima exchange that is also the sweep's grid
     // barrier (xchg_keys4; kXchgWords words cleared per run; nullptr: atomicMax slots + grid barrier)
     unsigned long long* xchg;
+    // 2-D grids with one resident CTA per tile (gs_flat2d.cuh): 2 (k2dK + 1) N-vectors of scratch
+    int use_2d;
+    double* x2d;
     Ctrl* ctrl;
     unsigned long long* trace;  // optional phase trace: (tag, globaltimer ns) pairs
     int trace_cap;
@@ -286,6 +289,14 @@ __global__ void advance_kernel(Ctrl* ctrl);
 // Taylor kernel as a launchable handle: FUSE = 2 or 3 Taylor terms per TMA pass, 4 = two
 // terms with the past-the-grid planes skipped (thin grids).
 const void* taylor_kernel_fn(int fuse);
+// The resident-tile Taylor kernel of 2-D grids (gs_flat2d.cuh): cooperative, one CTA per
+// 32 x 32 tile, k2dSmemBytes of dynamic shared memory; nullptr in builds without 512 threads.
+#ifndef GS_2D_K
+#define GS_2D_K 4
+#endif
+constexpr int k2dK = GS_2D_K;  // Taylor terms per round (one grid barrier): 2..4
+constexpr int k2dSmemBytes = (k2dK + 3) * (32 + 2 * k2dK) * (32 + 2 * k2dK) * 8;
+const void* taylor2d_kernel_fn();
 __global__ void update_kernel(const __grid_constant__ SolveParams p, int step);
 
 // Ensemble (C5) forms of the step's kernels: one launch serves every member; P is a device

@@ -2318,6 +2318,8 @@ __device__ __forceinline__ void taylor_body(const SolveParams& p, int border_blo
     if (p.use_tma) fence_proxy_async_global();
 }
 
+#include "gs_flat2d.cuh"
+
 __global__ void advance_kernel(Ctrl* ctrl) { ctrl->step += 1; }
 
 // ------------------------------------------------------------------------------------------
@@ -2391,6 +2393,13 @@ struct GroupBarrier {
         __syncthreads();
     }
 };
+
+__global__ void __launch_bounds__(kSolveThreads) taylor2d_kernel(const __grid_constant__ SolveParams p, int border_blocks,
+                                                                  int step) {
+    vgrid_set(blockIdx.x, gridDim.x);
+    cg::grid_group grid = cg::this_grid();
+    taylor2d_body(p, border_blocks, step, [&] { grid.sync(); });
+}
 
 template <int FUSE>
 __global__ void __launch_bounds__(kSolveThreads, kMinBlocks) taylor_kernel(const __grid_constant__ SolveParams p,
@@ -2532,6 +2541,9 @@ const void* taylor_kernel_fn(int fuse) {
            : fuse == 4 ? reinterpret_cast<const void*>(taylor_kernel<4>)
                        : reinterpret_cast<const void*>(taylor_kernel<2>);
 #endif
+}
+const void* taylor2d_kernel_fn() {
+    return kSolveThreads == 512 ? reinterpret_cast<const void*>(taylor2d_kernel) : nullptr;
 }
 const void* ens_taylor_kernel_fn(int fuse) {
     return fuse == 4 ? reinterpret_cast<const void*>(ens_taylor_kernel<4>)

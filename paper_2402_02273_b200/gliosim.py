@@ -305,6 +305,10 @@ class StencilOperator:
         """True when gs_run takes the small-grid single-cluster path."""
         return bool(self.lib.gs_uses_cluster(self.ctx))
 
+    def uses_flat2d(self) -> bool:
+        """True when the Taylor loop takes the resident-tile 2-D path (cluster-path runs aside)."""
+        return bool(self.lib.gs_uses_flat2d(self.ctx))
+
     def set_kernel_timing(self, enable: bool):
         """CUDA-event timing of every kernel launch of later calls (on the context's stream)."""
         self._check(self.lib.gs_set_kernel_timing(self.ctx, 1 if enable else 0))

@@ -38,10 +38,13 @@ def _oracle(port, shape, h, d, u, steps, rho=0.025):
 
 
 @pytest.mark.parametrize("path,shape", [("tma2", (48, 32, 20)), ("tma3", (48, 32, 20)), ("l1", (40, 24, 18)),
-                                        ("cluster", (32, 32, 32)), ("thin", (64, 48, 1))])
+                                        ("cluster", (32, 32, 32)), ("thin", (64, 48, 1)),
+                                        ("flat2d", (200, 190, 1))])
 def test_repeated_runs_identical(G, port, path, shape, monkeypatch):
     if path != "cluster":
         monkeypatch.setenv("GS_NO_CLUSTER", "1")
+    if path != "flat2d":
+        monkeypatch.setenv("GS_NO_2D", "1")
     if path == "l1":
         monkeypatch.setenv("GS_DISABLE_TMA", "1")
     if path == "tma3":
@@ -51,6 +54,7 @@ def test_repeated_runs_identical(G, port, path, shape, monkeypatch):
     want = _oracle(port, shape, h, d, u0, 3)
     with G.assemble_diffusion(G.Grid(*shape, h=h), d) as op:
         assert op.uses_cluster() == (path == "cluster")
+        assert op.uses_flat2d() == (path == "flat2d")
         for _ in range(REPEATS):
             op.set_state(u0)
             op.run_resident(3, 0.025, 33.5, 1e-8, metrics=True, infos=True)
