@@ -52,6 +52,28 @@ def taylor_bytes_per_voxel(info):
     return BYTES_FIRST_ZERO + BYTES_PER_SWEEP * (sweeps - 1) + BYTES_IMPLICIT * implicit, sweeps, implicit
 
 
+def l2_note(n):
+    ws = 7 * 8 * n / 2 ** 20
+    if ws > 126:
+        return f"working set 7 x {8 * n / 2 ** 20:.0f} MiB fp64 = {ws:.0f} MiB > 126 MB L2 (no flush needed)"
+    return (f"working set {ws:.1f} MiB fits the 126 MB L2: the steps of one run follow each other on the same "
+            "vectors, so a run's steady state IS L2-resident; not flushed between steps (that would time a cold "
+            "start no run has); the roofline fraction against HBM is not meaningful here (SURVEY 8d)")
+
+
+FLAT2D_K = 4  # Taylor terms per round of the resident-tile 2-D kernel (gs_flat2d.cuh, k2dK)
+
+
+def flat2d_bytes_per_voxel(info):
+    """The 2-D resident-tile kernel (taylor2d_kernel): per round (K = 4 terms, one grid barrier)
+    a CTA writes its tile's f after each level and T_K (5 x 8 B per voxel) and reloads one 40 x 40
+    box (12.5 B per tile voxel); the state itself never leaves the SM.  Returns
+    (bytes per voxel, rounds, 0)."""
+    terms = info if isinstance(info, (list, tuple)) else info.stage_terms()
+    rounds = sum((t + FLAT2D_K - 1) // FLAT2D_K for t in terms)
+    return rounds * (8 * (FLAT2D_K + 1) + 8 * 1600 / 1024), rounds, 0
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -365,7 +387,8 @@ def run_ours(args, w, rank, world, local):
     ms_step = ms / args.steps
     value = world * args.steps / (ms / 1e3)
     # roofline of the dominant kernel (taylor_kernel): algorithmic bytes of the fused design
-    tb = [taylor_bytes_per_voxel(infos[q]) for q in range(args.steps)]
+    flat2d = op.uses_flat2d() and not op.uses_cluster()
+    tb = [(flat2d_bytes_per_voxel(infos[q]) if flat2d else taylor_bytes_per_voxel(infos[q])) for q in range(args.steps)]
     taylor_ms, taylor_n = ktimes["taylor"]
     taylor_bytes = w.n * sum(b for b, _, _ in tb)
     achieved = taylor_bytes / (taylor_ms / 1e3) / 1e9
@@ -446,23 +469,29 @@ def run_ours(args, w, rank, world, local):
         "config": {"workload": f"{w.name}: {w.note}", "grid": [w.nx, w.ny, w.nz], "h_mm": w.h, "rho": w.rho,
                    "tau_days": w.tau, "tol": W.TOL, "sigma_vox": w.sigma_vox,
                    "parallelism": f"replicas x{world} (path does not shard)",
-                   "l2": "working set 6x128 MiB fp64 > 126 MB L2 (no flush needed)",
+                   "l2": l2_note(w.n),
                    "s_m": sorted(set(sm)), "terms_per_step": float(np.mean(terms))},
         "taylor_terms_per_s": world * sum(terms) / (ms / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "frac_of_spec_8000GBs": achieved / 8000.0,
-                     "kernel": "gs::taylor_kernel (cooperative; one launch per step, fused two-term sweeps)",
+                     "kernel": ("gs::taylor2d_kernel (cooperative; one launch per step, one resident CTA per 32x32 "
+                                "tile, four terms per grid barrier; L2-resident, latency-bound)" if flat2d else
+                                "gs::taylor_kernel (cooperative; one launch per step, fused two-term sweeps)"),
                      "launches": taylor_n, "avg_launch_ms": taylor_ms / max(taylor_n, 1),
                      "share_of_step": taylor_ms / (pass2_ms if separate else ms),
                      "kernel_timing": ("separate pass of the same K steps inside bench.py (per-kernel events + step "
                                        f"log; {pass2_ms / args.steps:.4f} ms/step); `value` is the production path "
                                        "without them" if separate else "per-kernel events inside the timed region"),
-                     "algorithmic_bytes": ("per voxel: 33 B per fused two-term sweep (25 B stage-0 first sweep) "
-                                           "+ 8 B per stage started from an implicit f = F + T; "
-                                           f"{taylor_bytes / max(taylor_n, 1) / 1e9:.2f} GB per launch, "
-                                           f"{np.mean([x[1] for x in tb]):.1f} sweeps per step, "
-                                           f"{np.mean([x[2] for x in tb]):.1f} of them implicit stage starts"),
+                     "algorithmic_bytes": (("per voxel and round (4 terms): 40 B written (f after each level, T_4) + "
+                                            "12.5 B box reload, all L2; "
+                                            f"{taylor_bytes / max(taylor_n, 1) / 1e9:.2f} GB per launch, "
+                                            f"{np.mean([x[1] for x in tb]):.1f} rounds per step") if flat2d else
+                                           ("per voxel: 33 B per fused two-term sweep (25 B stage-0 first sweep) "
+                                            "+ 8 B per stage started from an implicit f = F + T; "
+                                            f"{taylor_bytes / max(taylor_n, 1) / 1e9:.2f} GB per launch, "
+                                            f"{np.mean([x[1] for x in tb]):.1f} sweeps per step, "
+                                            f"{np.mean([x[2] for x in tb]):.1f} of them implicit stage starts")),
                      "exact_reruns_per_step": float(np.mean([infos[q].reruns for q in range(args.steps)])),
                      "single_term_equivalent_GBs": single_term_equiv,
                      "single_term_note": ("SURVEY 8(d)'s 33 B/voxel per Taylor term over the same time; exceeds the "

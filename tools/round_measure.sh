@@ -14,5 +14,15 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --
 timeout 900 python tools/prof_step.py --config C4 --steps 1 --repeat 2 > gpurun_out/m_prof_plain.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:taylor_kernel -s 1 -c 1 \
     -o gpurun_out/m_taylor python tools/prof_step.py --config C4 --steps 1 --repeat 2 > gpurun_out/m_ncu_full.log 2>&1; echo "full rc=$?"
+# the same capture for the 128^3 Taylor path (C3), the batched ensemble (C5) and the 2-D kernel (C2)
+timeout 600 python tools/prof_step.py --config C3 --steps 1 --repeat 2 > gpurun_out/m_prof_c3.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:taylor_kernel -s 1 -c 1 \
+    -o gpurun_out/m_taylor_c3 python tools/prof_step.py --config C3 --steps 1 --repeat 2 > gpurun_out/m_ncu_c3.log 2>&1; echo "full C3 rc=$?"
+timeout 600 python tools/prof_ens.py > gpurun_out/m_prof_c5.log 2>&1 && \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ens_taylor -s 1 -c 1 \
+    -o gpurun_out/m_taylor_c5 python tools/prof_ens.py > gpurun_out/m_ncu_c5.log 2>&1; echo "full C5 rc=$?"
+timeout 600 python tools/prof_step.py --config C2 --steps 1 --repeat 2 > gpurun_out/m_prof_c2.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:taylor2d -s 1 -c 1 \
+    -o gpurun_out/m_taylor_c2 python tools/prof_step.py --config C2 --steps 1 --repeat 2 > gpurun_out/m_ncu_c2.log 2>&1; echo "full C2 rc=$?"
 bash tools/configs_measure.sh C1 C2 C3 C5 C4x4
 tail -3 gpurun_out/m_tests.log
