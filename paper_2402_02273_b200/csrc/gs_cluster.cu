@@ -1,7 +1,8 @@
 // gs_cluster.cu -- small grids: whole exponential-Euler runs inside one thread-block cluster.
 //
-// For grids whose state fits in the distributed shared memory of one 16-CTA cluster (C1
-// 32^3, C2 256^2: up to ~64 K voxels), the launch sequence of the large-grid path (prep,
+// For grids whose state fits in the distributed shared memory of one 16-CTA cluster (up to
+// 40 K voxels: C1 32^3; C2 256^2 does not fit beside the exact-sum item lists and takes the
+// 2-D resident-tile kernel, gs_flat2d.cuh), the launch sequence of the large-grid path (prep,
 // border, cooperative Taylor, update, each with grid-wide barriers) is replaced by ONE
 // persistent launch that runs every step of gs_run:
 //   * the voxels are split into 16 contiguous slices, one per CTA; every vector of the step
