@@ -603,10 +603,13 @@ template <bool kNeedF, bool kNeedB, class Body>
 __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring, int xbuf, int fbuf, int bbuf,
                                           uint32_t& seq, const double* s_wtab, Body&& body) {
     const StencilOp& op = p.op;
+    // read once (the ensemble kernels' p lives in global memory: see sweep2_tma)
+    const int op_nx = op.nx, op_ny = op.ny, op_nz = op.nz;
+    const int64_t op_sy = op.sy, op_sz = op.sz;
     const int tid = threadIdx.x;
     const int lane = tid & 31, row = tid >> 5;
-    const int tiles_x = (op.nx + kTmaTX - 1) / kTmaTX;
-    const int tiles_y = (op.ny + kTmaTY - 1) / kTmaTY;
+    const int tiles_x = (op_nx + kTmaTX - 1) / kTmaTX;
+    const int tiles_y = (op_ny + kTmaTY - 1) / kTmaTY;
     const CtaWork cw = cta_work();
     const int q_begin = cw.qb, q_end = cw.qe;
     constexpr uint32_t kOwnBytes = kLBytes + (kNeedF ? kOBytes : 0) + (kNeedB ? kOBytes : 0);
@@ -682,14 +685,14 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
             const double* Fo = ring.f(sc);
             const double* Bo = ring.b(sc);
             const uint8_t* Lo = ring.l(sc);
-            const bool hz0 = z > 0, hz1 = z < op.nz - 1;
+            const bool hz0 = z > 0, hz1 = z < op_nz - 1;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const int lx = lxs[c], rw = rws[c];
                 const int i = ii[c], j = jj[c];
-                const bool hy0 = j > 0, hy1 = j < op.ny - 1;
+                const bool hy0 = j > 0, hy1 = j < op_ny - 1;
                 const double xp = Xp[(rw + 1) * kXPitch + lx + kXHalo];
-                if (i < op.nx && j < op.ny) {
+                if (i < op_nx && j < op_ny) {
                     const double xym = Xc[rw * kXPitch + lx + kXHalo];
                     const double xyp = Xc[(rw + 2) * kXPitch + lx + kXHalo];
                     const double xxm = Xc[(rw + 1) * kXPitch + lx + kXHalo - 1];
@@ -698,9 +701,9 @@ __device__ __forceinline__ void sweep_tma(const SolveParams& p, const Ring& ring
                     RowCoef rc;
                     rc.w = s_wtab[Lo[o]];
                     rc.live = rc.w != 0.0;
-                    const int cnt = (i > 0) + (i < op.nx - 1) + hy0 + hy1 + hz0 + hz1;
+                    const int cnt = (i > 0) + (i < op_nx - 1) + hy0 + hy1 + hz0 + hz1;
                     const double acc = row_apply(rc, cnt, xm[c], xym, xxm, xc[c], xxp, xyp, xp);
-                    const int64_t v = i + static_cast<int64_t>(j) * op.sy + static_cast<int64_t>(z) * op.sz;
+                    const int64_t v = i + static_cast<int64_t>(j) * op_sy + static_cast<int64_t>(z) * op_sz;
                     body(v, acc, xc[c], kNeedF ? Fo[o] : 0.0, kNeedB ? Bo[o] : 0.0);
                 }
                 xm[c] = xc[c];
@@ -793,6 +796,11 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
     constexpr int kIssuer = kSolveThreads / 2 + 32;
     static_assert(kIssuer >= kRing && kIssuer < kSolveThreads, "the issuer has no ring point");
     const StencilOp& op = p.op;
+    // The grid extents and strides the z-loop uses, read once: in the ensemble kernel p lives in
+    // global memory and the compiler must otherwise reload them after every store (five LDG per
+    // plane at the head of the dependency chains; long_scoreboard 20% of its stall samples).
+    const int op_nz = op.nz;
+    const int64_t op_sy = op.sy, op_sz = op.sz;
     // dead-row selects only in the exact instantiation (row_apply_ns)
     auto rowap = [](double w, bool live, double negcnt, double a, double b, double c, double d, double e, double f,
                     double g) {
@@ -888,7 +896,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
         const double ncxy1 = -static_cast<double>(cxy + (gy0 + 1 > 0) + (gy0 + 1 < op.ny - 1));
         const int rgx = x0 - 1 + rc, rgy = y0 - 1 + rr;
         const double rncxy = -static_cast<double>((rgx > 0) + (rgx < op.nx - 1) + (rgy > 0) + (rgy < op.ny - 1));
-        const int64_t v0 = gx + static_cast<int64_t>(gy0) * op.sy;
+        const int64_t v0 = gx + static_cast<int64_t>(gy0) * op_sy;
 
         // Phase A: T1 of plane pl.  sm/sc/sp: ring slots of planes pl-1, pl, pl+1.
         // xm/xc/xp: own rows' X at pl-1, pl, pl+1.  Writes T1's shared plane (pl & 1).
@@ -897,7 +905,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
         auto phaseA = [&](int pl, int tslot, int sm_, int sc_, int sp_, const double (&xm)[2], const double (&xc)[2],
                           const double (&xp)[2], double (&t1)[2], double (&lw)[2]) {
             double* T1 = ring.t1(tslot);
-            if (kSkipOut && static_cast<unsigned>(pl) >= static_cast<unsigned>(op.nz)) {
+            if (kSkipOut && static_cast<unsigned>(pl) >= static_cast<unsigned>(op_nz)) {
                 // a plane past the grid (z = -1 or nz): T1 is all zero there -- no stencil work
                 // (2-D grids would otherwise compute three planes per useful one)
                 t1[0] = t1[1] = 0.0;
@@ -909,7 +917,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
 #ifdef GS_EXP_DHZ2
             const double dhz = 2.0;  // timing experiment only
 #else
-            const double dhz = static_cast<double>((pl > 0) + (pl < op.nz - 1));
+            const double dhz = static_cast<double>((pl > 0) + (pl < op_nz - 1));
 #endif
             const double* Xc = ring.x(sc_);
             const uint8_t* L = ring.l(sc_);
@@ -1043,8 +1051,8 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
         double X3[3][2] = {{xa[0], xa[1]}, {xb[0], xb[1]}, {0.0, 0.0}};
         double T3[3][2] = {{tm1[0], tm1[1]}, {t0[0], t0[1]}, {0.0, 0.0}};
         int sM = s1, sA = s2, sB = s3, sC = next_slot(s3);  // slots of planes z-1, z, z+1, z+2
-        double* pT = outT + v0 + static_cast<int64_t>(z0) * op.sz;
-        double* pF = outF + v0 + static_cast<int64_t>(z0) * op.sz;
+        double* pT = outT + v0 + static_cast<int64_t>(z0) * op_sz;
+        double* pF = outF + v0 + static_cast<int64_t>(z0) * op_sz;
         auto iter = [&](int z, auto jconst) {
             constexpr int j = decltype(jconst)::value;  // (z - z0) % 6 (static slots) or % 3
             constexpr int r = j % 3;
@@ -1064,7 +1072,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
 #ifdef GS_EXP_DHZ2
                 const double dhz = 2.0;
 #else
-                const double dhz = static_cast<double>((zo > 0) + (zo < op.nz - 1));
+                const double dhz = static_cast<double>((zo > 0) + (zo < op_nz - 1));
 #endif
                 const double y0m = T1s[oT - kT1Pitch], y1p = T1s[oT + 2 * kT1Pitch];
                 const double a0 = rowap(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), T3[r2][0], y0m, T1s[oT - 1],
@@ -1110,11 +1118,11 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
                     pF[0] = f10;
                 }
                 if (in1) {
-                    pT[op.sy] = t21;
-                    pF[op.sy] = f11;
+                    pT[op_sy] = t21;
+                    pF[op_sy] = f11;
                 }
-                pT += op.sz;
-                pF += op.sz;
+                pT += op_sz;
+                pF += op_sz;
             }
             if (z < z1) {
                 wait_slot(sC);

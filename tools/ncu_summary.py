@@ -44,9 +44,12 @@ def main():
         lines.append(f"{row[si]} | {row[mi]} | {row[vi]} {row[ui]}".rstrip())
     raw = ncu_csv(a.rep, "raw")
     d = dict(zip(raw[0], raw[2]))
-    f = lambda k: float(d[k])  # noqa: E731
+    units = dict(zip(raw[0], raw[1]))  # the raw page scales each metric: Kbyte / Mbyte / Gbyte, us / ms
+    scale = {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3,
+             "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
+    f = lambda k: float(d[k]) * scale.get(units.get(k, ""), 1.0)  # noqa: E731  (GB and ms)
     dur_ms = f("gpu__time_duration.sum")
-    rd, wr = f("dram__bytes_read.sum"), f("dram__bytes_write.sum")  # Gbyte in the raw page
+    rd, wr = f("dram__bytes_read.sum"), f("dram__bytes_write.sum")
     for k in ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
               "lts__t_sector_hit_rate.pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
               "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
