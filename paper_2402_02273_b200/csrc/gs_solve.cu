@@ -2326,7 +2326,9 @@ __device__ __forceinline__ void taylor_body(const SolveParams& p, int border_blo
     if (p.use_tma) fence_proxy_async_global();
 }
 
+#ifndef GS_TILE8  // (the 2-D kernel's thread mapping needs the default 512 threads)
 #include "gs_flat2d.cuh"
+#endif
 
 __global__ void advance_kernel(Ctrl* ctrl) { ctrl->step += 1; }
 
@@ -2402,12 +2404,14 @@ struct GroupBarrier {
     }
 };
 
+#ifndef GS_TILE8
 __global__ void __launch_bounds__(kSolveThreads) taylor2d_kernel(const __grid_constant__ SolveParams p, int border_blocks,
                                                                   int step) {
     vgrid_set(blockIdx.x, gridDim.x);
     cg::grid_group grid = cg::this_grid();
     taylor2d_body(p, border_blocks, step, [&] { grid.sync(); });
 }
+#endif
 
 template <int FUSE>
 __global__ void __launch_bounds__(kSolveThreads, kMinBlocks) taylor_kernel(const __grid_constant__ SolveParams p,
@@ -2551,7 +2555,11 @@ const void* taylor_kernel_fn(int fuse) {
 #endif
 }
 const void* taylor2d_kernel_fn() {
-    return kSolveThreads == 512 ? reinterpret_cast<const void*>(taylor2d_kernel) : nullptr;
+#ifndef GS_TILE8
+    return reinterpret_cast<const void*>(taylor2d_kernel);
+#else
+    return nullptr;
+#endif
 }
 const void* ens_taylor_kernel_fn(int fuse) {
     return fuse == 4 ? reinterpret_cast<const void*>(ens_taylor_kernel<4>)
