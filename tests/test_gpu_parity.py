@@ -334,7 +334,7 @@ TMA_SHAPES = [(48, 32, 20), (80, 40, 12), (64, 48, 1), (32, 32, 32), (16, 16, 16
               (20, 12, 10), (33, 7, 5)]
 
 
-SWEEP_PATHS = ["cluster", "flat2d", "tma2", "tma2exact", "tma2rerun", "tma3", "l1"]
+SWEEP_PATHS = ["cluster", "flat2d", "tma2", "tma2exact", "tma2rerun", "tma2noxchg", "tma3", "l1"]
 # 2-D shapes of the resident-tile path (gs_flat2d.cuh): ragged tiles, x extents TMA cannot
 # describe, one row, one tile, C2's size
 FLAT2D_SHAPES = [(64, 48, 1), (200, 190, 1), (256, 256, 1), (100, 70, 1), (33, 7, 1), (161, 1, 1), (32, 32, 1)]
@@ -346,8 +346,10 @@ def sweep_path_env(path, monkeypatch):
     on every sweep; tma3: fused three-term TMA; l1: the L1 single-term fallback."""
     if path != "cluster":
         monkeypatch.setenv("GS_NO_CLUSTER", "1")
-    if path != "flat2d":
+    if not path.startswith("flat2d"):
         monkeypatch.setenv("GS_NO_2D", "1")
+    if path == "tma2noxchg":  # atomicMax slots + grid barrier instead of the maxima exchange
+        monkeypatch.setenv("GS_NO_XCHG", "1")
     if path == "l1":
         monkeypatch.setenv("GS_DISABLE_TMA", "1")
     if path == "tma3":
@@ -363,7 +365,7 @@ def sweep_path_env(path, monkeypatch):
 CLUSTER_SHAPES = [(32, 32, 32), (16, 16, 16), (64, 48, 1), (24, 17, 16), (33, 7, 18), (20, 12, 40), (80, 16, 24),
                   (40, 30, 24), (200, 190, 1), (161, 1, 1)]
 SWEEP_CASES = ([("cluster", s) for s in CLUSTER_SHAPES] + [("flat2d", s) for s in FLAT2D_SHAPES] +
-               [(p, s) for p in SWEEP_PATHS if p not in ("cluster", "flat2d") for s in TMA_SHAPES])
+               [(p, s) for p in SWEEP_PATHS if p != "cluster" and not p.startswith("flat2d") for s in TMA_SHAPES])
 
 
 @pytest.mark.parametrize("path,shape", SWEEP_CASES)
@@ -380,7 +382,7 @@ def test_sweep_paths_vs_oracle(G, port, shape, path, monkeypatch):
     u = rng.uniform(0, 1, n)
     with G.assemble_diffusion(G.Grid(*shape, h=h), d) as op:
         assert op.uses_cluster() == (path == "cluster"), "shape does not take the path under test"
-        assert op.uses_flat2d() == (path == "flat2d"), "shape does not take the path under test"
+        assert op.uses_flat2d() == path.startswith("flat2d"), "shape does not take the path under test"
         assert np.array_equal(op.apply(x), port.apply(op_o, x))
         got, info = G.step(op, u, 0.1, 33.5, 1e-9, info=True)
         want, log = port.step(op_o, u, 0.1, 33.5, 1e-9, bnorm=info.bnorm, coln=info.coln)
@@ -399,7 +401,7 @@ def test_non_finite_inputs_vs_oracle(G, port, path, monkeypatch):
     norm infinite: numeric_error in both (expact.cpp:90-91).  On the two-term TMA path both
     cases go through the exact-maxima fallback (a non-finite key leaves the bounds open)."""
     sweep_path_env(path, monkeypatch)
-    shape = {"cluster": (24, 16, 16), "flat2d": (80, 48, 1)}.get(path, (48, 32, 12))
+    shape = (24, 16, 16) if path == "cluster" else (80, 48, 1) if path.startswith("flat2d") else (48, 32, 12)
     rng = np.random.default_rng(5)
     n = int(np.prod(shape))
     d = np.array([0.0, 0.13, 0.013, 0.05])[rng.integers(0, 4, n)]
@@ -408,7 +410,7 @@ def test_non_finite_inputs_vs_oracle(G, port, path, monkeypatch):
     x[n // 2 + 7] = np.nan
     with G.assemble_diffusion(G.Grid(*shape, h=2.0), d) as op:
         assert op.uses_cluster() == (path == "cluster")
-        assert op.uses_flat2d() == (path == "flat2d")
+        assert op.uses_flat2d() == path.startswith("flat2d")
         got = G.expmv(2.0, op, x, 1e-10)
         want, _ = port.expmv(2.0, op_o, x, 1e-10)
         assert np.isnan(got).any() and np.isnan(got).sum() < n
