@@ -35,3 +35,31 @@ def test_reference_arm_non_zero_ranks_exit_quietly(ref):
                          env=env)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.strip() == ""
+
+
+def test_algorithmic_byte_models():
+    """The roofline's byte models (pure functions of the step log): the fused two-term sweeps
+    and the 2-D kernel's four-term rounds."""
+    sys.path.insert(0, ROOT)
+    import bench
+    # stages of 5, 4 and 3 terms: 3 + 2 + 2 sweeps; the stage after the 4-term one starts from an
+    # implicit f = F + T
+    b, sweeps, implicit = bench.taylor_bytes_per_voxel([5, 4, 3])
+    assert (sweeps, implicit) == (7, 1)
+    assert b == bench.BYTES_FIRST_ZERO + bench.BYTES_PER_SWEEP * 6 + bench.BYTES_IMPLICIT
+    b2, rounds, _ = bench.flat2d_bytes_per_voxel([12, 11, 4, 1])
+    assert rounds == 3 + 3 + 1 + 1
+    assert b2 == rounds * (8 * 5 + 8 * 1600 / 1024)
+    assert "fits the 126 MB L2" in bench.l2_note(128 ** 3) and "no flush needed" in bench.l2_note(256 ** 3)
+
+
+def test_default_step_counts():
+    """Without --steps the headline config and the reference arm time 10 steps; the small
+    configs their own run length."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2402_02273_b200 import workloads as W
+    for cfg, impl, want in (("C4", "ours", 10), ("C2", "ours", 200), ("C5", "ours", 50), ("C2", "reference", 10)):
+        w = W.get(cfg)
+        steps = 10 if (impl == "reference" or w.n >= 256 ** 3) else w.steps
+        assert steps == want

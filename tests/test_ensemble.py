@@ -133,6 +133,33 @@ def test_batched_ensemble_bitwise_vs_oracle(port, shape, groups):
 
 
 @pytest.mark.gpu
+def test_batched_ensemble_reports_its_taylor_launch_times(port):
+    """Kernel timing on member 0 brackets every step's batched Taylor launch with CUDA events
+    (the C5 bench line's roofline): one launch per step, a positive total, results unchanged."""
+    from paper_2402_02273_b200 import gliosim as G
+    shape, h, tau, tol, steps = (48, 32, 20), 2.0, 33.5, 1e-8, 3
+    members = _random_members(port, shape, 4, 77)
+    ops = [G.assemble_diffusion(G.Grid(*shape, h=h), d) for d, _, _ in members]
+    try:
+        finals = []
+        for timing in (False, True):
+            for op, (_, u0, _) in zip(ops, members):
+                op.set_state(u0)
+            ops[0].set_kernel_timing(timing)
+            G.run_ensemble(ops, steps, [r for _, _, r in members], tau, tol, metrics=False, infos=False, groups=2)
+            if timing:
+                ms, n = ops[0].kernel_times()["taylor"]
+                assert n == steps and ms > 0.0
+            finals.append([op.get_state() for op in ops])
+        ops[0].set_kernel_timing(False)
+        for a, b in zip(*finals):
+            assert np.array_equal(a, b)
+    finally:
+        for op in ops:
+            op.close()
+
+
+@pytest.mark.gpu
 def test_batched_ensemble_matches_sequential_runs(port, monkeypatch):
     """The batched ensemble against the same members run one after another (gs_run each): the
     same terms per stage, states equal up to the ulps of the per-CTA partial sums."""
