@@ -463,11 +463,11 @@ gs_status setup_solve(gs_ctx* c, gs::SolveParams& p, int gb, int sb, int n_steps
     GS_CUDA(c, c->part_b.alloc(sizeof(double) * pb));
     GS_CUDA(c, c->part_c.alloc(sizeof(double) * pb));
     GS_CUDA(c, c->part_u.alloc(sizeof(double) * pb));
-    GS_CUDA(c, c->slots.alloc(sizeof(unsigned long long) * 24));
+    GS_CUDA(c, c->slots.alloc(sizeof(unsigned long long) * gs::kSlotWords));
     GS_CUDA(c, c->mslots.alloc(sizeof(unsigned long long) * 4));
     const bool fresh_ctrl = c->ctrl.p == nullptr;
     GS_CUDA(c, c->ctrl.alloc(sizeof(gs::Ctrl)));
-    GS_CUDA(c, cudaMemsetAsync(c->slots.p, 0, sizeof(unsigned long long) * 24, c->stream));
+    GS_CUDA(c, cudaMemsetAsync(c->slots.p, 0, sizeof(unsigned long long) * gs::kSlotWords, c->stream));
     GS_CUDA(c, c->xchg.alloc(sizeof(unsigned long long) * gs::kXchgWords));
     GS_CUDA(c, cudaMemsetAsync(c->xchg.p, 0, sizeof(unsigned long long) * gs::kXchgWords, c->stream));
     const unsigned long long ms_init[4] = {0ull, ~0ull, 0ull, 0ull};

@@ -24,7 +24,7 @@
 // The result f is written to F0 (ctrl->fres = F0, explicit).
 #pragma once
 
-__shared__ unsigned long long s_max2d[8];  // block maxima of a round
+__shared__ unsigned long long s_max2d[2 * k2dK];  // block maxima of a round
 #ifdef GS_2D_PROF
 __shared__ long long s_prof[10];
 #define PROF(k)                           \
@@ -40,7 +40,7 @@ __shared__ long long s_prof[10];
 constexpr int k2dT = 32;               // tile edge
 constexpr int k2dP = k2dT + 2 * k2dK;  // box edge and pitch (doubles): tile + halo K
 constexpr int k2dBox = k2dP * k2dP;
-static_assert(k2dK >= 2 && k2dK <= 4, "2K maxima must fit the eight slots of a round");
+static_assert(k2dK >= 2 && 2 * k2dK <= kSlots2d, "2K maxima must fit the slots of a round");
 static_assert(k2dSmemBytes == (k2dK + 3) * k2dBox * 8, "flat 2-D shared memory");
 
 template <class GridBar>
@@ -126,7 +126,7 @@ __device__ __forceinline__ void taylor2d_body(const SolveParams& p, int border_b
         NCS[e] = __dsub_rn(-static_cast<double>(cnt), 0.0);  // the TMA sweep's ncxy - dhz with dhz = 0
         XS[e] = 0.0;
     }
-    if (tid < 8) s_max2d[tid] = 0ull;
+    if (tid < 2 * k2dK) s_max2d[tid] = 0ull;
     const int64_t N = op.n;
     // Thread t owns tile column xl and rows ry0, ry0 + 1 for the whole launch (their f and the
     // current term stay in registers, w and -cnt too); at level k < K the first n_k - 1024
@@ -136,25 +136,28 @@ __device__ __forceinline__ void taylor2d_body(const SolveParams& p, int border_b
     const int gxo = x0 + xl, gyo = y0 + ry0;
     const bool inA = gxo < nx && gyo < ny, inB = gxo < nx && gyo + 1 < ny;
     const int64_t vA = gxo + static_cast<int64_t>(gyo) * nx;
-    int oR[k2dK - 1];
+    constexpr int kRimPer = ((k2dP - 2) * (k2dP - 2) - k2dT * k2dT + kSolveThreads - 1) / kSolveThreads;
+    int oR[k2dK - 1][kRimPer];
 #pragma unroll
     for (int k = 1; k < k2dK; ++k) {
         const int h = k2dK - k, wk = k2dP - 2 * k;
-        int j = tid, r = -1, c = -1;
-        if (j < h * wk) {  // rows above the tile
-            r = k + j / wk;
-            c = k + j % wk;
-        } else if ((j -= h * wk) < h * wk) {  // rows below
-            r = k2dK + k2dT + j / wk;
-            c = k + j % wk;
-        } else if ((j -= h * wk) < 2 * h * k2dT) {  // columns left and right of the tile
-            r = k2dK + j / (2 * h);
-            const int cc = j % (2 * h);
-            c = cc < h ? k + cc : k2dK + k2dT + (cc - h);
+#pragma unroll
+        for (int i = 0; i < kRimPer; ++i) {
+            int j = tid + i * kSolveThreads, r = -1, c = -1;
+            if (j < h * wk) {  // rows above the tile
+                r = k + j / wk;
+                c = k + j % wk;
+            } else if ((j -= h * wk) < h * wk) {  // rows below
+                r = k2dK + k2dT + j / wk;
+                c = k + j % wk;
+            } else if ((j -= h * wk) < 2 * h * k2dT) {  // columns left and right of the tile
+                r = k2dK + j / (2 * h);
+                const int cc = j % (2 * h);
+                c = cc < h ? k + cc : k2dK + k2dT + (cc - h);
+            }
+            oR[k - 1][i] = r >= 0 ? r * k2dP + c : -1;
         }
-        oR[k - 1] = r >= 0 ? r * k2dP + c : -1;
     }
-    static_assert((k2dP - 2) * (k2dP - 2) - k2dT * k2dT <= kSolveThreads, "one rim point per thread");
     // the box of `src` (global, L2) into registers, then into X (and f: a stage starts from f)
     constexpr int kBoxIt = (k2dBox + kSolveThreads - 1) / kSolveThreads;
     auto fetch_box = [&](const double* src, double (&xr)[kBoxIt]) {
@@ -227,9 +230,13 @@ __device__ __forceinline__ void taylor2d_body(const SolveParams& p, int border_b
                 if (k < k2dK) {
                     dst[oA] = nA;
                     dst[oB] = nB;
-                    const int o = oR[k < k2dK ? k - 1 : 0];
-                    if (o >= 0)
-                        dst[o] = term(o, WS[o], NCS[o], zero ? 0.0 : src[o - k2dP], zero ? 0.0 : src[o], zero ? 0.0 : src[o + k2dP]);
+#pragma unroll
+                    for (int i = 0; i < kRimPer; ++i) {
+                        const int o = oR[k < k2dK ? k - 1 : 0][i];
+                        if (o >= 0)
+                            dst[o] = term(o, WS[o], NCS[o], zero ? 0.0 : src[o - k2dP], zero ? 0.0 : src[o],
+                                          zero ? 0.0 : src[o + k2dP]);
+                    }
                 }
                 tA = nA;
                 tB = nB;
@@ -265,7 +272,7 @@ __device__ __forceinline__ void taylor2d_body(const SolveParams& p, int border_b
                 __syncthreads();
                 if (tid < 2 * k2dK) {
                     const unsigned long long v = s_max2d[tid];
-                    if (v) atomicMax(p.slots + (round % 3) * 8 + tid, v);
+                    if (v) atomicMax(p.slots + kSlots2dBase + (round % 3) * kSlots2d + tid, v);
                     s_max2d[tid] = 0ull;  // for the next round (barriers in between)
                 }
                 PROF(2)
@@ -273,11 +280,11 @@ __device__ __forceinline__ void taylor2d_body(const SolveParams& p, int border_b
                 PROF(3)
                 trace_mark(p, kind == k2Next ? kTrFusedNext : kTrFusedFirst);
                 if (leader) {
-                    unsigned long long* z = p.slots + ((round + 2) % 3) * 8;
+                    unsigned long long* z = p.slots + kSlots2dBase + ((round + 2) % 3) * kSlots2d;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) z[q] = 0ull;
+                    for (int q = 0; q < kSlots2d; ++q) z[q] = 0ull;
                 }
-                const unsigned long long* sl = p.slots + (round % 3) * 8;
+                const unsigned long long* sl = p.slots + kSlots2dBase + (round % 3) * kSlots2d;
 #pragma unroll
                 for (int q = 0; q < 2 * k2dK; ++q) mx[q] = slot_read(sl + q);
                 ++round;

@@ -206,7 +206,7 @@ struct SolveParams {
     int* seq_counts;
     int seq_tiles;
     int seq_exact;          // 1: the two sums are the reference's sequential ones; 0: tree sums (A/B)
-    unsigned long long* slots;   // [3][8] rotating max slots for per-term reductions
+    unsigned long long* slots;   // [3][8] rotating max slots for per-term reductions (+ the 2-D kernel's: kSlotWords)
     unsigned long long* mslots;  // [2][4] metric max/min/r2 slots (step parity)
     // Bounded two-term sweeps: the per-sweep maxima exchange that is also the sweep's grid
     // barrier (xchg_keys4; kXchgWords words cleared per run; nullptr: atomicMax slots + grid barrier)
@@ -294,7 +294,9 @@ const void* taylor_kernel_fn(int fuse);
 #ifndef GS_2D_K
 #define GS_2D_K 4
 #endif
-constexpr int k2dK = GS_2D_K;  // Taylor terms per round (one grid barrier): 2..4
+constexpr int k2dK = GS_2D_K;  // Taylor terms per round (one grid barrier): 2..6
+// max slots: [3][8] of the sweeps, then [3][kSlots2d] of the 2-D kernel's rounds (2K maxima each)
+constexpr int kSlots2dBase = 24, kSlots2d = 16, kSlotWords = kSlots2dBase + 3 * kSlots2d;
 constexpr int k2dSmemBytes = (k2dK + 3) * (32 + 2 * k2dK) * (32 + 2 * k2dK) * 8;
 const void* taylor2d_kernel_fn();
 __global__ void update_kernel(const __grid_constant__ SolveParams p, int step);

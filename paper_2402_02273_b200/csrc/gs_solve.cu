@@ -2343,7 +2343,7 @@ __device__ __forceinline__ void update_body(const SolveParams& p, int step) {
     // The Taylor kernel leaves its last round's maxima in one rotating slot; the next step's
     // first rounds expect all three slots zero (their atomicMax would otherwise see the stale
     // ||f|| of the previous step's last sweep).  The Taylor kernel has finished: stream order.
-    if (vcta() == 0 && threadIdx.x < 24) p.slots[threadIdx.x] = 0ull;
+    if (vcta() == 0 && threadIdx.x < kSlotWords) p.slots[threadIdx.x] = 0ull;
     if (__ldcg(&ctrl->status)) return;
     trace_mark(p, kTrUpdateIn);
     const int branch = __ldcg(&ctrl->branch);
