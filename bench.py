@@ -52,6 +52,19 @@ def taylor_bytes_per_voxel(info):
     return BYTES_FIRST_ZERO + BYTES_PER_SWEEP * (sweeps - 1) + BYTES_IMPLICIT * implicit, sweeps, implicit
 
 
+def timed_launches(op, steps, graph_pass):
+    """Kernels of this library launched inside the timed region (gs_capi.cu launch_solve): the
+    single-cluster path is one launch per call; otherwise one metrics launch, then per step prep,
+    border, Taylor, update, the tile and item pass of each of the two exact sums (seqsum) and,
+    in the graph-replayed production pass, the one-thread step counter."""
+    if op.uses_cluster():
+        return 1
+    per_step = 4 + (0 if os.environ.get("GS_TREE_SUMS") else 4)
+    if graph_pass and steps >= 2 and not os.environ.get("GS_NO_GRAPH"):
+        per_step += 1
+    return steps * per_step + 1
+
+
 def l2_note(n):
     ws = 7 * 8 * n / 2 ** 20
     if ws > 126:
@@ -501,7 +514,7 @@ def run_ours(args, w, rank, world, local):
                                           "HBM peak because each sweep applies two terms per pass (temporal blocking)")},
         "step_bytes_per_s_GBs": step_bytes / (ms / 1e3) / 1e9,
         "kernel_ms": {k: v[0] / args.steps for k, v in ktimes.items()},
-        "gpu_launches": sum(v[1] for v in ktimes.values()) + (1 if args.steps else 0),
+        "gpu_launches": timed_launches(op, args.steps, separate),
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
@@ -646,7 +659,9 @@ def run_ensemble(args, w, rank, world, local):
                    "terms_per_member_step": float(terms.mean()),
                    "rho_range": [float(min(runner.rhos)), float(max(runner.rhos))] if world == 1 else None,
                    "l2": "64 resident members x 7 x 16 MiB >> L2"},
-        "gpu_launches": (5 * args.steps + 1) if not os.environ.get("GS_ENS_SEQUENTIAL")
+        # per batched step: prep, border, order, Taylor, update and the two passes of each exact sum
+        "gpu_launches": ((5 if os.environ.get("GS_TREE_SUMS") else 9) * args.steps + 1)
+        if not os.environ.get("GS_ENS_SEQUENTIAL")
         else 4 * len(members) * args.steps + len(members),
         "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
         "metrics_all_finite": bool(np.isfinite(table).all()),
