@@ -914,11 +914,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
                 if (ringer) T1[rT] = 0.0;
                 return;
             }
-#ifdef GS_EXP_DHZ2
-            const double dhz = 2.0;  // timing experiment only
-#else
             const double dhz = static_cast<double>((pl > 0) + (pl < op_nz - 1));
-#endif
             const double* Xc = ring.x(sc_);
             const uint8_t* L = ring.l(sc_);
             const double* B = ring.b(sc_);
@@ -948,12 +944,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
             t1[1] = v1_;
             T1[oT] = v0_;
             T1[oT + kT1Pitch] = v1_;
-#ifdef GS_EXP_NORING
-            if (ringer) T1[rT] = 0.0;  // timing experiment only: WRONG results
-            if (false) {
-#else
             if (ringer) {
-#endif
                 const double w = s_wtab[L[rL]];
                 double sc;
                 if (KIND == k2FirstZero) {
@@ -1069,11 +1060,7 @@ __device__ __forceinline__ void sweep2_tma(const SolveParams& p, const R& ring, 
                 const double* T1s = ring.t1(r);  // plane zo = z - 1: slot (z - z0) % 3
                 const uint8_t* L = ring.l(sM);
                 const double w0 = s_wtab[L[oL]], w1 = s_wtab[L[oL + kLPitch]];
-#ifdef GS_EXP_DHZ2
-                const double dhz = 2.0;
-#else
                 const double dhz = static_cast<double>((zo > 0) + (zo < op_nz - 1));
-#endif
                 const double y0m = T1s[oT - kT1Pitch], y1p = T1s[oT + 2 * kT1Pitch];
                 const double a0 = rowap(w0, w0 != 0.0, __dsub_rn(ncxy0, dhz), T3[r2][0], y0m, T1s[oT - 1],
                                                T3[r][0], T1s[oT + 1], T3[r][1], T3[r1][0]);
