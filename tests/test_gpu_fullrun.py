@@ -73,7 +73,8 @@ def test_full_run_matches_reference(name, steps, port, ref):
         center = W.seed_points(w, labels)[0]
         rec = FR.full_run_parity(name, op, labels, u0, steps, w.rho, w.tau, W.TOL, center, port, ref)
         rec["material_map_equal"] = True
-        rec["path"] = "single-cluster" if op.uses_cluster() else "multi-kernel"
+        rec["path"] = ("single-cluster" if op.uses_cluster() else
+                       "resident tiles (2-D)" if op.uses_flat2d() else "multi-kernel")
         _save(rec)
         FR.assert_record(rec)
     finally:

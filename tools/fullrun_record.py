@@ -33,7 +33,9 @@ tic = time.perf_counter()
 want = ref.resample(data, dims[0], dims[1], dims[2], (w.nx, w.ny, w.nz))
 labels = op.labels()
 rec = dict(tool="tools/fullrun_record.py", host_cores=FR.host_cores(),
-           material_map_equal=labels.tobytes() == want.tobytes())
+           material_map_equal=labels.tobytes() == want.tobytes(),
+           path=("single-cluster" if op.uses_cluster() else
+                 "resident tiles (2-D)" if op.uses_flat2d() else "multi-kernel"))
 u0 = bench.initial_state(w, op, labels)
 center = W.seed_points(w, labels)[0]
 FR.full_run_parity(a.config, op, labels, u0, a.steps, w.rho, w.tau, W.TOL, center, port, ref, record=rec,
